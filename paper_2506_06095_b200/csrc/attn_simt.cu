@@ -1,0 +1,270 @@
+// attn_simt.cu — CUDA-core attention executors.
+//
+// attn_rowwise: replaces rowwise_sdpa (attention.hpp:177-213). One warp per (b, h, query row),
+//   split into 4 groups of 8 lanes; each group handles one gathered key at a time, so a K/V row
+//   of d fp16 is read by 8 lanes with 16-byte vector loads (coalesced 128-byte row for d=64).
+//   Per-group online softmax in fp32, merged across the 4 groups with shuffles at the end.
+//
+// attn_bsr_generic: the block-skipping executor (attention.hpp:71-172) for ANY tile shape the
+//   reference accepts (the tcgen05 kernel in attn_tc.cu covers block_m = 128). One CTA per
+//   (row block, b*h); one thread per query row; K/V tiles staged through shared memory; the
+//   per-load-entry tile id (-1 = full) replaces the merge walk.
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace sf {
+namespace {
+
+template <typename T>
+__device__ __forceinline__ void load8(const T* p, float* f) {
+    // 8 consecutive 16-bit elements -> fp32 (16-byte aligned vector load)
+    const uint4 raw = *reinterpret_cast<const uint4*>(p);
+    const T* h = reinterpret_cast<const T*>(&raw);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) f[e] = DT<T>::to_f(h[e]);
+}
+
+// DPL = dims per lane (ceil(d / 8)); VEC = 16-byte vector loads (d % 64 == 0, aligned strides).
+template <typename T, int DPL, bool VEC>
+__global__ void __launch_bounds__(256) attn_rowwise_kernel(sf_attn_args a, const int32_t* __restrict__ row_ptr,
+                                                           const int32_t* __restrict__ col_idx) {
+    const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t rows = static_cast<int64_t>(a.bs) * a.h * a.seq_len;
+    if (gw >= rows) return;
+    const int lane = threadIdx.x & 31, grp = lane >> 3, gl = lane & 7;
+    const int64_t i = gw % a.seq_len;
+    const int64_t bh = gw / a.seq_len;
+    const int64_t b = bh / a.h, hh = bh % a.h;
+    const T* Q = static_cast<const T*>(a.q) + b * a.q_sb + hh * a.q_sh;
+    const T* K = static_cast<const T*>(a.k) + b * a.q_sb + hh * a.q_sh;
+    const T* V = static_cast<const T*>(a.v) + b * a.q_sb + hh * a.q_sh;
+    T* O = static_cast<T*>(a.o) + b * a.o_sb + hh * a.o_sh + i * a.o_sn;
+    const int d = a.head_size;
+    const int d0 = gl * DPL;
+    const float sl2 = a.scale * 1.4426950408889634f;
+    float q[DPL], acc[DPL];
+#pragma unroll
+    for (int e = 0; e < DPL; ++e) {
+        q[e] = (d0 + e < d) ? DT<T>::to_f(Q[i * a.q_sn + d0 + e]) : 0.f;
+        acc[e] = 0.f;
+    }
+    float m = -INFINITY, l = 0.f;
+    const int32_t r0 = row_ptr[i], r1 = row_ptr[i + 1];
+    for (int32_t kk = r0 + grp; kk < r1; kk += 4) {
+        const int64_t j = col_idx[kk];
+        float kv[DPL];
+        if constexpr (VEC) {
+#pragma unroll
+            for (int e = 0; e < DPL; e += 8) load8(K + j * a.q_sn + d0 + e, kv + e);
+        } else {
+#pragma unroll
+            for (int e = 0; e < DPL; ++e) kv[e] = (d0 + e < d) ? DT<T>::to_f(K[j * a.q_sn + d0 + e]) : 0.f;
+        }
+        float dot = 0.f;
+#pragma unroll
+        for (int e = 0; e < DPL; ++e) dot += q[e] * kv[e];
+        dot += __shfl_xor_sync(0xffffffffu, dot, 1);
+        dot += __shfl_xor_sync(0xffffffffu, dot, 2);
+        dot += __shfl_xor_sync(0xffffffffu, dot, 4);
+        const float s = dot * sl2;  // log2-domain score
+        const float mn = fmaxf(m, s);
+        const float alpha = exp2f(m - mn);  // m == -inf -> 0
+        const float p = exp2f(s - mn);
+        l = l * alpha + p;
+        if constexpr (VEC) {
+#pragma unroll
+            for (int e = 0; e < DPL; e += 8) load8(V + j * a.q_sn + d0 + e, kv + e);
+        } else {
+#pragma unroll
+            for (int e = 0; e < DPL; ++e) kv[e] = (d0 + e < d) ? DT<T>::to_f(V[j * a.q_sn + d0 + e]) : 0.f;
+        }
+#pragma unroll
+        for (int e = 0; e < DPL; ++e) acc[e] = acc[e] * alpha + p * kv[e];
+        m = mn;
+    }
+    // merge the 4 groups (lanes gl, gl+8, gl+16, gl+24 hold the same dims)
+#pragma unroll
+    for (int o = 8; o < 32; o <<= 1) {
+        const float m2 = __shfl_xor_sync(0xffffffffu, m, o);
+        const float l2 = __shfl_xor_sync(0xffffffffu, l, o);
+        const float mn = fmaxf(m, m2);
+        const float a1 = (m == -INFINITY) ? 0.f : exp2f(m - mn);
+        const float a2 = (m2 == -INFINITY) ? 0.f : exp2f(m2 - mn);
+#pragma unroll
+        for (int e = 0; e < DPL; ++e) {
+            const float x2 = __shfl_xor_sync(0xffffffffu, acc[e], o);
+            acc[e] = acc[e] * a1 + x2 * a2;
+        }
+        l = l * a1 + l2 * a2;
+        m = mn;
+    }
+    if (grp == 0) {
+        const float inv = l > 0.f ? 1.f / l : 0.f;  // rows without valid columns stay zero
+#pragma unroll
+        for (int e = 0; e < DPL; ++e)
+            if (d0 + e < d) O[d0 + e] = DT<T>::from_f(acc[e] * inv);
+    }
+}
+
+// Generic block executor. DM = max head size handled (template), BN_MAX staged columns.
+template <typename T, int DM>
+__global__ void attn_bsr_generic_kernel(sf_attn_args a, sf_bsr_dev bsr) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int bm = bsr.block_m, bn = bsr.block_n, d = a.head_size;
+    T* Ks = reinterpret_cast<T*>(smem_raw);
+    T* Vs = Ks + static_cast<size_t>(bn) * d;
+    const int64_t br = blockIdx.x;
+    const int64_t bh = blockIdx.y;
+    const int64_t b = bh / a.h, hh = bh % a.h;
+    const int n = a.seq_len;
+    const T* Q = static_cast<const T*>(a.q) + b * a.q_sb + hh * a.q_sh;
+    const T* K = static_cast<const T*>(a.k) + b * a.q_sb + hh * a.q_sh;
+    const T* V = static_cast<const T*>(a.v) + b * a.q_sb + hh * a.q_sh;
+    T* O = static_cast<T*>(a.o) + b * a.o_sb + hh * a.o_sh;
+    const int r = threadIdx.x;
+    const int64_t i = br * bm + r;
+    const bool active = r < bm && i < n;
+    const float sl2 = a.scale * 1.4426950408889634f;
+    float q[DM], acc[DM];
+#pragma unroll
+    for (int e = 0; e < DM; ++e) {
+        q[e] = (active && e < d) ? DT<T>::to_f(Q[i * a.q_sn + e]) : 0.f;
+        acc[e] = 0.f;
+    }
+    float m = -INFINITY, l = 0.f;
+    const int32_t l0 = bsr.load_row_ptr[br], l1 = bsr.load_row_ptr[br + 1];
+    for (int32_t lk = l0; lk < l1; ++lk) {
+        const int64_t j0 = static_cast<int64_t>(bsr.load_col_idx[lk]) * bn;
+        const int cols = static_cast<int>(imin64(bn, n - j0));
+        const int32_t tid = bsr.load_tile[lk];
+        __syncthreads();
+        for (int t = threadIdx.x; t < cols * d; t += blockDim.x) {
+            const int c = t / d, e = t - c * d;
+            Ks[t] = K[(j0 + c) * a.q_sn + e];
+            Vs[t] = V[(j0 + c) * a.q_sn + e];
+        }
+        __syncthreads();
+        if (!active) continue;
+        const uint8_t* tile = tid < 0 ? nullptr : bsr.pool + static_cast<int64_t>(tid) * bsr.tile_bytes;
+        // tile max over valid columns, then rescale once per tile (attention.hpp:136-157)
+        float tmax = -INFINITY;
+        for (int c = 0; c < cols; ++c) {
+            if (tile) {
+                const int bit = r * bn + c;
+                if (!((tile[bit >> 3] >> (bit & 7)) & 1)) continue;
+            }
+            float dot = 0.f;
+#pragma unroll
+            for (int e = 0; e < DM; ++e)
+                if (e < d) dot += q[e] * DT<T>::to_f(Ks[c * d + e]);
+            tmax = fmaxf(tmax, dot * sl2);
+        }
+        const float mn = fmaxf(m, tmax);
+        if (mn == -INFINITY) continue;
+        const float alpha = exp2f(m - mn);
+        l *= alpha;
+#pragma unroll
+        for (int e = 0; e < DM; ++e) acc[e] *= alpha;
+        for (int c = 0; c < cols; ++c) {
+            if (tile) {
+                const int bit = r * bn + c;
+                if (!((tile[bit >> 3] >> (bit & 7)) & 1)) continue;
+            }
+            float dot = 0.f;
+#pragma unroll
+            for (int e = 0; e < DM; ++e)
+                if (e < d) dot += q[e] * DT<T>::to_f(Ks[c * d + e]);
+            const float p = exp2f(dot * sl2 - mn);
+            l += p;
+#pragma unroll
+            for (int e = 0; e < DM; ++e)
+                if (e < d) acc[e] += p * DT<T>::to_f(Vs[c * d + e]);
+        }
+        m = mn;
+    }
+    if (active) {
+        const float inv = l > 0.f ? 1.f / l : 0.f;
+#pragma unroll
+        for (int e = 0; e < DM; ++e)
+            if (e < d) O[i * a.o_sn + e] = DT<T>::from_f(acc[e] * inv);
+    }
+}
+
+template <typename T, int DPL, bool VEC = false>
+sf_status launch_rowwise(const sf_attn_args& a, const sf_csr_dev& c, cudaStream_t st) {
+    const int64_t warps = static_cast<int64_t>(a.bs) * a.h * a.seq_len;
+    attn_rowwise_kernel<T, DPL, VEC><<<static_cast<unsigned>(ceil_div(warps * 32, 256)), 256, 0, st>>>(a, c.row_ptr,
+                                                                                                  c.col_idx);
+    SF_LAUNCH_CHECK();
+    return SF_OK;
+}
+
+template <typename T>
+sf_status rowwise_dispatch(const sf_attn_args& a, const sf_csr_dev& c, cudaStream_t st) {
+    const int d = a.head_size;
+    const bool vec = (d % 64 == 0) && (a.q_sn % 8 == 0) && (a.q_sb % 8 == 0) && (a.q_sh % 8 == 0) &&
+                     (reinterpret_cast<uintptr_t>(a.k) % 16 == 0) && (reinterpret_cast<uintptr_t>(a.v) % 16 == 0);
+    if (d == 64 && vec) return launch_rowwise<T, 8, true>(a, c, st);
+    if (d == 128 && vec) return launch_rowwise<T, 16, true>(a, c, st);
+    if (d <= 8) return launch_rowwise<T, 1>(a, c, st);
+    if (d <= 16) return launch_rowwise<T, 2>(a, c, st);
+    if (d <= 32) return launch_rowwise<T, 4>(a, c, st);
+    if (d <= 64) return launch_rowwise<T, 8>(a, c, st);
+    if (d <= 128) return launch_rowwise<T, 16>(a, c, st);
+    return fail(SF_SHAPE_ERROR, "row-wise kernel supports head_size <= 128");
+}
+
+template <typename T, int DM>
+sf_status launch_generic(const sf_attn_args& a, const sf_bsr_dev& b, cudaStream_t st) {
+    const int threads = static_cast<int>(imax64(32, ceil_div(b.block_m, 32) * 32));
+    if (threads > 1024) return fail(SF_PLAN_ERROR, "generic block kernel supports block_m <= 1024");
+    const size_t smem = static_cast<size_t>(b.block_n) * a.head_size * sizeof(T) * 2;
+    if (smem > 200 * 1024) return fail(SF_PLAN_ERROR, "tile too large for shared memory");
+    auto k = attn_bsr_generic_kernel<T, DM>;
+    if (smem > 48 * 1024) SF_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    dim3 grid(b.n_rows, static_cast<unsigned>(a.bs) * a.h);
+    k<<<grid, threads, smem, st>>>(a, b);
+    SF_LAUNCH_CHECK();
+    return SF_OK;
+}
+
+template <typename T>
+sf_status generic_dispatch(const sf_attn_args& a, const sf_bsr_dev& b, cudaStream_t st) {
+    const int d = a.head_size;
+    if (d <= 8) return launch_generic<T, 8>(a, b, st);
+    if (d <= 16) return launch_generic<T, 16>(a, b, st);
+    if (d <= 32) return launch_generic<T, 32>(a, b, st);
+    if (d <= 64) return launch_generic<T, 64>(a, b, st);
+    if (d <= 128) return launch_generic<T, 128>(a, b, st);
+    return fail(SF_SHAPE_ERROR, "block kernel supports head_size <= 128");
+}
+
+}  // namespace
+
+sf_status check_attn_args(const sf_attn_args& a) {
+    if (a.bs < 1 || a.h < 1 || a.seq_len < 1 || a.head_size < 1)
+        return fail(SF_SHAPE_ERROR, "empty attention input");                    // tensor.hpp:47
+    if (!a.q || !a.k || !a.v || !a.o) return fail(SF_INVALID_PARAMETER, "null tensor pointer");
+    if (a.dtype != SF_F16 && a.dtype != SF_BF16) return fail(SF_INVALID_PARAMETER, "dtype must be f16/bf16");
+    return SF_OK;
+}
+
+sf_status attn_generic(const sf_attn_args& a, const sf_bsr_dev& b, cudaStream_t st) {
+    return a.dtype == SF_F16 ? generic_dispatch<__half>(a, b, st) : generic_dispatch<__nv_bfloat16>(a, b, st);
+}
+
+}  // namespace sf
+
+using namespace sf;
+
+extern "C" sf_status sf_mha_rowwise(const sf_attn_args* args, const sf_csr_dev* csr, void* stream) {
+    if (!args || !csr) return fail(SF_INVALID_PARAMETER, "null argument");
+    SF_TRY(check_attn_args(*args));
+    if (csr->seq_len != args->seq_len)
+        return fail(SF_SHAPE_ERROR, "rowwise mask seq_len differs from input");   // attention.hpp:179
+    sf_attn_args a = *args;
+    if (a.scale == 0.f) a.scale = 1.0f / sqrtf(static_cast<float>(a.head_size));
+    cudaStream_t st = as_stream(stream);
+    return a.dtype == SF_F16 ? rowwise_dispatch<__half>(a, *csr, st) : rowwise_dispatch<__nv_bfloat16>(a, *csr, st);
+}

@@ -1,0 +1,537 @@
+// formats.cu — device builders for the storage formats, bit-exact with the reference.
+//   sf_bsr_build     <- build_bsr     (bsr.hpp:47-101)
+//   sf_rowwise_build <- build_rowwise (bsr.hpp:198-209)
+//
+// BSR pipeline (all stream-ordered; two small D2H syncs to size the outputs):
+//   1. classify: one warp per tile; lanes walk the tile's rows, extract the bn-bit row slices
+//      from the bit mask (cells past n read as 0, bsr.hpp:72), popcount -> empty/full/part,
+//      and fold a 64-bit content hash (row index mixed in, so the fold is order-free).
+//   2. per-tile-row counts -> single-CTA exclusive scans -> full/part/load row pointers.
+//   3. compaction: one CTA per tile row; a block-wide scan of the full/part flags writes the
+//      column lists in ascending column order (bsr.hpp:64-65 loop order).
+//   4. dedup: open-addressing table keyed by content (hash compared first, then the tile bits
+//      themselves); each slot keeps the MIN row-major tile index of its content via atomicMin.
+//      A part entry whose own tile index equals its slot's minimum is a first occurrence.
+//   5. exclusive scan of the first-occurrence flags over the row-major part list = pool ids in
+//      first-occurrence order (bsr.hpp:84-88); ids are scattered back through the slots.
+//   6. pool: one warp per distinct tile writes pack_bits(tile) (common.hpp:77-83).
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "common.cuh"
+#include "scan.cuh"
+
+namespace sf {
+namespace {
+
+struct Geo {
+    int32_t n, words, bm, bn, n_rows, n_cols;
+};
+
+// Content hash + popcount of tile (br, bc); executed by one full warp.
+__device__ __forceinline__ void tile_scan(const uint32_t* __restrict__ bits, const Geo& g,
+                                          int64_t br, int64_t bc, int64_t* count_out,
+                                          uint64_t* hash_out) {
+    const int lane = threadIdx.x & 31;
+    int64_t cnt = 0;
+    uint64_t h = 0;
+    const int64_t j0 = bc * g.bn;
+    const int64_t jlim = imin64(g.n, j0 + g.bn);
+    for (int di = lane; di < g.bm; di += 32) {
+        const int64_t i = br * g.bm + di;
+        if (i >= g.n) continue;
+        const uint32_t* row = bits + i * g.words;
+        for (int64_t c = 0; c * 64 < g.bn; ++c) {
+            const uint64_t v = row_bits64(row, j0 + 64 * c, jlim);
+            cnt += __popcll(v);
+            h += mix64(v ^ (0x9e3779b97f4a7c15ull * static_cast<uint64_t>(di * 1024 + c + 1)));
+        }
+    }
+    for (int o = 16; o; o >>= 1) {
+        cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+        h += __shfl_xor_sync(0xffffffffu, h, o);
+    }
+    *count_out = cnt;
+    *hash_out = h;
+}
+
+// cls: 0 empty, 1 full, 2 part
+__global__ void classify_kernel(const uint32_t* __restrict__ bits, Geo g, uint8_t* __restrict__ cls,
+                                uint64_t* __restrict__ hash) {
+    const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t tiles = static_cast<int64_t>(g.n_rows) * g.n_cols;
+    if (warp >= tiles) return;
+    const int64_t br = warp / g.n_cols, bc = warp - br * g.n_cols;
+    int64_t cnt;
+    uint64_t h;
+    tile_scan(bits, g, br, bc, &cnt, &h);
+    if ((threadIdx.x & 31) == 0) {
+        const int64_t full = static_cast<int64_t>(g.bm) * g.bn;
+        cls[warp] = cnt == 0 ? 0 : (cnt == full ? 1 : 2);
+        hash[warp] = h;
+    }
+}
+
+__device__ __forceinline__ int32_t block_excl_scan(int32_t v, int32_t* sh, int32_t* total) {
+    // blockDim.x == 256
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int32_t x = v;
+    for (int o = 1; o < 32; o <<= 1) {
+        int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) sh[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+        int32_t s = lane < 8 ? sh[lane] : 0;
+        for (int o = 1; o < 8; o <<= 1) {
+            int32_t y = __shfl_up_sync(0xffffffffu, s, o);
+            if (lane >= o) s += y;
+        }
+        if (lane < 8) sh[lane] = s;
+    }
+    __syncthreads();
+    const int32_t r = x - v + (wid ? sh[wid - 1] : 0);
+    *total = sh[7];
+    __syncthreads();
+    return r;
+}
+
+__global__ void row_count_kernel(const uint8_t* __restrict__ cls, Geo g, int32_t* full_cnt,
+                                 int32_t* part_cnt, int32_t* load_cnt) {
+    const int64_t br = blockIdx.x;
+    int32_t f = 0, p = 0;
+    for (int64_t bc = threadIdx.x; bc < g.n_cols; bc += blockDim.x) {
+        const uint8_t c = cls[br * g.n_cols + bc];
+        f += c == 1;
+        p += c == 2;
+    }
+    for (int o = 16; o; o >>= 1) {
+        f += __shfl_xor_sync(0xffffffffu, f, o);
+        p += __shfl_xor_sync(0xffffffffu, p, o);
+    }
+    __shared__ int32_t sf_[8], sp_[8];
+    if ((threadIdx.x & 31) == 0) {
+        sf_[threadIdx.x >> 5] = f;
+        sp_[threadIdx.x >> 5] = p;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int32_t F = 0, P = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { F += sf_[w]; P += sp_[w]; }
+        full_cnt[br] = F;
+        part_cnt[br] = P;
+        load_cnt[br] = F + P;
+    }
+}
+
+// One 256-thread CTA per tile row: ordered compaction of the three column lists.
+__global__ void compact_kernel(const uint8_t* __restrict__ cls, Geo g,
+                               const int32_t* __restrict__ full_ptr, const int32_t* __restrict__ part_ptr,
+                               const int32_t* __restrict__ load_ptr, int32_t* full_col,
+                               int32_t* part_col, int32_t* load_col, int32_t* part_lin,
+                               int32_t* load_part) {
+    __shared__ int32_t sh[8];
+    const int64_t br = blockIdx.x;
+    int32_t fo = full_ptr[br], po = part_ptr[br], lo = load_ptr[br];
+    for (int64_t c0 = 0; c0 < g.n_cols; c0 += blockDim.x) {
+        const int64_t bc = c0 + threadIdx.x;
+        const uint8_t c = bc < g.n_cols ? cls[br * g.n_cols + bc] : 0;
+        int32_t tf, tp;
+        const int32_t ef = block_excl_scan(c == 1, sh, &tf);
+        const int32_t ep = block_excl_scan(c == 2, sh, &tp);
+        if (c == 1) full_col[fo + ef] = static_cast<int32_t>(bc);
+        if (c == 2) {
+            part_col[po + ep] = static_cast<int32_t>(bc);
+            part_lin[po + ep] = static_cast<int32_t>(br * g.n_cols + bc);
+        }
+        if (c) {
+            load_col[lo + ef + ep] = static_cast<int32_t>(bc);
+            load_part[lo + ef + ep] = c == 2 ? po + ep : -1;
+        }
+        fo += tf;
+        po += tp;
+        lo += tf + tp;
+    }
+}
+
+__device__ bool tiles_equal(const uint32_t* __restrict__ bits, const Geo& g, int64_t ta, int64_t tb) {
+    const int64_t ar = ta / g.n_cols, ac = ta - ar * g.n_cols;
+    const int64_t br_ = tb / g.n_cols, bc_ = tb - br_ * g.n_cols;
+    for (int di = 0; di < g.bm; ++di) {
+        const int64_t ia = ar * g.bm + di, ib = br_ * g.bm + di;
+        for (int64_t c = 0; c * 64 < g.bn; ++c) {
+            const int64_t ja = ac * g.bn + 64 * c, jb = bc_ * g.bn + 64 * c;
+            const uint64_t va = ia < g.n ? row_bits64(bits + ia * g.words, ja, imin64(g.n, ac * g.bn + g.bn)) : 0ull;
+            const uint64_t vb = ib < g.n ? row_bits64(bits + ib * g.words, jb, imin64(g.n, bc_ * g.bn + g.bn)) : 0ull;
+            if (va != vb) return false;
+        }
+    }
+    return true;
+}
+
+__global__ void dedup_insert_kernel(const uint32_t* __restrict__ bits, Geo g, int32_t n_part,
+                                    const int32_t* __restrict__ part_lin, const uint64_t* __restrict__ hash,
+                                    int32_t* table, uint32_t cap_mask, int32_t* part_slot) {
+    const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k >= n_part) return;
+    const int32_t lin = part_lin[k];
+    const uint64_t h = hash[lin];
+    uint32_t s = static_cast<uint32_t>(h ^ (h >> 32)) & cap_mask;
+    for (;;) {
+        int32_t cur = atomicCAS(&table[s], -1, lin);
+        if (cur == -1) break;  // claimed an empty slot
+        if (hash[cur] == h && tiles_equal(bits, g, cur, lin)) {
+            atomicMin(&table[s], lin);
+            break;
+        }
+        s = (s + 1) & cap_mask;
+    }
+    part_slot[k] = static_cast<int32_t>(s);
+}
+
+__global__ void first_flag_kernel(int32_t n_part, const int32_t* __restrict__ part_lin,
+                                  const int32_t* __restrict__ table, const int32_t* __restrict__ part_slot,
+                                  int32_t* first) {
+    const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k >= n_part) return;
+    first[k] = table[part_slot[k]] == part_lin[k] ? 1 : 0;
+}
+
+__global__ void slot_id_kernel(int32_t n_part, const int32_t* __restrict__ first,
+                               const int32_t* __restrict__ first_scan, const int32_t* __restrict__ part_slot,
+                               int32_t* slot_id, int32_t* pool_src) {
+    const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k >= n_part) return;
+    if (first[k]) {
+        slot_id[part_slot[k]] = first_scan[k];
+        pool_src[first_scan[k]] = static_cast<int32_t>(k);
+    }
+}
+
+__global__ void tile_ids_kernel(int32_t n_part, const int32_t* __restrict__ part_slot,
+                                const int32_t* __restrict__ slot_id, int32_t* tile_ids) {
+    const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k >= n_part) return;
+    tile_ids[k] = slot_id[part_slot[k]];
+}
+
+__global__ void load_tile_kernel(int32_t n_load, const int32_t* __restrict__ load_part,
+                                 const int32_t* __restrict__ tile_ids, int32_t* load_tile) {
+    const int64_t l = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (l >= n_load) return;
+    const int32_t k = load_part[l];
+    load_tile[l] = k < 0 ? -1 : tile_ids[k];
+}
+
+// One warp per pool tile; lanes produce bytes of pack_bits(tile).
+__global__ void pool_write_kernel(const uint32_t* __restrict__ bits, Geo g, int32_t n_pool,
+                                  const int32_t* __restrict__ pool_src,
+                                  const int32_t* __restrict__ part_lin, int32_t tile_bytes,
+                                  uint8_t* __restrict__ pool) {
+    const int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    if (w >= n_pool) return;
+    const int lane = threadIdx.x & 31;
+    const int64_t lin = part_lin[pool_src[w]];
+    const int64_t br = lin / g.n_cols, bc = lin - br * g.n_cols;
+    const int64_t nbits = static_cast<int64_t>(g.bm) * g.bn;
+    for (int64_t byte = lane; byte < tile_bytes; byte += 32) {
+        uint32_t v = 0;
+        for (int b = 0; b < 8; ++b) {
+            const int64_t t = byte * 8 + b;
+            if (t >= nbits) break;
+            const int64_t di = t / g.bn, dj = t - di * g.bn;
+            const int64_t i = br * g.bm + di, j = bc * g.bn + dj;
+            if (i < g.n && j < g.n && ((bits[i * g.words + (j >> 5)] >> (j & 31)) & 1u)) v |= 1u << b;
+        }
+        pool[w * tile_bytes + byte] = static_cast<uint8_t>(v);
+    }
+}
+
+// ---- row-wise CSR ----
+__global__ void row_popc_kernel(const uint32_t* __restrict__ bits, int32_t n, int32_t words,
+                                int32_t* cnt) {
+    const int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    if (i >= n) return;
+    const int lane = threadIdx.x & 31;
+    int32_t c = 0;
+    for (int w = lane; w < words; w += 32) c += __popc(bits[i * words + w]);
+    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if (lane == 0) cnt[i] = c;
+}
+
+__global__ void row_compact_kernel(const uint32_t* __restrict__ bits, int32_t n, int32_t words,
+                                   const int32_t* __restrict__ row_ptr, int32_t* __restrict__ col) {
+    const int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    if (i >= n) return;
+    const int lane = threadIdx.x & 31;
+    int32_t base = row_ptr[i];
+    for (int w0 = 0; w0 < words; w0 += 32) {
+        const int w = w0 + lane;
+        uint32_t v = w < words ? bits[i * words + w] : 0u;
+        const int c = __popc(v);
+        int x = c;
+        for (int o = 1; o < 32; o <<= 1) {
+            int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        int pos = base + x - c;
+        while (v) {
+            const int b = __ffs(v) - 1;
+            col[pos++] = w * 32 + b;
+            v &= v - 1;
+        }
+        base += __shfl_sync(0xffffffffu, x, 31);
+    }
+}
+
+template <typename T>
+T* carve(char*& p, int64_t count) {
+    T* r = reinterpret_cast<T*>(p);
+    p += ((count * static_cast<int64_t>(sizeof(T)) + 255) / 256) * 256;
+    return r;
+}
+
+unsigned blocks_for(int64_t threads, int per = 256) {
+    return static_cast<unsigned>(imax64(1, ceil_div(threads, per)));
+}
+
+}  // namespace
+}  // namespace sf
+
+using namespace sf;
+
+extern "C" sf_status sf_bsr_build(const uint32_t* d_bits, int32_t seq_len, int32_t block_m,
+                                  int32_t block_n, sf_bsr_dev* out, void* stream) {
+    if (!out) return fail(SF_INVALID_PARAMETER, "null output");
+    *out = sf_bsr_dev{};
+    if (block_m < 1 || block_n < 1) return fail(SF_INVALID_PARAMETER, "block sizes must be >= 1");
+    if (seq_len < 1) return fail(SF_INVALID_PARAMETER, "seq_len must be positive");
+    cudaStream_t st = as_stream(stream);
+    Geo g{seq_len, sf_mask_words(seq_len), block_m, block_n,
+          static_cast<int32_t>(ceil_div(seq_len, block_m)), static_cast<int32_t>(ceil_div(seq_len, block_n))};
+    const int64_t tiles = static_cast<int64_t>(g.n_rows) * g.n_cols;
+    if (tiles > (1ll << 31) - 1) return fail(SF_INVALID_PARAMETER, "tile grid too large");
+
+    // scratch 1: per-tile class + hash, per-row counts, row pointers, counts
+    char* s1 = nullptr;
+    const int64_t s1_bytes = ceil_div(tiles, 256) * 256 + ceil_div(tiles * 8, 256) * 256 +
+                             6 * (ceil_div((g.n_rows + 1) * 4, 256) * 256) + 256;
+    SF_CUDA_TRY(cudaMallocAsync(&s1, s1_bytes, st));
+    char* p = s1;
+    uint8_t* cls = carve<uint8_t>(p, tiles);
+    uint64_t* hash = carve<uint64_t>(p, tiles);
+    int32_t* fcnt = carve<int32_t>(p, g.n_rows + 1);
+    int32_t* pcnt = carve<int32_t>(p, g.n_rows + 1);
+    int32_t* lcnt = carve<int32_t>(p, g.n_rows + 1);
+    int32_t* fptr = carve<int32_t>(p, g.n_rows + 1);
+    int32_t* pptr = carve<int32_t>(p, g.n_rows + 1);
+    int32_t* lptr = carve<int32_t>(p, g.n_rows + 1);
+    int32_t* totals = carve<int32_t>(p, 4);
+
+    classify_kernel<<<blocks_for(tiles * 32), 256, 0, st>>>(d_bits, g, cls, hash);
+    SF_LAUNCH_CHECK();
+    row_count_kernel<<<g.n_rows, 256, 0, st>>>(cls, g, fcnt, pcnt, lcnt);
+    SF_LAUNCH_CHECK();
+    SF_TRY(scan_exclusive(fcnt, fptr, g.n_rows, totals + 0, st));
+    SF_TRY(scan_exclusive(pcnt, pptr, g.n_rows, totals + 1, st));
+    SF_TRY(scan_exclusive(lcnt, lptr, g.n_rows, totals + 2, st));
+    int32_t h_tot[3] = {0, 0, 0};
+    SF_CUDA_TRY(cudaMemcpyAsync(h_tot, totals, 12, cudaMemcpyDeviceToHost, st));
+    SF_CUDA_TRY(cudaStreamSynchronize(st));
+    const int32_t n_full = h_tot[0], n_part = h_tot[1], n_load = h_tot[2];
+    const int32_t tile_bytes = static_cast<int32_t>(ceil_div(static_cast<int64_t>(block_m) * block_n, 8));
+
+    // output block (owned by the sf_bsr_dev)
+    const int64_t rp = g.n_rows + 1;
+    const int64_t out_bytes = 3 * ceil_div(rp * 4, 256) * 256 + ceil_div(std::max(1, n_full) * 4ll, 256) * 256 +
+                              2 * ceil_div(std::max(1, n_part) * 4ll, 256) * 256 +
+                              2 * ceil_div(std::max(1, n_load) * 4ll, 256) * 256 +
+                              ceil_div(imax64(1, static_cast<int64_t>(n_part) * tile_bytes), 256) * 256;
+    char* ob = nullptr;
+    SF_CUDA_TRY(cudaMallocAsync(&ob, out_bytes, st));
+    p = ob;
+    out->full_row_ptr = carve<int32_t>(p, rp);
+    out->part_row_ptr = carve<int32_t>(p, rp);
+    out->load_row_ptr = carve<int32_t>(p, rp);
+    out->full_col_idx = carve<int32_t>(p, std::max(1, n_full));
+    out->part_col_idx = carve<int32_t>(p, std::max(1, n_part));
+    out->part_tile_ids = carve<int32_t>(p, std::max(1, n_part));
+    out->load_col_idx = carve<int32_t>(p, std::max(1, n_load));
+    out->load_tile = carve<int32_t>(p, std::max(1, n_load));
+    out->pool = carve<uint8_t>(p, imax64(1, static_cast<int64_t>(n_part) * tile_bytes));
+    out->_alloc = ob;
+    SF_CUDA_TRY(cudaMemcpyAsync(out->full_row_ptr, fptr, rp * 4, cudaMemcpyDeviceToDevice, st));
+    SF_CUDA_TRY(cudaMemcpyAsync(out->part_row_ptr, pptr, rp * 4, cudaMemcpyDeviceToDevice, st));
+    SF_CUDA_TRY(cudaMemcpyAsync(out->load_row_ptr, lptr, rp * 4, cudaMemcpyDeviceToDevice, st));
+
+    // scratch 2: dedup
+    uint32_t cap = 16;
+    while (cap < static_cast<uint32_t>(std::max(1, n_part)) * 2u) cap <<= 1;
+    char* s2 = nullptr;
+    const int64_t np1 = std::max(1, n_part);
+    const int64_t s2_bytes = 5 * ceil_div((np1 + 1) * 4, 256) * 256 + 2 * ceil_div(cap * 4ll, 256) * 256 +
+                             ceil_div(std::max(1, n_load) * 4ll, 256) * 256;
+    SF_CUDA_TRY(cudaMallocAsync(&s2, s2_bytes, st));
+    p = s2;
+    int32_t* part_lin = carve<int32_t>(p, np1);
+    int32_t* part_slot = carve<int32_t>(p, np1);
+    int32_t* first = carve<int32_t>(p, np1);
+    int32_t* first_scan = carve<int32_t>(p, np1 + 1);
+    int32_t* pool_src = carve<int32_t>(p, np1);
+    int32_t* table = carve<int32_t>(p, cap);
+    int32_t* slot_id = carve<int32_t>(p, cap);
+    int32_t* load_part = carve<int32_t>(p, std::max(1, n_load));
+    SF_CUDA_TRY(cudaMemsetAsync(table, 0xff, cap * 4ll, st));
+
+    if (n_load > 0) {
+        compact_kernel<<<g.n_rows, 256, 0, st>>>(cls, g, fptr, pptr, lptr, out->full_col_idx,
+                                                 out->part_col_idx, out->load_col_idx, part_lin, load_part);
+        SF_LAUNCH_CHECK();
+    }
+    int32_t n_pool = 0;
+    if (n_part > 0) {
+        dedup_insert_kernel<<<blocks_for(n_part), 256, 0, st>>>(d_bits, g, n_part, part_lin, hash, table,
+                                                                cap - 1, part_slot);
+        SF_LAUNCH_CHECK();
+        first_flag_kernel<<<blocks_for(n_part), 256, 0, st>>>(n_part, part_lin, table, part_slot, first);
+        SF_LAUNCH_CHECK();
+        SF_TRY(scan_exclusive(first, first_scan, n_part, totals + 3, st));
+        slot_id_kernel<<<blocks_for(n_part), 256, 0, st>>>(n_part, first, first_scan, part_slot, slot_id, pool_src);
+        SF_LAUNCH_CHECK();
+        tile_ids_kernel<<<blocks_for(n_part), 256, 0, st>>>(n_part, part_slot, slot_id, out->part_tile_ids);
+        SF_LAUNCH_CHECK();
+        SF_CUDA_TRY(cudaMemcpyAsync(&n_pool, totals + 3, 4, cudaMemcpyDeviceToHost, st));
+        SF_CUDA_TRY(cudaStreamSynchronize(st));
+        pool_write_kernel<<<blocks_for(static_cast<int64_t>(n_pool) * 32), 256, 0, st>>>(
+            d_bits, g, n_pool, pool_src, part_lin, tile_bytes, out->pool);
+        SF_LAUNCH_CHECK();
+    }
+    if (n_load > 0) {
+        load_tile_kernel<<<blocks_for(n_load), 256, 0, st>>>(n_load, load_part, out->part_tile_ids, out->load_tile);
+        SF_LAUNCH_CHECK();
+    }
+    SF_CUDA_TRY(cudaFreeAsync(s2, st));
+    SF_CUDA_TRY(cudaFreeAsync(s1, st));
+
+    out->seq_len = seq_len;
+    out->block_m = block_m;
+    out->block_n = block_n;
+    out->n_rows = g.n_rows;
+    out->n_cols = g.n_cols;
+    out->n_full = n_full;
+    out->n_part = n_part;
+    out->n_load = n_load;
+    out->n_pool = n_pool;
+    out->tile_bytes = tile_bytes;
+    return SF_OK;
+}
+
+extern "C" sf_status sf_bsr_free(sf_bsr_dev* bsr, void* stream) {
+    if (!bsr) return SF_OK;
+    if (bsr->_alloc) SF_CUDA_TRY(cudaFreeAsync(bsr->_alloc, as_stream(stream)));
+    *bsr = sf_bsr_dev{};
+    return SF_OK;
+}
+
+extern "C" sf_status sf_bsr_to_host(const sf_bsr_dev* b, int32_t* full_row_ptr, int32_t* full_col_idx,
+                                    int32_t* part_row_ptr, int32_t* part_col_idx, int32_t* part_tile_ids,
+                                    int32_t* load_row_ptr, int32_t* load_col_idx, uint8_t* pool,
+                                    void* stream) {
+    cudaStream_t st = as_stream(stream);
+    const int64_t rp = (b->n_rows + 1) * 4ll;
+    auto cp = [&](void* dst, const void* src, int64_t bytes) -> sf_status {
+        if (dst && bytes > 0) SF_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st));
+        return SF_OK;
+    };
+    SF_TRY(cp(full_row_ptr, b->full_row_ptr, rp));
+    SF_TRY(cp(part_row_ptr, b->part_row_ptr, rp));
+    SF_TRY(cp(load_row_ptr, b->load_row_ptr, rp));
+    SF_TRY(cp(full_col_idx, b->full_col_idx, b->n_full * 4ll));
+    SF_TRY(cp(part_col_idx, b->part_col_idx, b->n_part * 4ll));
+    SF_TRY(cp(part_tile_ids, b->part_tile_ids, b->n_part * 4ll));
+    SF_TRY(cp(load_col_idx, b->load_col_idx, b->n_load * 4ll));
+    SF_TRY(cp(pool, b->pool, static_cast<int64_t>(b->n_pool) * b->tile_bytes));
+    SF_CUDA_TRY(cudaStreamSynchronize(st));
+    return SF_OK;
+}
+
+extern "C" sf_status sf_bsr_serialize(const sf_bsr_dev* b, uint8_t* buf, int64_t cap, int64_t* nbytes,
+                                      void* stream) {
+    // io.hpp:103-122 layout
+    const int64_t rp = b->n_rows + 1;
+    const int64_t size = 4 + 16 + 7 * 4 + 4 * (3 * rp + b->n_full + 2ll * b->n_part + b->n_load) + 4 +
+                         static_cast<int64_t>(b->n_pool) * b->tile_bytes;
+    if (nbytes) *nbytes = size;
+    if (!buf) return SF_OK;
+    std::vector<int32_t> frp(rp), fci(b->n_full), prp(rp), pci(b->n_part), pti(b->n_part), lrp(rp), lci(b->n_load);
+    std::vector<uint8_t> pool(static_cast<size_t>(b->n_pool) * b->tile_bytes);
+    SF_TRY(sf_bsr_to_host(b, frp.data(), fci.data(), prp.data(), pci.data(), pti.data(), lrp.data(), lci.data(),
+                          pool.data(), stream));
+    std::vector<uint8_t> o;
+    o.reserve(static_cast<size_t>(size));
+    auto u32 = [&](uint32_t v) { for (int s = 0; s < 32; s += 8) o.push_back(static_cast<uint8_t>(v >> s)); };
+    auto arr = [&](const std::vector<int32_t>& a) { u32(static_cast<uint32_t>(a.size())); for (auto x : a) u32(static_cast<uint32_t>(x)); };
+    o.insert(o.end(), {'S', 'F', 'B', 'R'});
+    u32(1);
+    u32(static_cast<uint32_t>(b->seq_len));
+    u32(static_cast<uint32_t>(b->block_m));
+    u32(static_cast<uint32_t>(b->block_n));
+    arr(frp); arr(fci); arr(prp); arr(pci); arr(pti); arr(lrp); arr(lci);
+    u32(static_cast<uint32_t>(b->n_pool));
+    o.insert(o.end(), pool.begin(), pool.end());
+    std::memcpy(buf, o.data(), static_cast<size_t>(imin64(cap, static_cast<int64_t>(o.size()))));
+    return SF_OK;
+}
+
+extern "C" sf_status sf_rowwise_build(const uint32_t* d_bits, int32_t seq_len, sf_csr_dev* out, void* stream) {
+    if (!out) return fail(SF_INVALID_PARAMETER, "null output");
+    *out = sf_csr_dev{};
+    if (seq_len < 1) return fail(SF_INVALID_PARAMETER, "seq_len must be positive");
+    cudaStream_t st = as_stream(stream);
+    const int32_t words = sf_mask_words(seq_len);
+    int32_t* cnt = nullptr;
+    SF_CUDA_TRY(cudaMallocAsync(&cnt, (seq_len + 1) * 4ll + 256, st));
+    int32_t* total = cnt + seq_len;
+    char* blk = nullptr;
+    row_popc_kernel<<<blocks_for(static_cast<int64_t>(seq_len) * 32), 256, 0, st>>>(d_bits, seq_len, words, cnt);
+    SF_LAUNCH_CHECK();
+    int32_t* rp_tmp = nullptr;
+    SF_CUDA_TRY(cudaMallocAsync(&rp_tmp, (seq_len + 1) * 4ll, st));
+    SF_TRY(scan_exclusive(cnt, rp_tmp, seq_len, total, st));
+    int32_t nnz = 0;
+    SF_CUDA_TRY(cudaMemcpyAsync(&nnz, total, 4, cudaMemcpyDeviceToHost, st));
+    SF_CUDA_TRY(cudaStreamSynchronize(st));
+    const int64_t rp_bytes = ceil_div((seq_len + 1) * 4ll, 256) * 256;
+    SF_CUDA_TRY(cudaMallocAsync(&blk, rp_bytes + imax64(4, nnz * 4ll), st));
+    out->row_ptr = reinterpret_cast<int32_t*>(blk);
+    out->col_idx = reinterpret_cast<int32_t*>(blk + rp_bytes);
+    SF_CUDA_TRY(cudaMemcpyAsync(out->row_ptr, rp_tmp, (seq_len + 1) * 4ll, cudaMemcpyDeviceToDevice, st));
+    row_compact_kernel<<<blocks_for(static_cast<int64_t>(seq_len) * 32), 256, 0, st>>>(d_bits, seq_len, words,
+                                                                                       out->row_ptr, out->col_idx);
+    SF_LAUNCH_CHECK();
+    SF_CUDA_TRY(cudaFreeAsync(rp_tmp, st));
+    SF_CUDA_TRY(cudaFreeAsync(cnt, st));
+    out->seq_len = seq_len;
+    out->nnz = nnz;
+    out->_alloc = blk;
+    return SF_OK;
+}
+
+extern "C" sf_status sf_csr_free(sf_csr_dev* csr, void* stream) {
+    if (!csr) return SF_OK;
+    if (csr->_alloc) SF_CUDA_TRY(cudaFreeAsync(csr->_alloc, as_stream(stream)));
+    *csr = sf_csr_dev{};
+    return SF_OK;
+}
+
+extern "C" sf_status sf_csr_to_host(const sf_csr_dev* csr, int32_t* row_ptr, int32_t* col_idx, void* stream) {
+    cudaStream_t st = as_stream(stream);
+    if (row_ptr)
+        SF_CUDA_TRY(cudaMemcpyAsync(row_ptr, csr->row_ptr, (csr->seq_len + 1) * 4ll, cudaMemcpyDeviceToHost, st));
+    if (col_idx && csr->nnz > 0)
+        SF_CUDA_TRY(cudaMemcpyAsync(col_idx, csr->col_idx, csr->nnz * 4ll, cudaMemcpyDeviceToHost, st));
+    SF_CUDA_TRY(cudaStreamSynchronize(st));
+    return SF_OK;
+}

@@ -1,0 +1,393 @@
+"""Host-side mirror of the reference operator API for the hot path, over the C ABI.
+
+Names, argument meaning and error classes follow /root/reference/proj/include/sparsefuse/:
+  generate_mask / gen_*            io.hpp:192-204, mask.hpp:74-179
+  build_bsr / build_rowwise        bsr.hpp:47-101, 198-209
+  block_stats                      bsr.hpp:186-196
+  threshold / select_plan          planner.hpp:67-161 (+ a B200 mode)
+  block_sparse_sdpa / rowwise_sdpa attention.hpp:71-213, planner.hpp:165-172
+  mha                              the unified MHA entry (new: the reference's exec_mha always
+                                   runs the block executor, backend.hpp:347)
+Every computation runs in libsf_b200.so on the GPU; tensors are torch CUDA tensors used as
+device memory only.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass
+from typing import Iterable, Optional, Sequence, Union
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import (AttnArgs, AttnStats, BsrDev, CsrDev, HwSpec, MaskDesc, Plan, check, lib, SF_BF16, SF_F16,
+                   SF_BLOCK_WISE, SF_ROW_WISE, SF_PATTERN, SF_PLAN_B200, SF_PLAN_REFERENCE)
+
+
+def _stream(stream=None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+# ---------------------------------------------------------------------------------------------
+# Mask descriptors (io.hpp:158-190 MaskDescriptor; mask.hpp:64-71 PatternParams)
+@dataclass
+class MaskDescriptor:
+    pattern: str
+    seq_len: int
+    band_width: int = 0
+    global_width: int = 0
+    dilation_rate: int = 0
+    filling_rate: float = 0.0
+    block: int = 16
+    seed: int = 0
+
+    def to_c(self) -> MaskDesc:
+        if self.pattern not in SF_PATTERN:
+            raise _lib.InvalidParameter(f"unknown mask pattern: {self.pattern}")
+        return MaskDesc(SF_PATTERN[self.pattern], self.seq_len, self.band_width, self.global_width,
+                        self.dilation_rate, self.block, self.filling_rate, self.seed)
+
+    @staticmethod
+    def from_json(j: dict) -> "MaskDescriptor":
+        # io.hpp:179-190 defaults
+        return MaskDescriptor(j["pattern"], int(j["seq_len"]), int(j.get("band_width", 0)),
+                              int(j.get("global_width", 0)), int(j.get("dilation_rate", 0)),
+                              float(j.get("filling_rate", 0.0)), int(j.get("block", 16)), int(j.get("seed", 0)))
+
+    def to_json(self) -> dict:
+        # io.hpp:164-177: only the fields the pattern uses
+        j = {"pattern": self.pattern, "seq_len": self.seq_len, "seed": self.seed}
+        if self.pattern in ("sliding", "dilated", "longformer", "bigbird", "causal_local", "strided"):
+            j["band_width"] = self.band_width
+        if self.pattern == "dilated":
+            j["dilation_rate"] = self.dilation_rate
+        if self.pattern in ("global", "longformer", "bigbird"):
+            j["global_width"] = self.global_width
+        if self.pattern in ("random", "bigbird"):
+            j["filling_rate"] = self.filling_rate
+            j["block"] = self.block
+        return j
+
+
+class DenseMask:
+    """A seq_len x seq_len validity mask resident on the GPU, bit-packed (sf_capi.h layout).
+
+    Mirrors DenseMask (mask.hpp:18-54); the host uint8 form is available via to_numpy().
+    """
+
+    def __init__(self, seq_len: int, bits: torch.Tensor):
+        self.seq_len = int(seq_len)
+        self.bits = bits  # int32 [seq_len, words]
+
+    @property
+    def words(self) -> int:
+        return int(lib().sf_mask_words(self.seq_len))
+
+    @staticmethod
+    def empty(seq_len: int, device="cuda") -> "DenseMask":
+        if seq_len <= 0:
+            raise _lib.InvalidParameter("seq_len must be positive")
+        w = int(lib().sf_mask_words(seq_len))
+        return DenseMask(seq_len, torch.zeros((seq_len, w), dtype=torch.int32, device=device))
+
+    @staticmethod
+    def from_numpy(m: np.ndarray, device="cuda", stream=None) -> "DenseMask":
+        m = np.ascontiguousarray(m, dtype=np.uint8)
+        n = m.shape[0]
+        dm = DenseMask.empty(n, device)
+        u8 = torch.from_numpy(m).to(device)
+        check(lib().sf_mask_pack_u8(u8.data_ptr(), n, dm.bits.data_ptr(), _stream(stream)))
+        torch.cuda.current_stream().synchronize()
+        return dm
+
+    def to_numpy(self) -> np.ndarray:
+        w = self.bits.cpu().numpy().view(np.uint32)
+        bits = np.unpackbits(w.view(np.uint8), axis=1, bitorder="little")
+        return bits[:, : self.seq_len].astype(np.uint8)
+
+    def true_count(self, stream=None) -> int:
+        c = C.c_int64()
+        check(lib().sf_mask_count(self.bits.data_ptr(), self.seq_len, C.byref(c), _stream(stream)))
+        return c.value
+
+
+def _descs(terms) -> tuple:
+    if isinstance(terms, (MaskDescriptor, dict)):
+        terms = [terms]
+    ds = [t if isinstance(t, MaskDescriptor) else MaskDescriptor(**t) for t in terms]
+    arr = (MaskDesc * len(ds))()
+    for i, d in enumerate(ds):
+        arr[i] = d.to_c()
+    return arr, len(ds)
+
+
+def generate_mask(terms: Union[MaskDescriptor, dict, Sequence], stream=None) -> DenseMask:
+    """generate_mask (io.hpp:192) of one descriptor, or compose (mask.hpp:146) of several."""
+    arr, cnt = _descs(terms)
+    check(lib().sf_mask_validate(arr, cnt))
+    dm = DenseMask.empty(arr[0].seq_len)
+    check(lib().sf_mask_generate(arr, cnt, dm.bits.data_ptr(), _stream(stream)))
+    return dm
+
+
+def gen_sliding_window(seq_len, band_width):
+    return generate_mask(MaskDescriptor("sliding", seq_len, band_width=band_width))
+
+
+def gen_dilated(seq_len, band_width, dilation_rate):
+    return generate_mask(MaskDescriptor("dilated", seq_len, band_width=band_width, dilation_rate=dilation_rate))
+
+
+def gen_global(seq_len, global_width):
+    return generate_mask(MaskDescriptor("global", seq_len, global_width=global_width))
+
+
+def gen_random_blocks(seq_len, block, filling_rate, seed):
+    return generate_mask(MaskDescriptor("random", seq_len, filling_rate=filling_rate, block=block, seed=seed))
+
+
+def gen_longformer(seq_len, global_width, band_width):
+    return generate_mask(MaskDescriptor("longformer", seq_len, band_width=band_width, global_width=global_width))
+
+
+def gen_bigbird(seq_len, global_width, band_width, filling_rate, seed, block=16):
+    return generate_mask(MaskDescriptor("bigbird", seq_len, band_width=band_width, global_width=global_width,
+                                        filling_rate=filling_rate, block=block, seed=seed))
+
+
+# ---------------------------------------------------------------------------------------------
+# Storage formats
+class BsrMask:
+    """Device dual-BSR (bsr.hpp:21-37) built by sf_bsr_build; freed with the object."""
+
+    def __init__(self, dev: BsrDev):
+        self.dev = dev
+
+    def __del__(self):
+        try:
+            if self.dev._alloc:
+                lib().sf_bsr_free(C.byref(self.dev), None)
+        except Exception:
+            pass
+
+    def __getattr__(self, name):
+        if name in ("seq_len", "block_m", "block_n", "n_rows", "n_cols", "n_full", "n_part", "n_load", "n_pool",
+                    "tile_bytes"):
+            return getattr(self.dev, name)
+        raise AttributeError(name)
+
+    def to_host(self, stream=None) -> dict:
+        d = self.dev
+        rp = d.n_rows + 1
+        out = {k: np.zeros(n, np.int32) for k, n in (("full_row_ptr", rp), ("full_col_idx", d.n_full),
+                                                    ("part_row_ptr", rp), ("part_col_idx", d.n_part),
+                                                    ("part_tile_ids", d.n_part), ("load_row_ptr", rp),
+                                                    ("load_col_idx", d.n_load))}
+        pool = np.zeros(d.n_pool * d.tile_bytes, np.uint8)
+        ptr = lambda a: a.ctypes.data if a.size else None
+        check(lib().sf_bsr_to_host(C.byref(d), ptr(out["full_row_ptr"]), ptr(out["full_col_idx"]),
+                                   ptr(out["part_row_ptr"]), ptr(out["part_col_idx"]), ptr(out["part_tile_ids"]),
+                                   ptr(out["load_row_ptr"]), ptr(out["load_col_idx"]), ptr(pool), _stream(stream)))
+        out["pool_packed"] = pool.reshape(d.n_pool, d.tile_bytes) if d.n_pool else np.zeros((0, d.tile_bytes), np.uint8)
+        nbits = d.block_m * d.block_n
+        out["part_mask_pool"] = (np.unpackbits(out["pool_packed"], axis=1, bitorder="little")[:, :nbits]
+                                 if d.n_pool else np.zeros((0, nbits), np.uint8))
+        return out
+
+    def sfbr(self, stream=None) -> bytes:
+        """write_bsr bytes (io.hpp:103-122)."""
+        nb = C.c_int64()
+        check(lib().sf_bsr_serialize(C.byref(self.dev), None, 0, C.byref(nb), _stream(stream)))
+        buf = (C.c_uint8 * nb.value)()
+        check(lib().sf_bsr_serialize(C.byref(self.dev), buf, nb.value, C.byref(nb), _stream(stream)))
+        return bytes(buf)
+
+
+def build_bsr(mask: DenseMask, block_m: int, block_n: int, stream=None) -> BsrMask:
+    dev = BsrDev()
+    check(lib().sf_bsr_build(mask.bits.data_ptr(), mask.seq_len, block_m, block_n, C.byref(dev), _stream(stream)))
+    return BsrMask(dev)
+
+
+@dataclass
+class BlockStats:
+    full_count: int
+    part_count: int
+    empty_count: int
+    valid_block_ratio: float
+
+
+def block_stats(b: BsrMask) -> BlockStats:
+    """bsr.hpp:186-196 (host arithmetic on the device builder's counts)."""
+    total = b.n_rows * b.n_cols
+    return BlockStats(b.n_full, b.n_part, total - b.n_full - b.n_part,
+                      (b.n_full + b.n_part) / total if total > 0 else 0.0)
+
+
+class RowwiseMask:
+    """Device CSR (bsr.hpp:41-45)."""
+
+    def __init__(self, dev: CsrDev):
+        self.dev = dev
+
+    def __del__(self):
+        try:
+            if self.dev._alloc:
+                lib().sf_csr_free(C.byref(self.dev), None)
+        except Exception:
+            pass
+
+    @property
+    def seq_len(self):
+        return self.dev.seq_len
+
+    @property
+    def nnz(self):
+        return self.dev.nnz
+
+    def to_host(self, stream=None):
+        n, nnz = self.dev.seq_len, self.dev.nnz
+        rp = np.zeros(n + 1, np.int32)
+        ci = np.zeros(max(nnz, 1), np.int32)
+        check(lib().sf_csr_to_host(C.byref(self.dev), rp.ctypes.data, ci.ctypes.data, _stream(stream)))
+        return rp, ci[:nnz]
+
+
+def build_rowwise(mask: DenseMask, stream=None) -> RowwiseMask:
+    dev = CsrDev()
+    check(lib().sf_rowwise_build(mask.bits.data_ptr(), mask.seq_len, C.byref(dev), _stream(stream)))
+    return RowwiseMask(dev)
+
+
+# ---------------------------------------------------------------------------------------------
+# Analytical selector
+@dataclass
+class HardwareSpec:
+    name: str
+    sm_num: int
+    smem_size: int
+    max_warp: int
+    element_bytes: int = 2
+
+    def to_c(self) -> HwSpec:
+        return HwSpec(self.name.encode()[:31], self.sm_num, self.smem_size, self.max_warp, self.element_bytes)
+
+
+def hw_preset(name: str) -> HardwareSpec:
+    hw = HwSpec()
+    check(lib().sf_hw_preset(name.encode(), C.byref(hw)))
+    return HardwareSpec(hw.name.decode(), hw.sm_num, hw.smem_size, hw.max_warp, hw.element_bytes)
+
+
+@dataclass
+class KernelPlan:
+    kind: str = "row_wise"
+    block_m: int = 0
+    block_n: int = 0
+    num_warps: int = 0
+    score: float = 0.0
+    threshold: float = float("nan")
+    fallback: bool = False
+
+    def to_c(self) -> Plan:
+        return Plan(SF_BLOCK_WISE if self.kind == "block_wise" else SF_ROW_WISE, self.block_m, self.block_n,
+                    self.num_warps, self.score, self.threshold, int(self.fallback))
+
+    @staticmethod
+    def from_c(p: Plan) -> "KernelPlan":
+        return KernelPlan("block_wise" if p.kind == SF_BLOCK_WISE else "row_wise", p.block_m, p.block_n,
+                          p.num_warps, p.score, p.threshold, bool(p.fallback))
+
+
+def threshold(mask: DenseMask, tau: float = 1.2, stream=None) -> float:
+    out = C.c_double()
+    check(lib().sf_threshold(mask.bits.data_ptr(), mask.seq_len, tau, C.byref(out), _stream(stream)))
+    return out.value
+
+
+def select_plan(mask: DenseMask, hw: HardwareSpec, seq_len: int, h: int, bs: int, head_size: int,
+                mode: str = "reference", stream=None) -> KernelPlan:
+    if mask.seq_len != seq_len:
+        raise _lib.ShapeError("mask seq_len differs from requested")  # planner.hpp:133
+    p = Plan()
+    hwc = hw.to_c()
+    check(lib().sf_select_plan(mask.bits.data_ptr(), C.byref(hwc), seq_len, h, bs, head_size,
+                               SF_PLAN_B200 if mode == "b200" else SF_PLAN_REFERENCE, C.byref(p), _stream(stream)))
+    return KernelPlan.from_c(p)
+
+
+# ---------------------------------------------------------------------------------------------
+# Attention
+def _dtype_code(t: torch.Tensor) -> int:
+    if t.dtype == torch.float16:
+        return SF_F16
+    if t.dtype == torch.bfloat16:
+        return SF_BF16
+    raise _lib.InvalidParameter("attention tensors must be float16 or bfloat16")
+
+
+def attn_args(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, o: torch.Tensor, scale: float = 0.0) -> AttnArgs:
+    """(bs, h, n, d) views with a unit last stride; q, k, v share strides."""
+    for t in (q, k, v, o):
+        if t.dim() != 4 or t.stride(3) != 1 or not t.is_cuda:
+            raise _lib.ShapeError("attention tensors must be CUDA (bs, h, n, d) views with unit last stride")
+    if not (q.shape == k.shape == v.shape == o.shape):
+        raise _lib.ShapeError("Q, K, V shapes differ")  # tensor.hpp:46
+    if not (q.stride() == k.stride() == v.stride()):
+        raise _lib.ShapeError("q, k, v must share strides")
+    if not (q.dtype == k.dtype == v.dtype == o.dtype):
+        raise _lib.InvalidParameter("dtype mismatch")
+    bs, h, n, d = q.shape
+    return AttnArgs(bs, h, n, d, _dtype_code(q), q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(),
+                    q.stride(0), q.stride(1), q.stride(2), o.stride(0), o.stride(1), o.stride(2), scale)
+
+
+def block_sparse_sdpa(q, k, v, bsr: BsrMask, plan: Optional[KernelPlan] = None, out=None, stats: bool = False,
+                      stream=None):
+    """attention.hpp:71 (plan=None) / planner.hpp:165 (plan given: must match the BSR)."""
+    o = out if out is not None else torch.empty_like(q)
+    a = attn_args(q, k, v, o)
+    st = AttnStats()
+    pc = plan.to_c() if plan is not None else None
+    check(lib().sf_mha_blockwise(C.byref(a), C.byref(bsr.dev), C.byref(pc) if pc is not None else None,
+                                 C.byref(st), _stream(stream)))
+    if stats:
+        return o, {"tiles_loaded": st.tiles_loaded, "full_tiles": st.full_tiles, "part_tiles": st.part_tiles}
+    return o
+
+
+def rowwise_sdpa(q, k, v, rw: RowwiseMask, out=None, stream=None):
+    """attention.hpp:177."""
+    o = out if out is not None else torch.empty_like(q)
+    a = attn_args(q, k, v, o)
+    check(lib().sf_mha_rowwise(C.byref(a), C.byref(rw.dev), _stream(stream)))
+    return o
+
+
+class MhaContext:
+    """Formats + plan for one session mask (backend.hpp:309-321 MhaContext), built on device."""
+
+    def __init__(self, mask: DenseMask, plan: KernelPlan, stream=None):
+        self.mask = mask
+        self.plan = plan
+        if plan.kind == "block_wise":
+            self.bsr = build_bsr(mask, plan.block_m, plan.block_n, stream)
+            self.csr = None
+        else:
+            self.bsr = None
+            self.csr = build_rowwise(mask, stream)
+
+
+def mha(q, k, v, ctx: MhaContext, out=None, stream=None):
+    """Unified MHA entry: dispatches the row-wise or block-wise executor from the plan."""
+    if ctx.plan.kind == "block_wise":
+        return block_sparse_sdpa(q, k, v, ctx.bsr, ctx.plan, out=out, stream=stream)
+    return rowwise_sdpa(q, k, v, ctx.csr, out=out, stream=stream)
+
+
+def set_attn_impl(impl: str) -> None:
+    """'auto' | 'generic' | 'tcgen05' kernel selection for block_sparse_sdpa."""
+    check(lib().sf_set_attn_impl({"auto": 0, "generic": 1, "tcgen05": 2}[impl]))

@@ -1,0 +1,175 @@
+"""Masked MHA on the GPU vs the reference executors (north-star bar: fp16 outputs within
+max-abs 2e-2 and mean-rel (sum|d| / sum|ref|) 1e-3 of the reference's fp32 results on the same
+fp16-rounded inputs). Cases follow test_attention.cpp."""
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from oracle.oracle import CONFIG_MASKS
+
+pytestmark = pytest.mark.gpu
+G = Path(__file__).resolve().parent / "golden"
+MAX_ABS, MEAN_REL = 2e-2, 1e-3
+
+
+def parity(out, ref, max_abs=MAX_ABS, mean_rel=MEAN_REL):
+    out = out.float().cpu().numpy().astype(np.float64) if hasattr(out, "cpu") else out
+    ref = np.asarray(ref, np.float64)
+    d = np.abs(out - ref)
+    ma = float(d.max()) if d.size else 0.0
+    mr = float(d.sum() / max(np.abs(ref).sum(), 1e-30))
+    assert ma <= max_abs and mr <= mean_rel, f"max_abs {ma:.3e} mean_rel {mr:.3e}"
+    return ma, mr
+
+
+def to_dev(x, dtype):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(x)).to("cuda", dtype)
+
+
+def fp16_inputs(oracle, bs, h, n, d, seed):
+    return [x.astype(np.float16).astype(np.float32) for x in oracle.random_attention_input(bs, h, n, d, seed)]
+
+
+@pytest.mark.parametrize("impl", ["generic", "auto"])
+def test_golden_attention_cases(sf, oracle, impl):
+    import torch
+    from tests.golden.make_golden import ATTN_CASES
+    z = np.load(G / "attn_small.npz")
+    sf.set_attn_impl(impl)
+    try:
+        for name, (terms, bm, bn, bs, h, d, seed) in ATTN_CASES.items():
+            dm = sf.generate_mask(terms)
+            q, k, v = fp16_inputs(oracle, bs, h, dm.seq_len, d, seed)
+            b = sf.build_bsr(dm, bm, bn)
+            out, st = sf.block_sparse_sdpa(to_dev(q, torch.float16), to_dev(k, torch.float16),
+                                           to_dev(v, torch.float16), b, stats=True)
+            parity(out, z[name + "/out"])
+            ref_stats = z[name + "/stats"]
+            assert (st["tiles_loaded"], st["full_tiles"], st["part_tiles"]) == tuple(int(x) for x in ref_stats)
+    finally:
+        sf.set_attn_impl("auto")
+
+
+@pytest.mark.parametrize("cfg,tile,bs,h", [("cfg1", (128, 16), 1, 12), ("cfg2", (128, 16), 2, 12),
+                                           ("cfg3", (128, 16), 1, 4), ("cfg4", (128, 64), 1, 2),
+                                           ("cfg2", (16, 16), 1, 4), ("cfg1", (64, 32), 1, 4)])
+def test_config_attention_matches_oracle(sf, oracle, cfg, tile, bs, h):
+    import torch
+    terms = CONFIG_MASKS[cfg]
+    m = oracle.mask(terms)
+    n = m.shape[0]
+    q, k, v = fp16_inputs(oracle, bs, h, n, 64, 1)
+    ref, _ = oracle.block_sparse_sdpa(q, k, v, m, *tile, threads=8)
+    dm = sf.generate_mask(terms)
+    b = sf.build_bsr(dm, *tile)
+    for impl in ("generic", "auto"):
+        sf.set_attn_impl(impl)
+        out = sf.block_sparse_sdpa(to_dev(q, torch.float16), to_dev(k, torch.float16), to_dev(v, torch.float16), b)
+        parity(out, ref)
+    sf.set_attn_impl("auto")
+    # row-wise executor over the same mask
+    rw = sf.build_rowwise(dm)
+    out = sf.rowwise_sdpa(to_dev(q, torch.float16), to_dev(k, torch.float16), to_dev(v, torch.float16), rw)
+    parity(out, ref)
+
+
+def test_fully_masked_rows_are_exact_zero(sf, oracle):
+    import torch
+    # test_attention.cpp:41-50
+    q, k, v = fp16_inputs(oracle, 2, 2, 16, 8, 1)
+    dm = sf.DenseMask.from_numpy(np.zeros((16, 16), np.uint8))
+    o = sf.block_sparse_sdpa(to_dev(q, torch.float16), to_dev(k, torch.float16), to_dev(v, torch.float16),
+                             sf.build_bsr(dm, 4, 4))
+    assert torch.count_nonzero(o).item() == 0
+    o = sf.rowwise_sdpa(to_dev(q, torch.float16), to_dev(k, torch.float16), to_dev(v, torch.float16),
+                        sf.build_rowwise(dm))
+    assert torch.count_nonzero(o).item() == 0
+    # partially masked: rows 0..3 empty in a causal-shifted pattern
+    m = np.tril(np.ones((200, 200), np.uint8), -4)
+    q, k, v = fp16_inputs(oracle, 1, 2, 200, 64, 3)
+    ref, _ = oracle.block_sparse_sdpa(q, k, v, m, 128, 16)
+    o = sf.block_sparse_sdpa(to_dev(q, torch.float16), to_dev(k, torch.float16), to_dev(v, torch.float16),
+                             sf.build_bsr(sf.DenseMask.from_numpy(m), 128, 16))
+    parity(o, ref)
+    assert torch.count_nonzero(o[:, :, :4]).item() == 0
+
+
+def test_single_valid_position_copies_v(sf, oracle):
+    import torch
+    # test_attention.cpp:52-60 (diagonal) through both executors
+    n, d = 40, 64
+    q, k, v = fp16_inputs(oracle, 1, 1, n, d, 3)
+    dm = sf.gen_sliding_window(n, 1)
+    Q, K, V = (to_dev(x, torch.float16) for x in (q, k, v))
+    for o in (sf.block_sparse_sdpa(Q, K, V, sf.build_bsr(dm, 128, 16)), sf.rowwise_sdpa(Q, K, V, sf.build_rowwise(dm))):
+        assert np.abs(o.float().cpu().numpy() - v).max() <= 1e-3
+
+
+def test_all_ones_v_normalisation(sf, oracle):
+    import torch
+    # test_attention.cpp:122-139: probabilities sum to one
+    n = 48
+    terms = [dict(pattern="bigbird", seq_len=n, global_width=4, band_width=6, filling_rate=0.2, seed=41)]
+    m = oracle.mask(terms)
+    q, k, _ = fp16_inputs(oracle, 1, 2, n, 64, 43)
+    v = np.ones_like(q)
+    dm = sf.generate_mask(terms)
+    Q, K, V = (to_dev(x, torch.float16) for x in (q, k, v))
+    expect = np.broadcast_to((m.sum(1) > 0).astype(np.float32)[None, None, :, None], q.shape)
+    for o in (sf.block_sparse_sdpa(Q, K, V, sf.build_bsr(dm, 128, 16)), sf.rowwise_sdpa(Q, K, V, sf.build_rowwise(dm))):
+        assert np.abs(o.float().cpu().numpy() - expect).max() <= 2e-3
+
+
+def test_strided_activation_layout(sf, oracle):
+    """(bs*seq, 3*heads*d) fused-QKV layout read in place; output in (bs*seq, heads*d)."""
+    import torch
+    bs, h, n, d = 2, 3, 256, 64
+    terms = [dict(pattern="longformer", seq_len=n, global_width=16, band_width=16)]
+    m = oracle.mask(terms)
+    q, k, v = fp16_inputs(oracle, bs, h, n, d, 9)
+    ref, _ = oracle.block_sparse_sdpa(q, k, v, m, 128, 16)
+    qkv = torch.empty(bs * n, 3 * h * d, dtype=torch.float16, device="cuda")
+    for t, x in enumerate((q, k, v)):
+        qkv[:, t * h * d:(t + 1) * h * d] = to_dev(x.transpose(0, 2, 1, 3).reshape(bs * n, h * d), torch.float16)
+    view = lambda t: qkv[:, t * h * d:(t + 1) * h * d].view(bs, n, h, d).permute(0, 2, 1, 3)
+    out = torch.zeros(bs * n, h * d, dtype=torch.float16, device="cuda")
+    ov = out.view(bs, n, h, d).permute(0, 2, 1, 3)
+    dm = sf.generate_mask(terms)
+    sf.block_sparse_sdpa(view(0), view(1), view(2), sf.build_bsr(dm, 128, 16), out=ov)
+    parity(ov, ref)
+    out.zero_()
+    sf.rowwise_sdpa(view(0), view(1), view(2), sf.build_rowwise(dm), out=ov)
+    parity(ov, ref)
+
+
+def test_plan_errors(sf, oracle):
+    import torch
+    # test_attention.cpp:158-170
+    q, k, v = (to_dev(x, torch.float16) for x in fp16_inputs(oracle, 1, 1, 64, 16, 3))
+    b = sf.build_bsr(sf.DenseMask.from_numpy(np.ones((64, 64), np.uint8)), 16, 16)
+    with pytest.raises(sf._lib.PlanError):
+        sf.block_sparse_sdpa(q, k, v, b, sf.KernelPlan("block_wise", 32, 16, 4))
+    sf.block_sparse_sdpa(q, k, v, b, sf.KernelPlan("block_wise", 16, 16, 4))
+    with pytest.raises(sf._lib.PlanError):
+        sf.block_sparse_sdpa(q, k, v, b, sf.KernelPlan("row_wise"))
+    with pytest.raises(sf._lib.ShapeError):
+        sf.block_sparse_sdpa(q, k, v, sf.build_bsr(sf.gen_sliding_window(32, 2), 16, 16))
+
+
+def test_unified_mha_dispatch(sf, oracle):
+    import torch
+    n = 2048
+    terms = [dict(pattern="sliding", seq_len=n, band_width=4)]  # narrow band: Eq. 1 routes row-wise
+    dm = sf.generate_mask(terms)
+    plan = sf.select_plan(dm, sf.hw_preset("b200"), n, 2, 1, 64, mode="b200")
+    assert plan.kind == "row_wise" and plan.threshold < 0
+    ctx = sf.MhaContext(dm, plan)
+    q, k, v = fp16_inputs(oracle, 1, 2, n, 64, 5)
+    ref, _ = oracle.block_sparse_sdpa(q, k, v, oracle.mask(terms), 16, 16, threads=8)
+    parity(sf.mha(*(to_dev(x, torch.float16) for x in (q, k, v)), ctx), ref)
+    wide = sf.generate_mask([dict(pattern="bigbird", seq_len=1024, global_width=32, band_width=32,
+                                  filling_rate=0.1, seed=0)])
+    plan = sf.select_plan(wide, sf.hw_preset("b200"), 1024, 12, 16, 64, mode="b200")
+    assert plan.kind == "block_wise" and plan.block_m == 128

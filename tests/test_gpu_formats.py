@@ -1,0 +1,125 @@
+"""Device mask generation and format builders are bit-exact with the reference (via the pinned
+C oracle and the reference-generated golden fixtures)."""
+import json
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from oracle.oracle import CONFIG_MASKS
+
+pytestmark = pytest.mark.gpu
+G = Path(__file__).resolve().parent / "golden"
+FP = json.loads((G / "fingerprints.json").read_text())
+
+PATTERN_CASES = [
+    [dict(pattern="sliding", seq_len=37, band_width=5)],
+    [dict(pattern="sliding", seq_len=4, band_width=4)],
+    [dict(pattern="sliding", seq_len=8, band_width=1)],
+    [dict(pattern="dilated", seq_len=41, band_width=4, dilation_rate=2)],
+    [dict(pattern="dilated", seq_len=8, band_width=2, dilation_rate=1)],
+    [dict(pattern="dilated", seq_len=300, band_width=17, dilation_rate=0)],
+    [dict(pattern="global", seq_len=50, global_width=7)],
+    [dict(pattern="global", seq_len=33, global_width=0)],
+    [dict(pattern="random", seq_len=100, block=16, filling_rate=0.3, seed=11)],
+    [dict(pattern="random", seq_len=97, block=5, filling_rate=0.5, seed=3)],
+    [dict(pattern="random", seq_len=1000, block=1, filling_rate=0.25, seed=9)],  # > 312 draws per twist, many twists
+    [dict(pattern="longformer", seq_len=96, global_width=8, band_width=8)],
+    [dict(pattern="bigbird", seq_len=100, global_width=10, band_width=10, filling_rate=0.2, seed=7)],
+    [dict(pattern="causal", seq_len=70)],
+    [dict(pattern="causal_local", seq_len=70, band_width=9)],
+    [dict(pattern="strided", seq_len=130, band_width=11)],
+    [dict(pattern="sliding", seq_len=64, band_width=8), dict(pattern="global", seq_len=64, global_width=3)],
+]
+
+
+@pytest.mark.parametrize("terms", PATTERN_CASES)
+def test_device_mask_equals_oracle(sf, oracle, terms):
+    dm = sf.generate_mask(terms)
+    assert np.array_equal(dm.to_numpy(), oracle.mask(terms))
+    assert dm.true_count() == int(oracle.mask(terms).sum())
+
+
+@pytest.mark.parametrize("cfg", list(CONFIG_MASKS))
+def test_config_masks_and_formats_match_golden(sf, oracle, cfg):
+    dm = sf.generate_mask(CONFIG_MASKS[cfg])
+    ent = FP[cfg]
+    assert dm.true_count() == ent["true_count"]
+    rw = sf.build_rowwise(dm)
+    rp, ci = rw.to_host()
+    assert len(ci) == ent["rowwise_nnz"]
+    assert "%016x" % oracle.fnv1a(rp.tobytes() + ci.tobytes()) == ent["rowwise_fnv"]
+    for tile, t in ent["tiles"].items():
+        bm, bn = map(int, tile.split("x"))
+        b = sf.build_bsr(dm, bm, bn)
+        s = sf.block_stats(b)
+        assert (s.full_count, s.part_count, s.empty_count, b.n_pool) == (t["full"], t["part"], t["empty"], t["pool"])
+        assert "%016x" % oracle.fnv1a(b.sfbr()) == t["fnv"], (cfg, tile)
+
+
+def test_small_bsr_dumps_match_golden(sf):
+    z = np.load(G / "bsr_small.npz")
+    for i in range(24):
+        n, bm, bn = (int(x) for x in z[f"{i}/shape"])
+        m = np.unpackbits(z[f"{i}/mask"], bitorder="little")[: n * n].reshape(n, n)
+        b = sf.build_bsr(sf.DenseMask.from_numpy(m), bm, bn)
+        assert b.sfbr() == z[f"{i}/sfbr"].tobytes(), (i, n, bm, bn)
+
+
+def test_randomized_round_trip_1000(sf, oracle):
+    # test_bsr.cpp:65-84: 1000 random masks, n <= 96, bm, bn <= 24 — device bytes == oracle bytes
+    rng = np.random.default_rng(2024)
+    for it in range(1000):
+        n = int(rng.integers(1, 97)); bm = int(rng.integers(1, 25)); bn = int(rng.integers(1, 25))
+        m = (rng.random((n, n)) < rng.random()).astype(np.uint8)
+        b = sf.build_bsr(sf.DenseMask.from_numpy(m), bm, bn)
+        assert b.sfbr() == oracle.bsr(m, bm, bn)["sfbr"], (it, n, bm, bn)
+
+
+def test_extremes_and_dedup(sf, oracle):
+    # test_bsr.cpp:14-34, 86-92
+    b = sf.build_bsr(sf.DenseMask.from_numpy(np.zeros((64, 64), np.uint8)), 16, 16)
+    assert (b.n_full, b.n_part, b.n_load, b.n_pool) == (0, 0, 0, 0)
+    b = sf.build_bsr(sf.DenseMask.from_numpy(np.ones((64, 64), np.uint8)), 16, 16)
+    assert (b.n_full, b.n_part, b.n_pool) == (16, 0, 0)
+    i, j = np.indices((64, 64))
+    b = sf.build_bsr(sf.DenseMask.from_numpy((i % 8 == j % 8).astype(np.uint8)), 8, 8)
+    assert b.n_part == 64 and b.n_pool == 1
+
+
+@pytest.mark.parametrize("n,tile", [(8192, (16, 16)), (8192, (128, 16)), (4096, (128, 64))])
+def test_large_masks_match_oracle(sf, oracle, n, tile):
+    w = int(np.sqrt(n))
+    terms = [dict(pattern="bigbird", seq_len=n, global_width=w, band_width=w, filling_rate=0.1, seed=5)]
+    m = oracle.mask(terms)
+    dm = sf.generate_mask(terms)
+    assert np.array_equal(dm.to_numpy(), m)
+    assert sf.build_bsr(dm, *tile).sfbr() == oracle.bsr(m, *tile)["sfbr"]
+
+
+def test_parameter_errors(sf):
+    with pytest.raises(sf._lib.InvalidParameter):
+        sf.gen_sliding_window(16, 0)
+    with pytest.raises(sf._lib.InvalidParameter):
+        sf.gen_sliding_window(16, 17)
+    with pytest.raises(sf._lib.InvalidParameter):
+        sf.gen_dilated(16, 2, -1)
+    with pytest.raises(sf._lib.InvalidParameter):
+        sf.gen_random_blocks(16, 0, 0.5, 1)
+    with pytest.raises(sf._lib.ShapeError):
+        sf.generate_mask([dict(pattern="sliding", seq_len=16, band_width=2), dict(pattern="sliding", seq_len=8, band_width=2)])
+    with pytest.raises(sf._lib.InvalidParameter):
+        sf.build_bsr(sf.gen_sliding_window(16, 2), 0, 4)
+
+
+def test_planner_matches_golden(sf):
+    plans = json.loads((G / "plans.json").read_text())
+    for key, e in plans.items():
+        cfg, preset = key.split("/")
+        dm = sf.generate_mask(CONFIG_MASKS[cfg])
+        p = sf.select_plan(dm, sf.hw_preset(preset), dm.seq_len, 12, e["bs"], 64)
+        assert (p.kind == "block_wise") == (e["kind"] == 1)
+        assert (p.block_m, p.block_n, p.num_warps) == (e["block_m"], e["block_n"], e["num_warps"])
+        assert p.score == e["score"] and p.threshold == e["threshold"]
+    with pytest.raises(sf._lib.DegenerateInput):
+        sf.threshold(sf.generate_mask(dict(pattern="sliding", seq_len=16, band_width=2)))
