@@ -64,9 +64,11 @@ __global__ void __launch_bounds__(256) attn_rowwise_kernel(sf_attn_args a, const
         float dot = 0.f;
 #pragma unroll
         for (int e = 0; e < DPL; ++e) dot += q[e] * kv[e];
-        dot += __shfl_xor_sync(0xffffffffu, dot, 1);
-        dot += __shfl_xor_sync(0xffffffffu, dot, 2);
-        dot += __shfl_xor_sync(0xffffffffu, dot, 4);
+        // groups run different trip counts: reduce within the group's own 8 lanes only
+        const unsigned gmask = 0xffu << (grp * 8);
+        dot += __shfl_xor_sync(gmask, dot, 1);
+        dot += __shfl_xor_sync(gmask, dot, 2);
+        dot += __shfl_xor_sync(gmask, dot, 4);
         const float s = dot * sl2;  // log2-domain score
         const float mn = fmaxf(m, s);
         const float alpha = exp2f(m - mn);  // m == -inf -> 0

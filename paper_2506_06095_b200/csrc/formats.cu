@@ -39,11 +39,12 @@ __device__ __forceinline__ void tile_scan(const uint32_t* __restrict__ bits, con
     const int64_t j0 = bc * g.bn;
     const int64_t jlim = imin64(g.n, j0 + g.bn);
     for (int di = lane; di < g.bm; di += 32) {
+        // rows past n are all-invalid cells (bsr.hpp:72): they hash as zero bits, exactly like
+        // an in-range all-zero row, so equal tile contents always get equal hashes.
         const int64_t i = br * g.bm + di;
-        if (i >= g.n) continue;
-        const uint32_t* row = bits + i * g.words;
+        const uint32_t* row = bits + imin64(i, g.n - 1) * g.words;
         for (int64_t c = 0; c * 64 < g.bn; ++c) {
-            const uint64_t v = row_bits64(row, j0 + 64 * c, jlim);
+            const uint64_t v = i < g.n ? row_bits64(row, j0 + 64 * c, jlim) : 0ull;
             cnt += __popcll(v);
             h += mix64(v ^ (0x9e3779b97f4a7c15ull * static_cast<uint64_t>(di * 1024 + c + 1)));
         }

@@ -1,0 +1,58 @@
+"""Fused segment templates over the C ABI (backend.hpp:228-306 exec_mi_chain / exec_ci_mi).
+
+Weights are kept in the kernel-native layout: a reference Gemm weight (inner x cols, row-major,
+backend.hpp:54,81) is stored transposed as (cols x inner) = (N x K) row-major, the K-major
+operand TMA stages for tcgen05. Bias / LayerNorm parameters stay fp32.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional
+
+import torch
+
+from . import _lib
+from ._lib import GemmArgs, GemmEpilogue, SF_ACT, check, lib
+from .sparsefuse import _dtype_code, _stream
+
+
+def _ptr(t: Optional[torch.Tensor]) -> Optional[int]:
+    return None if t is None else t.data_ptr()
+
+
+def epilogue(bias=None, act: str = "none", aux=None, ln_gamma=None, ln_beta=None, out_pre_ln=None) -> GemmEpilogue:
+    for t in (bias, ln_gamma, ln_beta):
+        if t is not None and t.dtype != torch.float32:
+            raise _lib.InvalidParameter("bias / LayerNorm parameters must be float32")
+    return GemmEpilogue(_ptr(bias), SF_ACT[act], _ptr(aux), aux.stride(0) if aux is not None else 0,
+                        _ptr(ln_gamma), _ptr(ln_beta), _ptr(out_pre_ln))
+
+
+def gemm_fused(x: torch.Tensor, w_nk: torch.Tensor, out: Optional[torch.Tensor] = None, *, bias=None,
+               act: str = "none", aux=None, ln_gamma=None, ln_beta=None, out_pre_ln=None, stream=None) -> torch.Tensor:
+    """out = LN(act(x @ w_nk.T + bias) + aux) — the CiMi template, one tcgen05 kernel."""
+    M, K = x.shape
+    N, K2 = w_nk.shape
+    if K != K2:
+        raise _lib.ShapeError("gemm input width mismatch")  # backend.hpp:245
+    if out is None:
+        out = torch.empty((M, N), dtype=x.dtype, device=x.device)
+    for t in (x, w_nk, out):
+        if t.stride(1) != 1:
+            raise _lib.ShapeError("GEMM operands must be row-major")
+    a = GemmArgs(M, N, K, _dtype_code(x), x.data_ptr(), x.stride(0), w_nk.data_ptr(), w_nk.stride(0),
+                 out.data_ptr(), out.stride(0), epilogue(bias, act, aux, ln_gamma, ln_beta, out_pre_ln))
+    check(lib().sf_gemm_fused(C.byref(a), _stream(stream)))
+    return out
+
+
+def mi_chain(x: torch.Tensor, out: Optional[torch.Tensor] = None, *, bias=None, act: str = "none", aux=None,
+             ln_gamma=None, ln_beta=None, out_pre_ln=None, stream=None) -> torch.Tensor:
+    """The MiChain template: bias -> act -> +aux -> LayerNorm in one pass."""
+    M, N = x.shape
+    if out is None:
+        out = torch.empty_like(x)
+    e = epilogue(bias, act, aux, ln_gamma, ln_beta, out_pre_ln)
+    check(lib().sf_mi_chain(M, N, _dtype_code(x), x.data_ptr(), x.stride(0), C.byref(e), out.data_ptr(),
+                            out.stride(0), _stream(stream)))
+    return out

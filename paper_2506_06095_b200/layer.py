@@ -1,0 +1,145 @@
+"""Encoder/decoder layer executor over the fused templates (the preset chains of
+build_preset_graph, fusion.hpp:343-397), B200 fusion scheme:
+
+  bert-layer (post-norm, GELU)            gpt-layer / t5-layer (pre-norm, GELU / ReLU)
+  -------------------------------------   -------------------------------------------------
+  qkv = X Wqkv + b            [tcgen05]   h   = LN1(X)                         [mi_chain]
+  A   = MHA(q, k, v; mask)    [attention] qkv = h Wqkv + b                     [tcgen05]
+  X1  = LN(A Wo + bo + X)     [tcgen05]   A   = MHA(q, k, v; mask)             [attention]
+  F   = GELU(X1 W1 + b1)      [tcgen05]   X1  = A Wo + bo + X ; h2 = LN2(X1)   [tcgen05, 2 outs]
+  Y   = LN(F W2 + b2 + X1)    [tcgen05]   F   = act(h2 W1 + b1)                [tcgen05]
+                                          Y   = F W2 + b2 + X1                 [tcgen05]
+
+`compat=True` reproduces the reference chain exactly as the reference executes it: no QKV
+projection (Q = K = V = the MHA input, backend.hpp:345-346) and every residual Add adds its
+recorded `aux` matrix (backend.hpp:98-100), so results can be compared with CpuBackend::run_chain.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Dict, Optional
+
+import torch
+
+from . import fused
+from . import sparsefuse as sf
+
+
+@dataclass
+class LayerShape:
+    bs: int
+    seq_len: int
+    hidden: int = 768
+    heads: int = 12
+    head_size: int = 64
+    ff: int = 0
+
+    def __post_init__(self):
+        if self.ff == 0:
+            self.ff = 4 * self.hidden  # GraphHyper ff_dim = 0 -> 4 * hidden (fusion.hpp:351)
+
+    @property
+    def rows(self):
+        return self.bs * self.seq_len
+
+
+def init_weights(model: str, s: LayerShape, dtype=torch.float16, device="cuda", seed: int = 1,
+                 compat: bool = False) -> Dict[str, torch.Tensor]:
+    """Random-init weights of the architecture (synthetic; no checkpoints offline). Gemm weights
+    U(+-1/sqrt(inner)), bias U[-0.5,0.5), LN gamma U[0.5,1.5), beta U[-0.5,0.5) like GraphData."""
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    H, F = s.hidden, s.ff
+
+    def w(n, k):
+        a = 1.0 / k ** 0.5
+        return ((torch.rand(n, k, generator=g) * 2 - 1) * a).to(device, dtype)
+
+    def u(n, lo, hi):
+        return (lo + torch.rand(n, generator=g) * (hi - lo)).to(device, torch.float32)
+
+    W = {"wo": w(H, H), "bo": u(H, -0.5, 0.5), "w1": w(F, H), "b1": u(F, -0.5, 0.5), "w2": w(H, F),
+         "b2": u(H, -0.5, 0.5), "ln1_g": u(H, 0.5, 1.5), "ln1_b": u(H, -0.5, 0.5), "ln2_g": u(H, 0.5, 1.5),
+         "ln2_b": u(H, -0.5, 0.5)}
+    if not compat:
+        W["wqkv"] = w(3 * H, H)
+        W["bqkv"] = u(3 * H, -0.5, 0.5)
+    return W
+
+
+class EncoderLayer:
+    """One layer of `model` on a fixed (bs, seq_len) with activations resident in HBM."""
+
+    def __init__(self, model: str, shape: LayerShape, weights: Dict[str, torch.Tensor], ctx: sf.MhaContext,
+                 compat: bool = False, aux: Optional[Dict[str, torch.Tensor]] = None, dtype=torch.float16):
+        if model not in ("bert-layer", "gpt-layer", "t5-layer"):
+            raise sf._lib.InvalidParameter(f"unknown preset model: {model}")  # fusion.hpp:394
+        if shape.heads * shape.head_size != shape.hidden:
+            raise sf._lib.ShapeError("activation shape incompatible with MHA reshape")  # backend.hpp:331
+        if ctx.mask.seq_len != shape.seq_len:
+            raise sf._lib.ShapeError("MHA mask seq_len mismatch")  # backend.hpp:333
+        self.model, self.s, self.W, self.ctx, self.compat = model, shape, weights, ctx, compat
+        self.aux = aux or {}
+        self.act = "relu" if model == "t5-layer" else "gelu"
+        M, H, F = shape.rows, shape.hidden, shape.ff
+        dev = weights["wo"].device
+        e = lambda *sz: torch.empty(*sz, dtype=dtype, device=dev)
+        self.qkv = None if compat else e(M, 3 * H)
+        self.h = e(M, H)       # pre-norm LN1 output
+        self.attn = e(M, H)
+        self.x1 = e(M, H)
+        self.h2 = e(M, H)
+        self.f = e(M, F)
+        self.out = e(M, H)
+        self.graph = None
+
+    # (bs, heads, seq, d) views of a (bs*seq, width) activation at column offset c0
+    def _heads(self, t: torch.Tensor, c0: int) -> torch.Tensor:
+        s = self.s
+        return t[:, c0:c0 + s.hidden].view(s.bs, s.seq_len, s.heads, s.head_size).permute(0, 2, 1, 3)
+
+    def _mha(self, src: torch.Tensor, stream=None):
+        H = self.s.hidden
+        if self.compat:
+            q = k = v = self._heads(src, 0)
+        else:
+            fused.gemm_fused(src, self.W["wqkv"], self.qkv, bias=self.W["bqkv"], stream=stream)
+            q, k, v = self._heads(self.qkv, 0), self._heads(self.qkv, H), self._heads(self.qkv, 2 * H)
+        sf.mha(q, k, v, self.ctx, out=self._heads(self.attn, 0), stream=stream)
+
+    def forward(self, x: torch.Tensor, stream=None) -> torch.Tensor:
+        W, A = self.W, self.aux
+        if self.model == "bert-layer":
+            self._mha(x, stream)
+            fused.gemm_fused(self.attn, W["wo"], self.x1, bias=W["bo"], aux=A.get("add1", x),
+                             ln_gamma=W["ln1_g"], ln_beta=W["ln1_b"], stream=stream)
+            fused.gemm_fused(self.x1, W["w1"], self.f, bias=W["b1"], act="gelu", stream=stream)
+            fused.gemm_fused(self.f, W["w2"], self.out, bias=W["b2"], aux=A.get("add2", self.x1),
+                             ln_gamma=W["ln2_g"], ln_beta=W["ln2_b"], stream=stream)
+        else:
+            fused.mi_chain(x, self.h, ln_gamma=W["ln1_g"], ln_beta=W["ln1_b"], stream=stream)
+            self._mha(self.h, stream)
+            fused.gemm_fused(self.attn, W["wo"], self.h2, bias=W["bo"], aux=A.get("add1", x),
+                             ln_gamma=W["ln2_g"], ln_beta=W["ln2_b"], out_pre_ln=self.x1, stream=stream)
+            fused.gemm_fused(self.h2, W["w1"], self.f, bias=W["b1"], act=self.act, stream=stream)
+            fused.gemm_fused(self.f, W["w2"], self.out, bias=W["b2"], aux=A.get("add2", self.x1), stream=stream)
+        return self.out
+
+    def kernels_per_step(self) -> int:
+        n = 4 if self.model == "bert-layer" else 5
+        return n + (0 if self.compat else 1)
+
+    # CUDA graph of one step (launch-bound small configs)
+    def capture(self, x: torch.Tensor) -> None:
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            self.forward(x, stream=s)  # warm (tensor maps, attributes)
+        torch.cuda.current_stream().wait_stream(s)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            self.forward(x, stream=s)
+        self.graph = g
+
+    def replay(self):
+        self.graph.replay()
+        return self.out

@@ -159,3 +159,15 @@ def test_graph_params_restated(oracle, reference):
     assert np.array_equal(w, oracle.random_matrix(hid, hid, oracle.mix_seed(1, 1), -a, a).ravel())
     aux = reference.graph_param(*args, 3, 5)
     assert np.array_equal(aux, oracle.random_matrix(rows, hid, oracle.mix_seed(1, 3)).ravel())
+
+
+@pytest.mark.parametrize("model", ["bert-layer", "gpt-layer", "t5-layer"])
+def test_chain_oracle_equals_reference_run_chain(oracle, reference, model):
+    """The composed per-op oracle chain reproduces CpuBackend::run_chain (backend.hpp:430-441)."""
+    from tests.chain_oracle import graph_data, run_chain
+    bs, seq, hid, heads, hs = 1, 64, 64, 2, 32
+    m = oracle.mask([dict(pattern="bigbird", seq_len=seq, global_width=8, band_width=8, filling_rate=0.2, seed=3)])
+    gd = graph_data(oracle, model, bs, seq, hid, 4 * hid, 1)
+    ours = run_chain(oracle, model, gd, gd["input"], m, bs, seq, heads, hs, 16, 16, threads=1)
+    ref = reference.run_chain(model, bs, seq, hid, heads, hs, 1, m, 16, 16)
+    assert np.max(np.abs(ours - ref)) <= 1e-5, np.max(np.abs(ours - ref))
