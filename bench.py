@@ -1,0 +1,357 @@
+#!/usr/bin/env python
+"""Benchmark of the STOF hot path on B200.
+
+Default workload = BASELINE.json configs[1]: one BERT-base encoder layer (masked MHA + fused
+FFN/LayerNorm), batch 16, seq 1024, 12 heads x 64, BigBird(global 32, band 32, random 10% of
+16x16 tiles, seed 0) mask. A step = one layer forward over the batch; metric = tokens/s.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2] [--impl ours|reference]
+
+N > 1 runs under torchrun, one rank per GPU; each rank processes its own batch (weak scaling,
+no collective on the data path); timing is the max over ranks of device (CUDA-event) time.
+`--impl reference` times the reference's own CPU implementation (oracle/_ref: the unmodified
+reference headers compiled in place; CpuBackend::run_chain of the same chain) on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CONFIGS = {
+    "cfg1": dict(model="bert-layer", bs=1, seq=512, hidden=768, heads=12,
+                 mask=[dict(pattern="sliding", seq_len=512, band_width=22)],
+                 desc="BERT-base MHA layer, bs1 seq512, sliding(22)"),
+    "cfg2": dict(model="bert-layer", bs=16, seq=1024, hidden=768, heads=12,
+                 mask=[dict(pattern="bigbird", seq_len=1024, global_width=32, band_width=32, filling_rate=0.10,
+                            seed=0, block=16)],
+                 desc="BERT-base encoder layer, bs16 seq1024, BigBird(32,32,0.10)"),
+    "cfg3": dict(model="gpt-layer", bs=8, seq=2048, hidden=768, heads=12,
+                 mask=[dict(pattern="strided", seq_len=2048, band_width=45)],
+                 desc="GPT-2 decoder layer, bs8 seq2048, causal+strided(45)"),
+    "cfg4": dict(model="t5-layer", bs=8, seq=4096, hidden=768, heads=12,
+                 mask=[dict(pattern="dilated", seq_len=4096, band_width=64, dilation_rate=1),
+                       dict(pattern="global", seq_len=4096, global_width=64)],
+                 desc="T5-base layer, bs8 seq4096, dilated(64,1)+global(64)"),
+}
+METRIC = "BERT/GPT/T5 layer tokens/s (masked MHA + fused FFN/LayerNorm)"
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        j = json.loads(p.read_text())
+        return {"hbm_gbs": j["hbm_gbs"], "tflops": j["bf16_tflops"], "tflops_sustained": j.get("bf16_tflops_sustained"),
+                "source": "measured (MEASURED_PEAKS.json)"}
+    return {"hbm_gbs": 6650.0, "tflops": 1590.0, "tflops_sustained": 1400.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    def __init__(self, idx: int):
+        self.idx, self.proc, self.lines = idx, None, []
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 6:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+# ----------------------------------------------------------------------------------------------
+# reference arm / CPU baseline
+def cpu_reference(cfg, threads, reps):
+    """Time the reference's CpuBackend::run_chain of the config chain (oracle/_ref), one sequence
+    (bs = 1) per host thread; returns (tokens/s, kind, sample description)."""
+    from oracle.oracle import Oracle, Reference
+    o, r = Oracle(), Reference()
+    m = o.mask(cfg["mask"])
+    seq, hid, heads = cfg["seq"], cfg["hidden"], cfg["heads"]
+    if r.available:
+        kind = "reference"
+        run = lambda: r.run_chain(cfg["model"], 1, seq, hid, heads, hid // heads, 1, m, 16, 16, threads=threads)
+    else:  # the C restatement (oracle port), same chain semantics
+        from tests.chain_oracle import graph_data, run_chain
+        kind = "port"
+        gd = graph_data(o, cfg["model"], 1, seq, hid, 4 * hid, 1)
+        run = lambda: [run_chain(o, cfg["model"], gd, gd["input"], m, 1, seq, heads, hid // heads, 16, 16, threads=1)
+                       for _ in range(1)]
+        threads = 1
+    times = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        run()
+        times.append(time.perf_counter() - t0)
+    best = min(times)
+    tokens = threads * seq
+    sample = (f"{threads} independent sequences x {seq} tokens ({threads} of the batch's {cfg['bs']} sequences), "
+              f"1 layer {cfg['model']} unfused chain, BSR 16x16 (the reference's own a100/rtx4090 plan); "
+              f"best of {reps}")
+    return tokens / best, kind, sample, threads
+
+
+def run_reference_arm(args, cfg):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    threads = min(os.cpu_count() or 1, cfg["bs"])
+    from oracle.oracle import Reference
+    # warmup + timed steps, each a bounded sample of the workload
+    vals = []
+    v0, kind, sample, threads = cpu_reference(cfg, threads, 1) if args.warmup else (None, None, None, threads)
+    for _ in range(max(0, args.warmup - 1)):
+        cpu_reference(cfg, threads, 1)
+    for _ in range(args.steps):
+        v, kind, sample, threads = cpu_reference(cfg, threads, 1)
+        vals.append(v)
+    value = float(np.mean(vals))
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * threads * cfg["seq"] / value,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (GraphData seeds)",
+            "config": {"workload": cfg["desc"], "model": cfg["model"], "global_batch": cfg["bs"], "seq_len": cfg["seq"]},
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": kind, "sample": sample},
+            "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------------------------
+def kernel_breakdown(L, x, torch, reps=20):
+    """Each launch of one step timed alone (CUDA events, warm, min of reps): name -> ms."""
+    from paper_2506_06095_b200 import fused, sparsefuse as sf
+    W, s = L.W, L.s
+    H = s.hidden
+    ev = lambda: torch.cuda.Event(enable_timing=True)
+    parts = {}
+
+    def t(name, fn):
+        for _ in range(3):
+            fn()
+        best = 1e9
+        for _ in range(reps):
+            a, b = ev(), ev()
+            a.record(); fn(); b.record()
+            torch.cuda.synchronize()
+            best = min(best, a.elapsed_time(b))
+        parts[name] = best
+
+    src = x if L.model == "bert-layer" else L.h
+    if L.model != "bert-layer":
+        t("ln1_mi_chain", lambda: fused.mi_chain(x, L.h, ln_gamma=W["ln1_g"], ln_beta=W["ln1_b"]))
+    t("qkv_gemm", lambda: fused.gemm_fused(src, W["wqkv"], L.qkv, bias=W["bqkv"]))
+    q, k, v = L._heads(L.qkv, 0), L._heads(L.qkv, H), L._heads(L.qkv, 2 * H)
+    t("masked_mha", lambda: sf.mha(q, k, v, L.ctx, out=L._heads(L.attn, 0)))
+    if L.model == "bert-layer":
+        t("out_proj_gemm_ln", lambda: fused.gemm_fused(L.attn, W["wo"], L.x1, bias=W["bo"], aux=x, ln_gamma=W["ln1_g"],
+                                                       ln_beta=W["ln1_b"]))
+        t("ffn1_gemm_gelu", lambda: fused.gemm_fused(L.x1, W["w1"], L.f, bias=W["b1"], act="gelu"))
+        t("ffn2_gemm_ln", lambda: fused.gemm_fused(L.f, W["w2"], L.out, bias=W["b2"], aux=L.x1, ln_gamma=W["ln2_g"],
+                                                   ln_beta=W["ln2_b"]))
+    else:
+        t("out_proj_gemm_ln", lambda: fused.gemm_fused(L.attn, W["wo"], L.h2, bias=W["bo"], aux=x, ln_gamma=W["ln2_g"],
+                                                       ln_beta=W["ln2_b"], out_pre_ln=L.x1))
+        t("ffn1_gemm_act", lambda: fused.gemm_fused(L.h2, W["w1"], L.f, bias=W["b1"], act=L.act))
+        t("ffn2_gemm", lambda: fused.gemm_fused(L.f, W["w2"], L.out, bias=W["b2"], aux=L.x1))
+    return parts
+
+
+def work_model(cfg, nnz):
+    """Algorithmic work per launch: flops for GEMMs, compulsory bytes
+    and useful flops for the masked MHA."""
+    M, H, F = cfg["bs"] * cfg["seq"], cfg["hidden"], 4 * cfg["hidden"]
+    d = H // cfg["heads"]
+    w = {"qkv_gemm": ("tensor", 2.0 * M * 3 * H * H), "out_proj_gemm_ln": ("tensor", 2.0 * M * H * H),
+         "ffn1_gemm_gelu": ("tensor", 2.0 * M * F * H), "ffn1_gemm_act": ("tensor", 2.0 * M * F * H),
+         "ffn2_gemm_ln": ("tensor", 2.0 * M * H * F), "ffn2_gemm": ("tensor", 2.0 * M * H * F),
+         "ln1_mi_chain": ("hbm", 2.0 * M * H * 2),
+         "masked_mha": ("hbm", 4.0 * cfg["bs"] * cfg["heads"] * cfg["seq"] * d * 2)}
+    mha_flops = 4.0 * d * cfg["bs"] * cfg["heads"] * nnz
+    return w, mha_flops
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference_arm(args, cfg)
+
+    import torch
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2506_06095_b200 import _lib, layer, sparsefuse as sf
+
+    s = layer.LayerShape(cfg["bs"], cfg["seq"], cfg["hidden"], cfg["heads"], cfg["hidden"] // cfg["heads"])
+    dm = sf.generate_mask(cfg["mask"])
+    nnz = dm.true_count()
+    plan = sf.select_plan(dm, sf.hw_preset("b200"), s.seq_len, s.heads, s.bs, s.head_size, mode="b200")
+    ctx = sf.MhaContext(dm, plan)
+    W = layer.init_weights(cfg["model"], s, seed=1 + rank)
+    L = layer.EncoderLayer(cfg["model"], s, W, ctx)
+    g = torch.Generator(device="cuda").manual_seed(7 + rank)
+    x = (torch.rand(s.rows, s.hidden, device="cuda", generator=g) * 2 - 1).half()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
+
+    for _ in range(args.warmup):
+        L.forward(x)
+    torch.cuda.synchronize()
+
+    # ---- timed region: K steps, L2 flushed between steps (outside the per-step events) ----
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    launches0 = _lib.launch_count()
+    with ClockSampler(local) as clk:
+        for a, b in evs:
+            flush.zero_()
+            a.record()
+            L.forward(x)
+            b.record()
+        torch.cuda.synchronize()
+    launches = _lib.launch_count() - launches0
+    if world > 1:
+        torch.distributed.barrier()
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    total_ms = float(sum(step_ms))
+    if world > 1:
+        t = torch.tensor([total_ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    tokens = s.rows * world
+    value = tokens / (ms_per_step / 1e3)
+
+    # ---- e2e through the public API with host buffers: H2D input, layer, D2H output ----
+    hx = torch.empty(s.rows, s.hidden, dtype=torch.float16, pin_memory=True)
+    hx.copy_(x.cpu())
+    hy = torch.empty_like(hx, pin_memory=True)
+    e2e_steps = max(3, min(args.steps, 50))
+    for _ in range(2):
+        x.copy_(hx, non_blocking=True); L.forward(x); hy.copy_(L.out, non_blocking=True)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(e2e_steps):
+        x.copy_(hx, non_blocking=True)
+        L.forward(x)
+        hy.copy_(L.out, non_blocking=True)
+    e1.record()
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / e2e_steps
+    if world > 1:
+        t = torch.tensor([e2e_ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+
+    # ---- per-kernel breakdown (each launch timed alone) and roofline of the dominant kernel ----
+    parts = kernel_breakdown(L, x, torch)
+    wm, mha_flops = work_model(cfg, nnz)
+    pk = peaks()
+    dom = max(parts, key=parts.get)
+    bound, work = wm[dom]
+    if bound == "tensor":
+        achieved = work / (parts[dom] / 1e3) / 1e12
+        roof = {"kernel": dom, "bound": "tensor", "achieved": achieved, "peak": pk["tflops"], "unit": "TFLOP/s",
+                "frac": achieved / pk["tflops"], "peak_kind": "burst, " + pk["source"]}
+    else:
+        achieved = work / (parts[dom] / 1e3) / 1e9
+        roof = {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                "frac": achieved / pk["hbm_gbs"], "peak_kind": pk["source"]}
+    traffic_file = ROOT / "profiles" / "traffic.json"
+    roof["traffic"] = None
+    if traffic_file.exists():
+        roof["traffic"] = json.loads(traffic_file.read_text()).get(args.config, {}).get(dom)
+    mha_ms = parts["masked_mha"]
+    mha = {"latency_us": mha_ms * 1e3, "plan": [plan.kind, plan.block_m, plan.block_n],
+           "nnz_per_slice": nnz, "useful_tflops": mha_flops / (mha_ms / 1e3) / 1e12,
+           "compulsory_gbs": wm["masked_mha"][1] / (mha_ms / 1e3) / 1e9,
+           "hbm_frac": wm["masked_mha"][1] / (mha_ms / 1e3) / 1e9 / pk["hbm_gbs"]}
+
+    line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f16",
+            "data": "synthetic (uniform[-1,1) activations, random-init weights of the architecture)",
+            "config": {"workload": cfg["desc"], "model": cfg["model"], "global_batch": cfg["bs"] * world,
+                       "seq_len": cfg["seq"], "hidden": cfg["hidden"], "heads": cfg["heads"],
+                       "parallelism": f"dp{world} (batch x heads sharded, no collective)",
+                       "l2": "flushed (256 MB write) between timed steps, outside the step events"},
+            "e2e": {"value": tokens / (e2e_ms / 1e3), "unit": "tokens/s",
+                    "h2d_bytes_per_step": int(hx.numel() * 2), "d2h_bytes_per_step": int(hy.numel() * 2)},
+            "gpu_launches": int(launches), "roofline": roof, "kernels_ms": parts, "mha": mha,
+            "clocks": clk.summary()}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, kind, sample, thr = cpu_reference(cfg, min(os.cpu_count() or 1, cfg["bs"]), 1)
+        line["cpu_baseline"] = {"value": v, "unit": "tokens/s", "cores": thr, "kind": kind, "sample": sample}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -64,7 +64,8 @@ def test_config_attention_matches_oracle(sf, oracle, cfg, tile, bs, h):
     ref, _ = oracle.block_sparse_sdpa(q, k, v, m, *tile, threads=8)
     dm = sf.generate_mask(terms)
     b = sf.build_bsr(dm, *tile)
-    for impl in ("generic", "auto"):
+    impls = ("generic", "tcgen05") if tile[0] == 128 and tile[1] in (16, 32, 64) else ("generic", "auto")
+    for impl in impls:
         sf.set_attn_impl(impl)
         out = sf.block_sparse_sdpa(to_dev(q, torch.float16), to_dev(k, torch.float16), to_dev(v, torch.float16), b)
         parity(out, ref)
