@@ -3,22 +3,24 @@
 // and block_n in {16, 32, 64} key columns, head_size 64, fp16/bf16.
 //
 // One CTA per (128-row block, b*h slice); 192 threads, 2 CTAs per SM:
-//   warp 0     TMA producer. Q tile once (128 x 64, 128B-swizzled), then per step the K and V rows
-//              of G = 64/block_n load-list column blocks, GATHERED into one contiguous 64-key
-//              stage (a 4-D tensor map over (d, n, h, b) reads Q/K/V in any (b,h,i) stride layout,
-//              including the fused-QKV activation, in place).
+//   warp 0     producer. Lane 0 issues TMA: the Q tile once (128 x 64, 128B-swizzled), then per
+//              step the K and V rows of G = 64/block_n load-list column blocks, GATHERED into one
+//              contiguous 64-key stage (4-D tensor maps over (d, n, h, b) read Q/K/V in any
+//              (b,h,i) stride layout in place, e.g. the fused-QKV activation). The packed bit
+//              tiles of the step's PART tiles are bulk-copied from the BSR pool into the same
+//              stage (one transaction barrier); full tiles need no bits.
 //   warp 1     TMEM allocator + MMA issuer (one elected thread):
-//                S_j = Q K_j^T     tcgen05.mma M=128 N=64 K=16 x4  -> TMEM S[j%2] (fp32)
-//                O_j = P_j V_j     tcgen05.mma M=128 N=64 K=16 x4  -> TMEM O[j%2] (fp32), V as
-//                                  an MN-major B operand straight from the TMA stage
-//   warps 2-5  softmax / correction / epilogue, one thread per query row (TMEM lane):
-//                tcgen05.ld S_j row; apply the tile's mask bits (full tile -> all ones, part tile
-//                -> its pool bits; columns past seq_len are 0 bits in edge tiles) as -inf;
-//                online softmax in the log2 domain; P_j (fp16) written 128B-swizzled to smem as
-//                the A operand of the P.V MMA; O_j folded into a register accumulator
-//                acc = acc * alpha_j + O_j one step later (so softmax j+1 overlaps P_j V_j).
-// Empty tiles are never touched (only the BSR load set is iterated, attention.hpp:104-109);
-// rows whose running max stays -inf produce exact zeros (attention.hpp:160-166).
+//                S_j = Q K_j^T   tcgen05.mma M=128 N=64 K=16 x4 -> TMEM S[j%2] (fp32)
+//                O  += P_j V_j   tcgen05.mma M=128 N=64 K=16 x4 -> TMEM O (fp32, accumulated
+//                                across steps), V read as an MN-major B operand from the stage
+//   warps 2-5  softmax, one thread per query row (TMEM lane): tcgen05.ld S_j, masked row max,
+//              p = 2^(s*scale*log2e - m) with a lazily updated max m (O in TMEM is rescaled only
+//              when the row max grows by more than 2^8, FA4-style, so P <= 256 fits fp16),
+//              P_j (fp16) written 128B-swizzled to smem as the A operand of P.V. 16-column groups
+//              masked for all 32 rows of a warp skip their exp/max work entirely.
+//   epilogue   out = O / l; rows that never saw a valid score are exactly zero
+//              (attention.hpp:160-166).
+// Only the BSR load set is iterated: empty tiles are never touched (attention.hpp:104-109).
 #include <algorithm>
 
 #include "tc.cuh"
@@ -33,7 +35,10 @@ constexpr int kMaxLoads = 1024;  // load-list entries per row block staged in sm
 constexpr int kQBytes = kBM * kD * 2;
 constexpr int kKVBytes = kNS * kD * 2;  // one 64-key stage of K (or V)
 constexpr int kPBytes = kBM * kNS * 2;
-constexpr int kSmem = 1024 + kQBytes + 2 * kStages * kKVBytes + 2 * kPBytes + kMaxLoads * 8 + 256;
+constexpr int kMaskBytes = kBM * 8;     // one 64-bit mask row per query row per stage
+constexpr float kRescaleLog2 = 8.0f;    // lazy-rescale threshold (P <= 2^8)
+constexpr int kSmem = 1024 + kQBytes + 2 * kStages * kKVBytes + 2 * kPBytes + kStages * kMaskBytes +
+                      kMaxLoads * 8 + 256;
 
 struct AttnParams {
     CUtensorMap tq, tk, tv;  // 4-D (d, n, h, b) maps; boxes {64,128,1,1} / {64,bn,1,1}
@@ -84,7 +89,8 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
     unsigned char* sK = sQ + kQBytes;
     unsigned char* sV = sK + kStages * kKVBytes;
     unsigned char* sP = sV + kStages * kKVBytes;
-    int32_t* s_col = reinterpret_cast<int32_t*>(sP + 2 * kPBytes);
+    uint64_t* sMask = reinterpret_cast<uint64_t*>(sP + 2 * kPBytes);  // [kStages][128]
+    int32_t* s_col = reinterpret_cast<int32_t*>(sMask + kStages * kBM);
     int32_t* s_tile = s_col + kMaxLoads;
     uint64_t* bars = reinterpret_cast<uint64_t*>(s_tile + kMaxLoads);
     uint64_t* q_full = bars;
@@ -92,9 +98,9 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
     uint64_t* kv_empty = kv_full + kStages;
     uint64_t* s_full = kv_empty + kStages;  // [2]
     uint64_t* p_full = s_full + 2;          // [2]
-    uint64_t* o_full = p_full + 2;          // [2]
-    uint64_t* o_free = o_full + 2;          // [2]
-    uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(o_free + 2);
+    uint64_t* o_full = p_full + 2;          // [2]: P.V step j completes o_full[j&1] (a parity wait
+                                            // is only unambiguous within one phase of lag)
+    uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(o_full + 2);
 
     const uint32_t warp = tc::warp_id();
     const uint32_t lane = threadIdx.x & 31;
@@ -121,33 +127,43 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
         for (int s = 0; s < 2; ++s) {
             tc::mbar_init(&s_full[s], 1);
             tc::mbar_init(&p_full[s], 128);
-            tc::mbar_init(&o_full[s], 1);
-            tc::mbar_init(&o_free[s], 128);
         }
+        tc::mbar_init(&o_full[0], 1);
+        tc::mbar_init(&o_full[1], 1);
         tc::fence_barrier_init();
     }
     if (warp == 1) tc::tmem_alloc<256>(tmem_ptr);
     tc::fence_before_sync();
     __syncthreads();
     tc::fence_after_sync();
-    const uint32_t tmem = *tmem_ptr;  // S[0] @ +0, S[1] @ +64, O[0] @ +128, O[1] @ +192
+    const uint32_t tmem = *tmem_ptr;  // S[0] @ +0, S[1] @ +64, O @ +128
 
     if (warp == 0) {
-        // ------------------------------------------------------------------ TMA producer
-        if (tc::elect_one() && nsteps > 0) {
+        // ------------------------------------------------------------------ producer
+        if (nsteps > 0 && tc::elect_one()) {
+            const int bn = p.bn;
             tc::mbar_expect_tx(q_full, kQBytes);
             tma_load_4d(sQ, &p.tq, q_full, 0, br * kBM, hh, b);
-            const int chunk = p.bn * kD * 2;
+            const int chunk = bn * kD * 2;
             int s = 0;
             uint32_t ph = 0;
             for (int j = 0; j < nsteps; ++j) {
                 tc::mbar_wait(&kv_empty[s], ph ^ 1);
-                tc::mbar_expect_tx(&kv_full[s], 2 * kKVBytes);
+                int parts = 0;
                 for (int g = 0; g < p.G; ++g) {
                     const int e = j * p.G + g;
-                    const int col = (e < L ? s_col[e] : s_col[0]) * p.bn;  // pad: a valid, fully masked block
+                    parts += (e < L && s_tile[e] >= 0);
+                }
+                tc::mbar_expect_tx(&kv_full[s], 2 * kKVBytes + parts * p.tile_bytes);
+                for (int g = 0; g < p.G; ++g) {
+                    const int e = j * p.G + g;
+                    const int col = (e < L ? s_col[e] : s_col[0]) * bn;  // pad: valid, fully masked
                     tma_load_4d(sK + s * kKVBytes + g * chunk, &p.tk, &kv_full[s], 0, col, hh, b);
                     tma_load_4d(sV + s * kKVBytes + g * chunk, &p.tv, &kv_full[s], 0, col, hh, b);
+                    if (e < L && s_tile[e] >= 0)  // the part tile's packed bits (bsr pool) -> stage
+                        tc::bulk_load(reinterpret_cast<unsigned char*>(sMask) + s * kMaskBytes + g * p.tile_bytes,
+                                      p.pool + static_cast<int64_t>(s_tile[e]) * p.tile_bytes, p.tile_bytes,
+                                      &kv_full[s]);
                 }
                 if (++s == kStages) { s = 0; ph ^= 1; }
             }
@@ -175,15 +191,14 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
             if (nsteps > 1) issue_s(1);
             for (int j = 0; j < nsteps; ++j) {
                 const int s = j % kStages;
-                tc::mbar_wait(&p_full[j & 1], (j >> 1) & 1);  // P_j in smem; S[j&1] consumed
-                if (j >= 2) tc::mbar_wait(&o_free[j & 1], ((j - 2) >> 1) & 1);  // O_{j-2} folded
+                tc::mbar_wait(&p_full[j & 1], (j >> 1) & 1);  // P_j in smem, S[j&1] consumed, O rescaled
                 tc::fence_after_sync();
                 const uint32_t pa = tc::smem_u32(sP + (j & 1) * kPBytes);
                 const uint32_t v0 = tc::smem_u32(sV + s * kKVBytes);
 #pragma unroll
                 for (int k = 0; k < kNS / 16; ++k)
-                    tc::mma_f16_ss(tmem + 128 + (j & 1) * 64, tc::sdesc_sw128(pa + 32 * k),
-                                   tc::sdesc_sw128_mn(v0 + 2048 * k), idesc_o, k != 0);
+                    tc::mma_f16_ss(tmem + 128, tc::sdesc_sw128(pa + 32 * k), tc::sdesc_sw128_mn(v0 + 2048 * k),
+                                   idesc_o, (j | k) != 0);
                 tc::mma_commit(&o_full[j & 1]);
                 tc::mma_commit(&kv_empty[s]);
                 if (j + 2 < nsteps) issue_s(j + 2);
@@ -194,117 +209,130 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
         const uint32_t q = warp & 3;
         const int r = static_cast<int>(q * 32 + lane);
         const uint32_t trow = tmem + ((q * 32) << 16);
-        const int bn = p.bn;
-        const uint32_t full_bits = bn >= 32 ? 0xffffffffu : ((1u << bn) - 1u);
-        float acc[kD];
-#pragma unroll
-        for (int e = 0; e < kD; ++e) acc[e] = 0.f;
-        float m = -INFINITY, l = 0.f, alpha_prev = 1.f;
+        const float sl2 = p.scale_log2;
+        float m = -INFINITY, l = 0.f;
         unsigned char* prow_base = sP + r * 128;
         const int rsw = r & 7;
         for (int j = 0; j < nsteps; ++j) {
-            // ---- mask bits of this row for the 64 columns of step j
+            const int st = j % kStages;
+            tc::mbar_wait(&kv_full[st], (j / kStages) & 1);
+            // this row's 64 mask bits: full tile -> ones, part tile -> staged pool row, pad -> 0
             uint64_t bits = 0;
-            for (int g = 0; g < p.G; ++g) {
-                const int e = j * p.G + g;
-                uint64_t gb = 0;
-                if (e < L) {
-                    const int t = s_tile[e];
-                    if (t < 0) {
-                        gb = bn == 64 ? ~0ull : full_bits;
-                    } else {
-                        const uint8_t* tp = p.pool + static_cast<int64_t>(t) * p.tile_bytes + r * (bn >> 3);
-                        if (bn == 16) gb = *reinterpret_cast<const uint16_t*>(tp);
-                        else if (bn == 32) gb = *reinterpret_cast<const uint32_t*>(tp);
-                        else gb = *reinterpret_cast<const uint64_t*>(tp);
+            {
+                const int bn = p.bn;
+                const unsigned char* mrow = reinterpret_cast<const unsigned char*>(sMask) + st * kMaskBytes + r * (bn >> 3);
+                for (int g = 0; g < p.G; ++g) {
+                    const int e = j * p.G + g;
+                    const int t = e < L ? s_tile[e] : -2;
+                    uint64_t gb = 0;
+                    if (t == -1) {
+                        gb = bn >= 64 ? ~0ull : ((1ull << bn) - 1ull);
+                    } else if (t >= 0) {
+                        const unsigned char* tp = mrow + g * p.tile_bytes;
+                        gb = bn == 16 ? *reinterpret_cast<const uint16_t*>(tp)
+                                      : (bn == 32 ? *reinterpret_cast<const uint32_t*>(tp)
+                                                  : *reinterpret_cast<const uint64_t*>(tp));
                     }
+                    bits |= gb << (g * bn);
                 }
-                bits |= gb << (g * bn);
             }
-            // ---- S_j row from TMEM
             tc::mbar_wait(&s_full[j & 1], (j >> 1) & 1);
             tc::fence_after_sync();
             uint32_t lo[32], hi[32];
             tc::tmem_ld32(trow + (j & 1) * 64, lo);
             tc::tmem_ld32(trow + (j & 1) * 64 + 32, hi);
+            // warp-uniform activity of the four 16-column groups
+            uint32_t gact = 0;
+#pragma unroll
+            for (int g = 0; g < 4; ++g)
+                if (__any_sync(0xffffffffu, ((bits >> (16 * g)) & 0xffffull) != 0)) gact |= 1u << g;
             tc::tmem_ld_wait();
             float sr[64];
-            float mx = -INFINITY;
 #pragma unroll
             for (int c = 0; c < 32; ++c) {
-                sr[c] = ((bits >> c) & 1ull) ? __uint_as_float(lo[c]) * p.scale_log2 : -INFINITY;
-                sr[c + 32] = ((bits >> (c + 32)) & 1ull) ? __uint_as_float(hi[c]) * p.scale_log2 : -INFINITY;
-                mx = fmaxf(mx, fmaxf(sr[c], sr[c + 32]));
+                sr[c] = __uint_as_float(lo[c]) * sl2;
+                sr[c + 32] = __uint_as_float(hi[c]) * sl2;
             }
-            const float mn = fmaxf(m, mx);
-            float alpha = 1.f;
-            float rs = 0.f;
-            uint32_t pk[32];
-            if (mn == -INFINITY) {
+            float mx = -INFINITY;
 #pragma unroll
-                for (int c = 0; c < 32; ++c) pk[c] = 0u;
-            } else {
-                alpha = ex2(m - mn);  // m = -inf -> 0
+            for (int g = 0; g < 4; ++g) {
+                if (!(gact & (1u << g))) continue;
 #pragma unroll
-                for (int c = 0; c < 64; c += 2) {
-                    const float p0 = ex2(sr[c] - mn);
-                    const float p1 = ex2(sr[c + 1] - mn);
-                    rs += p0 + p1;
-                    pk[c >> 1] = pack2<T>(p0, p1);
-                }
-                m = mn;
+                for (int c = 16 * g; c < 16 * g + 16; ++c)
+                    if ((bits >> c) & 1ull) mx = fmaxf(mx, sr[c]);
             }
-            l = l * alpha + rs;
-            // P_j row -> smem, 128B-swizzled K-major A operand (row r: 8 chunks of 16 B)
-            unsigned char* prow = prow_base + (j & 1) * kPBytes;
-#pragma unroll
-            for (int c = 0; c < 8; ++c)
-                *reinterpret_cast<uint4*>(prow + ((c ^ rsw) << 4)) = make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
-            tc::fence_proxy_async();
-            tc::fence_before_sync();
-            tc::mbar_arrive(&p_full[j & 1]);
-            // ---- fold O_{j-1} (P_{j-1} V_{j-1}) into the register accumulator
-            if (j >= 1) {
-                const int jp = j - 1;
-                tc::mbar_wait(&o_full[jp & 1], (jp >> 1) & 1);
+            // lazy max update: rescale O / l only when the max grows by > 2^8 (or first time).
+            // tcgen05.ld/st are warp-collective, so the rescale is voted warp-uniformly and
+            // lanes that do not need it scale by 1.
+            const bool upd = mx > m + kRescaleLog2 || (m == -INFINITY && mx > -INFINITY);
+            const float m_new = upd ? mx : m;
+            const bool resc = upd && m > -INFINITY && j > 0;
+            if (__any_sync(0xffffffffu, resc)) {
+                const float a = resc ? ex2(m - m_new) : 1.f;
+                l *= a;
+                tc::mbar_wait(&o_full[(j - 1) & 1], ((j - 1) >> 1) & 1);  // P_{j-1} V_{j-1} landed in O
                 tc::fence_after_sync();
                 uint32_t ov[32];
 #pragma unroll
                 for (int h2 = 0; h2 < 2; ++h2) {
-                    tc::tmem_ld32(trow + 128 + (jp & 1) * 64 + h2 * 32, ov);
+                    tc::tmem_ld32(trow + 128 + h2 * 32, ov);
                     tc::tmem_ld_wait();
 #pragma unroll
-                    for (int e = 0; e < 32; ++e) acc[h2 * 32 + e] = acc[h2 * 32 + e] * alpha_prev + __uint_as_float(ov[e]);
+                    for (int e = 0; e < 32; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * a);
+                    tc::tmem_st32(trow + 128 + h2 * 32, ov);
                 }
-                tc::fence_before_sync();
-                tc::mbar_arrive(&o_free[jp & 1]);
+                tc::tmem_st_wait();
             }
-            alpha_prev = alpha;
-        }
-        if (nsteps > 0) {
-            const int jp = nsteps - 1;
-            tc::mbar_wait(&o_full[jp & 1], (jp >> 1) & 1);
-            tc::fence_after_sync();
-            uint32_t ov[32];
+            m = m_new;
+            uint32_t pk[32];
+            float rs = 0.f;
 #pragma unroll
-            for (int h2 = 0; h2 < 2; ++h2) {
-                tc::tmem_ld32(trow + 128 + (jp & 1) * 64 + h2 * 32, ov);
-                tc::tmem_ld_wait();
+            for (int g = 0; g < 4; ++g) {
+                if (!(gact & (1u << g)) || m == -INFINITY) {
 #pragma unroll
-                for (int e = 0; e < 32; ++e) acc[h2 * 32 + e] = acc[h2 * 32 + e] * alpha_prev + __uint_as_float(ov[e]);
+                    for (int c = 8 * g; c < 8 * g + 8; ++c) pk[c] = 0u;
+                    continue;
+                }
+#pragma unroll
+                for (int c = 16 * g; c < 16 * g + 16; c += 2) {
+                    const float p0 = ((bits >> c) & 1ull) ? ex2(sr[c] - m) : 0.f;
+                    const float p1 = ((bits >> (c + 1)) & 1ull) ? ex2(sr[c + 1] - m) : 0.f;
+                    rs += p0 + p1;
+                    pk[c >> 1] = pack2<T>(p0, p1);
+                }
             }
+            l += rs;
+            // P_j row -> smem, 128B-swizzled K-major A operand (row r: 8 chunks of 16 B)
+            unsigned char* prow = prow_base + (j & 1) * kPBytes;
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+                *reinterpret_cast<uint4*>(prow + ((c ^ rsw) << 4)) =
+                    make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+            tc::fence_proxy_async();
+            tc::fence_before_sync();
+            tc::mbar_arrive(&p_full[j & 1]);
         }
-        // ---- epilogue: out = acc / l; rows without a valid column stay exactly zero
+        // ---- epilogue: out = O / l; rows without a valid column stay exactly zero
         const int64_t i = static_cast<int64_t>(br) * kBM + r;
+        uint32_t ov[2][32];
+        if (nsteps > 0) {
+            tc::mbar_wait(&o_full[(nsteps - 1) & 1], ((nsteps - 1) >> 1) & 1);
+            tc::fence_after_sync();
+            tc::tmem_ld32(trow + 128, ov[0]);
+            tc::tmem_ld32(trow + 128 + 32, ov[1]);
+            tc::tmem_ld_wait();
+        }
         if (i < p.n) {
             const float inv = l > 0.f ? 1.f / l : 0.f;
             uint4* dst = reinterpret_cast<uint4*>(static_cast<T*>(p.o) + b * p.o_sb + hh * p.o_sh + i * p.o_sn);
 #pragma unroll
-            for (int c = 0; c < 8; ++c)
-                dst[c] = make_uint4(pack2<T>(acc[8 * c] * inv, acc[8 * c + 1] * inv),
-                                    pack2<T>(acc[8 * c + 2] * inv, acc[8 * c + 3] * inv),
-                                    pack2<T>(acc[8 * c + 4] * inv, acc[8 * c + 5] * inv),
-                                    pack2<T>(acc[8 * c + 6] * inv, acc[8 * c + 7] * inv));
+            for (int c = 0; c < 8; ++c) {
+                float v[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) v[e] = nsteps > 0 ? __uint_as_float(ov[c >> 2][(c & 3) * 8 + e]) * inv : 0.f;
+                dst[c] = make_uint4(pack2<T>(v[0], v[1]), pack2<T>(v[2], v[3]), pack2<T>(v[4], v[5]),
+                                    pack2<T>(v[6], v[7]));
+            }
         }
     }
     tc::fence_before_sync();

@@ -1,20 +1,22 @@
-// gemm_tc.cu — the CiMi fused template (backend.hpp:240-264) as one sm_100a kernel:
+// gemm_tc.cu — the CiMi fused template (backend.hpp:240-264) as one persistent sm_100a kernel:
 //   out[M x N] = epilogue( X[M x K] . W[N x K]^T )
 //   epilogue = +bias[N] -> GELU/ReLU -> +aux[M x N] (residual Add) -> LayerNorm over the row
 // (op semantics: backend.hpp:111-167; order = the chain's MI order after the Gemm).
 //
-// Structure (one 128 x BN output tile per CTA, 256 threads):
-//   warp 0      TMA producer: X and W tiles (BK = 64 fp16 = one 128-byte swizzle row) into a
-//               STAGES-deep smem ring, mbarrier complete_tx.
-//   warp 1      MMA issuer: one elected thread issues tcgen05.mma (M=128, N=BN, K=16) into a
-//               TMEM fp32 accumulator; tcgen05.commit frees each smem stage.
-//   warp 2      TMEM allocator.
-//   warps 4-7   epilogue: tcgen05.ld rows of the accumulator (warp w owns TMEM lanes
-//               32*(w%4)..+31 = tile rows), apply the MI ops in registers, store fp16.
-// LayerNorm needs whole rows: the N/BN CTAs of a row block form a thread-block cluster; each CTA
-// stages its x = acc+bias+aux slice as fp32 in the (now idle) pipeline smem, and the per-row
-// partial sums Σx and Σ(x-mean)² are exchanged through distributed shared memory (two-pass,
-// biased variance, eps 1e-5, exactly the reference's order of operations).
+// Persistent CTAs (one per SM) walk a static tile schedule of 128 x BN output tiles:
+//   warp 0        TMA producer: X and W tiles (BK = 64 fp16 = one 128-byte swizzle row) into a
+//                 STAGES-deep smem ring (mbarrier complete_tx).
+//   warp 1        TMEM allocator + MMA issuer: one elected thread issues tcgen05.mma
+//                 (M=128, N=BN, K=16) into one of TWO TMEM accumulators, so the epilogue of tile i
+//                 overlaps the mainloop of tile i+1; tcgen05.commit frees smem stages / signals
+//                 the epilogue.
+//   warps 4..     epilogue: tcgen05.ld accumulator rows (warp w owns TMEM lanes 32*(w%4)..+31),
+//                 apply the MI ops in registers, store fp16.
+// LayerNorm needs whole rows. The N/BN CTAs of a row block form a thread-block cluster (the
+// cluster walks row blocks together). x = acc+bias(+act)+aux is written back into the TMEM
+// accumulator, and the per-row partial sums Σx and Σ(x-mean)^2 are pushed into every peer's
+// shared memory (st.shared::cluster) followed by a remote mbarrier arrive; each CTA then reduces
+// its peers' partials locally. Two-pass mean / biased variance, eps 1e-5, as the reference.
 #include <algorithm>
 #include <cstring>
 
@@ -24,8 +26,8 @@ namespace sf {
 namespace {
 
 constexpr int BM = 128, BK = 64;
-constexpr int kThreads = 256;
 constexpr float kLnEps = 1e-5f;  // backend.hpp:111
+constexpr int kMaxCluster = 8;
 
 struct GemmParams {
     CUtensorMap ta;  // X: rows M, cols K
@@ -42,14 +44,16 @@ struct GemmParams {
     void* out_pre_ln;
 };
 
-template <int BN>
+template <int BN, bool LN>
 struct Cfg {
     static constexpr int STAGES = BN == 256 ? 4 : 6;
+    static constexpr int EPI_WARPS = LN ? 4 : 8;
+    static constexpr int THREADS = 128 + 32 * EPI_WARPS;
     static constexpr int A_BYTES = BM * BK * 2;
     static constexpr int B_BYTES = BN * BK * 2;
-    static constexpr int XS_STRIDE = BN + 4;  // fp32 staging row stride (bank-conflict free float4)
-    static constexpr int SMEM = STAGES * (A_BYTES + B_BYTES) + 1024 /*align*/ + 512 /*barriers*/ + 2 * BM * 4;
-    static_assert(BM * XS_STRIDE * 4 <= STAGES * (A_BYTES + B_BYTES), "LN staging must fit the ring");
+    static constexpr int RED_FLOATS = LN ? 2 * 2 * kMaxCluster * BM : 0;
+    static constexpr int SMEM = STAGES * (A_BYTES + B_BYTES) + 1024 /*align*/ + 256 /*barriers*/ + RED_FLOATS * 4;
+    static constexpr int TMEM_COLS = 2 * BN;  // two accumulator buffers
 };
 
 template <typename T>
@@ -116,24 +120,41 @@ __device__ __forceinline__ void store_chunk(void* base, int64_t ld, int64_t row,
 }
 
 template <typename T, int BN, bool LN>
-__global__ void __launch_bounds__(kThreads, 1) gemm_fused_kernel(const __grid_constant__ GemmParams p) {
-    using C = Cfg<BN>;
+__global__ void __launch_bounds__(Cfg<BN, LN>::THREADS, 1) gemm_fused_kernel(const __grid_constant__ GemmParams p) {
+    using C = Cfg<BN, LN>;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     unsigned char* sA = smem;
     unsigned char* sB = smem + C::STAGES * C::A_BYTES;
     uint64_t* full = reinterpret_cast<uint64_t*>(sB + C::STAGES * C::B_BYTES);
     uint64_t* empty = full + C::STAGES;
-    uint64_t* accum_full = empty + C::STAGES;
-    uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(accum_full + 1);
-    float* red_sum = reinterpret_cast<float*>(tmem_ptr + 4);
-    float* red_sq = red_sum + BM;
+    uint64_t* tfull = empty + C::STAGES;  // [2]
+    uint64_t* tempty = tfull + 2;        // [2]
+    uint64_t* lnb = tempty + 2;          // [2 parity][2 pass]
+    uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(lnb + 4);
+    float* red = reinterpret_cast<float*>(smem + C::STAGES * (C::A_BYTES + C::B_BYTES) + 256);  // [2][2][8][128]
 
     const uint32_t warp = tc::warp_id();
     const uint32_t lane = threadIdx.x & 31;
-    const int n0 = blockIdx.x * BN;
-    const int m0 = blockIdx.y * BM;
     const int nk = (p.K + BK - 1) / BK;
+    const int n_tiles = (p.N + BN - 1) / BN;
+    const int m_tiles = (p.M + BM - 1) / BM;
+    const uint32_t nct = LN ? gridDim.x : 1;  // cluster spans the row: cluster dims == (N/BN, 1, 1)
+    const uint32_t me = LN ? tc::cluster_rank() : 0;
+
+    // tile i of this CTA -> (m_blk, n_blk)
+    auto tile_of = [&](int i, int& mb, int& nb) -> bool {
+        if constexpr (LN) {
+            mb = blockIdx.y + i * gridDim.y;
+            nb = blockIdx.x;
+            return mb < m_tiles;
+        } else {
+            const int t = blockIdx.x + i * gridDim.x;
+            mb = t / n_tiles;
+            nb = t - mb * n_tiles;
+            return t < m_tiles * n_tiles;
+        }
+    };
 
     if (warp == 0 && lane == 0) {
         tc::prefetch_tmap(&p.ta);
@@ -142,140 +163,185 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_fused_kernel(const __grid_co
             tc::mbar_init(&full[s], 1);
             tc::mbar_init(&empty[s], 1);
         }
-        tc::mbar_init(accum_full, 1);
+        for (int b = 0; b < 2; ++b) {
+            tc::mbar_init(&tfull[b], 1);
+            tc::mbar_init(&tempty[b], 32 * C::EPI_WARPS);
+        }
+        if (LN && nct > 1)
+            for (int b = 0; b < 4; ++b) tc::mbar_init(&lnb[b], 128 * (nct - 1));
         tc::fence_barrier_init();
     }
-    if (warp == 2) tc::tmem_alloc<BN>(tmem_ptr);
+    if (warp == 1) tc::tmem_alloc<C::TMEM_COLS>(tmem_ptr);
     tc::fence_before_sync();
     __syncthreads();
+    if (LN && nct > 1) tc::cluster_sync_all();  // peers' barriers are initialised before any remote arrive
     tc::fence_after_sync();
     const uint32_t tmem = *tmem_ptr;
 
     if (warp == 0) {
+        // ------------------------------------------------------------------ TMA producer
         if (tc::elect_one()) {
-            const uint64_t pol_a = tc::policy_evict_first();  // X tile rows are re-read by N/BN CTAs only
+            const uint64_t pol_a = tc::policy_evict_first();
             int s = 0;
             uint32_t ph = 0;
-            for (int kb = 0; kb < nk; ++kb) {
-                tc::mbar_wait(&empty[s], ph ^ 1);
-                tc::mbar_expect_tx(&full[s], C::A_BYTES + C::B_BYTES);
-                tc::tma_load_2d_hint(sA + s * C::A_BYTES, &p.ta, &full[s], kb * BK, m0, pol_a);
-                tc::tma_load_2d(sB + s * C::B_BYTES, &p.tb, &full[s], kb * BK, n0);
-                if (++s == C::STAGES) { s = 0; ph ^= 1; }
+            int mb, nb;
+            for (int i = 0; tile_of(i, mb, nb); ++i) {
+                for (int kb = 0; kb < nk; ++kb) {
+                    tc::mbar_wait(&empty[s], ph ^ 1);
+                    tc::mbar_expect_tx(&full[s], C::A_BYTES + C::B_BYTES);
+                    tc::tma_load_2d_hint(sA + s * C::A_BYTES, &p.ta, &full[s], kb * BK, mb * BM, pol_a);
+                    tc::tma_load_2d(sB + s * C::B_BYTES, &p.tb, &full[s], kb * BK, nb * BN);
+                    if (++s == C::STAGES) { s = 0; ph ^= 1; }
+                }
             }
         }
     } else if (warp == 1) {
-        constexpr uint32_t idesc = tc::idesc_f16(BM, BN, sizeof(T) == 2 && !std::is_same<T, __half>::value, 0, 0);
+        // ------------------------------------------------------------------ MMA issuer
+        constexpr uint32_t idesc = tc::idesc_f16(BM, BN, std::is_same<T, __nv_bfloat16>::value, 0, 0);
         if (tc::elect_one()) {
             int s = 0;
             uint32_t ph = 0;
-            for (int kb = 0; kb < nk; ++kb) {
-                tc::mbar_wait(&full[s], ph);
+            int mb, nb;
+            for (int i = 0; tile_of(i, mb, nb); ++i) {
+                const int acc = i & 1;
+                tc::mbar_wait(&tempty[acc], ((i >> 1) & 1) ^ 1);  // epilogue drained this buffer
                 tc::fence_after_sync();
-                const uint32_t a0 = tc::smem_u32(sA + s * C::A_BYTES);
-                const uint32_t b0 = tc::smem_u32(sB + s * C::B_BYTES);
+                const uint32_t d = tmem + acc * BN;
+                for (int kb = 0; kb < nk; ++kb) {
+                    tc::mbar_wait(&full[s], ph);
+                    tc::fence_after_sync();
+                    const uint32_t a0 = tc::smem_u32(sA + s * C::A_BYTES);
+                    const uint32_t b0 = tc::smem_u32(sB + s * C::B_BYTES);
 #pragma unroll
-                for (int k = 0; k < BK / 16; ++k)
-                    tc::mma_f16_ss(tmem, tc::sdesc_sw128(a0 + 32 * k), tc::sdesc_sw128(b0 + 32 * k), idesc,
-                                   (kb | k) != 0);
-                tc::mma_commit(&empty[s]);
-                if (++s == C::STAGES) { s = 0; ph ^= 1; }
+                    for (int k = 0; k < BK / 16; ++k)
+                        tc::mma_f16_ss(d, tc::sdesc_sw128(a0 + 32 * k), tc::sdesc_sw128(b0 + 32 * k), idesc,
+                                       (kb | k) != 0);
+                    tc::mma_commit(&empty[s]);
+                    if (++s == C::STAGES) { s = 0; ph ^= 1; }
+                }
+                tc::mma_commit(&tfull[acc]);
             }
-            tc::mma_commit(accum_full);
         }
     } else if (warp >= 4) {
-        const uint32_t q = warp & 3;  // TMEM lane quarter this warp may access
+        // ------------------------------------------------------------------ epilogue
+        const uint32_t q = warp & 3;
         const int r_local = static_cast<int>(q * 32 + lane);
-        const int64_t row = m0 + r_local;
-        const bool row_ok = row < p.M;
-        const uint32_t taddr = tmem + ((q * 32) << 16);
-        tc::mbar_wait(accum_full, 0);
-        tc::fence_after_sync();
-        uint32_t r[32];
-        float x[32];
-        if constexpr (!LN) {
-            for (int c = 0; c < BN / 32; ++c) {
-                tc::tmem_ld32(taddr + c * 32, r);
-                tc::tmem_ld_wait();
-                const int64_t col = n0 + c * 32;
-                if (!row_ok || col >= p.N) continue;
-                epi_chunk<T>(p, r, row, col, x);
-                store_chunk<T>(p.out, p.ldout, row, col, x);
-            }
-        } else {
-            float* xs = reinterpret_cast<float*>(smem) + r_local * C::XS_STRIDE;  // reuse the ring
-            float sum = 0.f;
-            for (int c = 0; c < BN / 32; ++c) {
-                tc::tmem_ld32(taddr + c * 32, r);
-                tc::tmem_ld_wait();
-                const int64_t col = n0 + c * 32;
-                if (row_ok) epi_chunk<T>(p, r, row, col, x);
-                else
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) x[j] = 0.f;
-#pragma unroll
-                for (int j = 0; j < 32; j += 4) {
-                    *reinterpret_cast<float4*>(xs + c * 32 + j) = make_float4(x[j], x[j + 1], x[j + 2], x[j + 3]);
-                    sum += (x[j] + x[j + 1]) + (x[j + 2] + x[j + 3]);
+        constexpr int CHUNKS = BN / 32;
+        // non-LN: 8 warps, each lane quarter split in two column halves
+        const int half = LN ? 0 : static_cast<int>((warp - 4) >> 2);
+        const int c_begin = LN ? 0 : half * (CHUNKS / 2);
+        const int c_end = LN ? CHUNKS : c_begin + CHUNKS / 2;
+        int mb, nb;
+        for (int i = 0; tile_of(i, mb, nb); ++i) {
+            const int acc = i & 1;
+            tc::mbar_wait(&tfull[acc], (i >> 1) & 1);
+            tc::fence_after_sync();
+            const uint32_t taddr = tmem + acc * BN + ((q * 32) << 16);
+            const int64_t row = static_cast<int64_t>(mb) * BM + r_local;
+            const bool row_ok = row < p.M;
+            const int n0 = nb * BN;
+            uint32_t r[32];
+            float x[32];
+            if constexpr (!LN) {
+                for (int c = c_begin; c < c_end; ++c) {
+                    tc::tmem_ld32(taddr + c * 32, r);
+                    tc::tmem_ld_wait();
+                    if (c == c_end - 1) {  // accumulator fully read: hand it back to the MMA warp
+                        tc::fence_before_sync();
+                        tc::mbar_arrive(&tempty[acc]);
+                    }
+                    const int64_t col = n0 + c * 32;
+                    if (!row_ok || col >= p.N) continue;
+                    epi_chunk<T>(p, r, row, col, x);
+                    store_chunk<T>(p.out, p.ldout, row, col, x);
                 }
-            }
-            red_sum[r_local] = sum;
-        }
-    }
-    if constexpr (LN) {
-        // Cross-CTA row reductions. Every thread of every CTA in the cluster takes part in the
-        // three cluster barriers (non-epilogue warps simply pass through).
-        const uint32_t nct = gridDim.x;  // cluster spans the full row: cluster dims == (N/BN, 1, 1)
-        tc::cluster_sync_all();
-        float mean = 0.f, inv = 0.f;
-        const bool epi = warp >= 4;
-        const int r_local = static_cast<int>((warp & 3) * 32 + lane);
-        float* xs = reinterpret_cast<float*>(smem) + r_local * C::XS_STRIDE;
-        if (epi) {
-            float tot = 0.f;
-            for (uint32_t c = 0; c < nct; ++c) tot += tc::ld_dsmem_f32(&red_sum[r_local], c);
-            mean = tot / static_cast<float>(p.N);
-            float sq = 0.f;
-            for (int j = 0; j < BN; j += 4) {
-                const float4 v = *reinterpret_cast<const float4*>(xs + j);
-                const float d0 = v.x - mean, d1 = v.y - mean, d2 = v.z - mean, d3 = v.w - mean;
-                sq += (d0 * d0 + d1 * d1) + (d2 * d2 + d3 * d3);
-            }
-            red_sq[r_local] = sq;
-        }
-        tc::cluster_sync_all();
-        if (epi) {
-            float tot = 0.f;
-            for (uint32_t c = 0; c < nct; ++c) tot += tc::ld_dsmem_f32(&red_sq[r_local], c);
-            inv = 1.0f / sqrtf(tot / static_cast<float>(p.N) + kLnEps);
-            const int64_t row = static_cast<int64_t>(blockIdx.y) * BM + r_local;
-            if (row < p.M) {
-                float y[32], xx[32];
-                for (int c = 0; c < BN / 32; ++c) {
+            } else {
+                const int par = i & 1;
+                // pass 1: x = acc + bias (+act) + aux, kept in TMEM; partial Σx
+                float sum = 0.f;
+                for (int c = 0; c < CHUNKS; ++c) {
+                    tc::tmem_ld32(taddr + c * 32, r);
+                    tc::tmem_ld_wait();
+                    if (row_ok) epi_chunk<T>(p, r, row, n0 + c * 32, x);
+                    else
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) x[j] = 0.f;
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        sum += x[j];
+                        r[j] = __float_as_uint(x[j]);
+                    }
+                    tc::tmem_st32(taddr + c * 32, r);
+                }
+                tc::tmem_st_wait();
+                auto exchange = [&](float v, int pass) -> float {
+                    float* slot = red + ((par * 2 + pass) * kMaxCluster) * BM;
+                    slot[me * BM + r_local] = v;
+                    if (nct == 1) return v;
+                    for (uint32_t c = 0; c < nct; ++c)
+                        if (c != me) tc::st_dsmem_f32(&slot[me * BM + r_local], c, v);
+                    for (uint32_t c = 0; c < nct; ++c)
+                        if (c != me) tc::mbar_arrive_cluster(&lnb[par * 2 + pass], c);
+                    tc::mbar_wait_cluster(&lnb[par * 2 + pass], (i >> 1) & 1);
+                    float t = 0.f;
+                    for (uint32_t c = 0; c < nct; ++c) t += slot[c * BM + r_local];
+                    return t;
+                };
+                const float mean = exchange(sum, 0) / static_cast<float>(p.N);
+                // pass 2: Σ(x - mean)^2
+                float sq = 0.f;
+                for (int c = 0; c < CHUNKS; ++c) {
+                    tc::tmem_ld32(taddr + c * 32, r);
+                    tc::tmem_ld_wait();
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        const float d = __uint_as_float(r[j]) - mean;
+                        sq += d * d;
+                    }
+                }
+                const float inv = 1.0f / sqrtf(exchange(sq, 1) / static_cast<float>(p.N) + kLnEps);
+                // pass 3: normalise, store
+                float y[32];
+                for (int c = 0; c < CHUNKS; ++c) {
+                    tc::tmem_ld32(taddr + c * 32, r);
+                    tc::tmem_ld_wait();
+                    if (c == CHUNKS - 1) {
+                        tc::fence_before_sync();
+                        tc::mbar_arrive(&tempty[acc]);
+                    }
+                    if (!row_ok) continue;
                     const int64_t col = n0 + c * 32;
 #pragma unroll
-                    for (int j = 0; j < 32; j += 4) {
-                        const float4 v = *reinterpret_cast<const float4*>(xs + c * 32 + j);
-                        xx[j] = v.x; xx[j + 1] = v.y; xx[j + 2] = v.z; xx[j + 3] = v.w;
+                    for (int j = 0; j < 32; ++j) {
+                        x[j] = __uint_as_float(r[j]);
+                        y[j] = (x[j] - mean) * inv * __ldg(p.gamma + col + j) + __ldg(p.beta + col + j);
                     }
-#pragma unroll
-                    for (int j = 0; j < 32; ++j)
-                        y[j] = (xx[j] - mean) * inv * __ldg(p.gamma + col + j) + __ldg(p.beta + col + j);
                     store_chunk<T>(p.out, p.ldout, row, col, y);
-                    if (p.out_pre_ln) store_chunk<T>(p.out_pre_ln, p.ldout, row, col, xx);
+                    if (p.out_pre_ln) store_chunk<T>(p.out_pre_ln, p.ldout, row, col, x);
                 }
             }
         }
-        tc::cluster_sync_all();  // no CTA leaves while a peer may still read its partials
     }
     tc::fence_before_sync();
     __syncthreads();
-    if (warp == 2) tc::tmem_dealloc<BN>(tmem);
+    if (LN && nct > 1) tc::cluster_sync_all();  // no CTA exits while a peer may still write its smem
+    if (warp == 1) tc::tmem_dealloc<C::TMEM_COLS>(tmem);
+}
+
+int num_sms() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
 }
 
 template <typename T, int BN, bool LN>
 sf_status launch_gemm(const sf_gemm_args& a, cudaStream_t st) {
-    using Cf = Cfg<BN>;
+    using Cf = Cfg<BN, LN>;
     GemmParams p{};
     const bool bf = std::is_same<T, __nv_bfloat16>::value;
     SF_TRY(make_tmap_2d(&p.ta, a.x, a.M, a.K, a.ldx, BK, BM, bf));
@@ -290,20 +356,24 @@ sf_status launch_gemm(const sf_gemm_args& a, cudaStream_t st) {
     p.out_pre_ln = a.epi.out_pre_ln;
     auto kern = gemm_fused_kernel<T, BN, LN>;
     SF_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM));
+    const int m_tiles = static_cast<int>(ceil_div(a.M, BM)), n_tiles = static_cast<int>(ceil_div(a.N, BN));
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(static_cast<unsigned>(ceil_div(a.N, BN)), static_cast<unsigned>(ceil_div(a.M, BM)));
-    cfg.blockDim = dim3(kThreads);
+    cfg.blockDim = dim3(Cf::THREADS);
     cfg.dynamicSmemBytes = Cf::SMEM;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     if (LN) {
-        if (a.N / BN > 8) SF_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        const int nct = n_tiles;  // whole row per cluster
+        const int clusters = std::max(1, std::min(m_tiles, num_sms() / nct));
+        cfg.gridDim = dim3(nct, clusters);
         attr[0].id = cudaLaunchAttributeClusterDimension;
-        attr[0].val.clusterDim.x = static_cast<unsigned>(a.N / BN);
+        attr[0].val.clusterDim.x = static_cast<unsigned>(nct);
         attr[0].val.clusterDim.y = 1;
         attr[0].val.clusterDim.z = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
+    } else {
+        cfg.gridDim = dim3(std::min(m_tiles * n_tiles, num_sms()));
     }
     SF_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, p));
     SF_LAUNCH_CHECK();
@@ -313,10 +383,10 @@ sf_status launch_gemm(const sf_gemm_args& a, cudaStream_t st) {
 template <typename T>
 sf_status gemm_dispatch(const sf_gemm_args& a, cudaStream_t st) {
     const bool ln = a.epi.ln_gamma != nullptr;
-    // widest tile that divides N (LN needs whole rows inside one <= 16-CTA cluster)
+    // widest tile that divides N (LN needs whole rows inside one <= 8-CTA cluster)
     if (ln) {
-        if (a.N % 256 == 0 && a.N / 256 <= 8) return launch_gemm<T, 256, true>(a, st);
-        if (a.N % 128 == 0 && a.N / 128 <= 8) return launch_gemm<T, 128, true>(a, st);
+        if (a.N % 256 == 0 && a.N / 256 <= kMaxCluster) return launch_gemm<T, 256, true>(a, st);
+        if (a.N % 128 == 0 && a.N / 128 <= kMaxCluster) return launch_gemm<T, 128, true>(a, st);
         return fail(SF_SHAPE_ERROR, "fused LayerNorm needs N % 128 == 0 and N <= 2048");
     }
     if (a.N % 256 == 0) return launch_gemm<T, 256, false>(a, st);

@@ -45,7 +45,10 @@ def test_golden_attention_cases(sf, oracle, impl):
             b = sf.build_bsr(dm, bm, bn)
             out, st = sf.block_sparse_sdpa(to_dev(q, torch.float16), to_dev(k, torch.float16),
                                            to_dev(v, torch.float16), b, stats=True)
-            parity(out, z[name + "/out"])
+            try:
+                parity(out, z[name + "/out"])
+            except AssertionError as e:
+                raise AssertionError(f"{name} ({impl}): {e}")
             ref_stats = z[name + "/stats"]
             assert (st["tiles_loaded"], st["full_tiles"], st["part_tiles"]) == tuple(int(x) for x in ref_stats)
     finally:
