@@ -96,6 +96,10 @@ sf_status sf_mask_generate(const sf_mask_desc* terms, int32_t n_terms, uint32_t*
 sf_status sf_mask_pack_u8(const uint8_t* d_mask_u8, int32_t seq_len, uint32_t* d_bits,
                           void* stream);
 
+/* d_acc |= d_src over n rows of sf_mask_words(n) words: compose of arbitrary masks
+ * (mask.hpp:146-166) when they are not all descriptor-generated. */
+sf_status sf_mask_or(const uint32_t* d_src, uint32_t* d_acc, int32_t seq_len, void* stream);
+
 /* Valid-cell count of a device bit mask (DenseMask::true_count, mask.hpp:39-43). Synchronizes. */
 sf_status sf_mask_count(const uint32_t* d_bits, int32_t seq_len, int64_t* count, void* stream);
 
@@ -251,6 +255,7 @@ typedef struct sf_gemm_args {
     const void* w; int64_t ldw;   /* (N x K) row-major */
     void* out; int64_t ldout;
     sf_gemm_epilogue epi;
+    int32_t tile_n;          /* output tile width: 0 = auto, 128 or 256 (a tuning knob, params.hpp) */
 } sf_gemm_args;
 
 /* CiMi template (backend.hpp:240-264): tcgen05 GEMM + fused epilogue. */

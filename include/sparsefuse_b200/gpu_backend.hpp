@@ -1,0 +1,333 @@
+// gpu_backend.hpp — the B200 MeasurementBackend (backend.hpp:391-402): every segment of a fusion
+// scheme runs as the sm_100a fused templates and is timed on the device with CUDA events, with
+// the reference CpuBackend's protocol (3 warm-ups, best of 10; backend.hpp:443-500).
+//
+// Data are the reference's GraphData seeds (backend.hpp:61-107): identical fp32 values, rounded
+// once to fp16 on upload (weights stored transposed, N x K, the K-major operand of tcgen05).
+// The MHA unit follows exec_mha (backend.hpp:327-356): Q = K = V = the activation viewed as
+// (bs, heads, seq, head_size), executed by the plan's kernel (block-wise BSR or row-wise CSR).
+#pragma once
+
+#include <cuda_fp16.h>
+
+#include <functional>
+#include <memory>
+
+#include "search.hpp"
+
+namespace sparsefuse {
+
+// Host copy of GraphData::make(g, seed) (fp32, the reference's shapes and seeds).
+struct GraphData {
+    struct Node {
+        std::vector<float> weight;  // inner x cols (Gemm)
+        std::vector<float> bias, gamma, beta;
+        std::vector<float> aux;     // rows x cols (Add)
+    };
+    std::int64_t rows = 0, in_cols = 0;
+    std::vector<float> input;
+    std::vector<Node> params;
+
+    static std::vector<float> random_matrix(std::int64_t r, std::int64_t c, std::uint64_t seed, float lo = -1.f, float hi = 1.f) {
+        std::vector<float> m(static_cast<std::size_t>(r * c));
+        std::mt19937_64 rng(seed);
+        for (auto& x : m) x = lo + static_cast<float>(unit_real(rng)) * (hi - lo);
+        return m;
+    }
+    static GraphData make(const OpGraph& g, std::uint64_t seed) {
+        GraphData gd;
+        if (g.nodes.empty()) return gd;
+        const OpNode& first = g.nodes.front();
+        gd.rows = first.rows;
+        gd.in_cols = first.kind == OpKind::Gemm ? first.inner : first.cols;
+        gd.input = random_matrix(gd.rows, gd.in_cols, mix_seed(seed, 0xa11));
+        gd.params.resize(g.nodes.size());
+        for (const auto& n : g.nodes) {
+            Node& p = gd.params[static_cast<std::size_t>(n.id)];
+            const std::uint64_t s = mix_seed(seed, static_cast<std::uint64_t>(n.id));
+            std::mt19937_64 rng(s);
+            if (n.kind == OpKind::Gemm) {
+                const float a = 1.0f / std::sqrt(static_cast<float>(n.inner));
+                p.weight = random_matrix(n.inner, n.cols, s, -a, a);
+            } else if (n.kind == OpKind::Bias) {
+                p.bias.resize(static_cast<std::size_t>(n.cols));
+                for (auto& x : p.bias) x = static_cast<float>(unit_real(rng)) - 0.5f;
+            } else if (n.kind == OpKind::LayerNorm) {
+                p.gamma.resize(static_cast<std::size_t>(n.cols));
+                p.beta.resize(static_cast<std::size_t>(n.cols));
+                for (auto& x : p.gamma) x = 0.5f + static_cast<float>(unit_real(rng));
+                for (auto& x : p.beta) x = static_cast<float>(unit_real(rng)) - 0.5f;
+            } else if (n.kind == OpKind::Add) {
+                p.aux = random_matrix(n.rows, n.cols, s);
+            }
+        }
+        return gd;
+    }
+};
+
+class GpuBackend : public MeasurementBackend {
+public:
+    // `mask`/`plan` define the MHA unit (the session mask); without them the reference's default
+    // applies: an all-true mask (backend.hpp:458-467), planned here with the B200 selector.
+    GpuBackend(const OpGraph& g, std::uint64_t seed, std::optional<DenseMask> mask = {}, std::optional<KernelPlan> plan = {},
+               int warmups = 3, int repeats = 10)
+        : g_(g), warmups_(warmups), repeats_(repeats) {
+        cuda_check(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking), "stream");
+        cuda_check(cudaEventCreate(&e0_), "event");
+        cuda_check(cudaEventCreate(&e1_), "event");
+        upload(GraphData::make(g, seed));
+        const auto& hy = g.hyper;
+        if (std::any_of(g.nodes.begin(), g.nodes.end(), [](const OpNode& n) { return n.kind == OpKind::MhaFused; })) {
+            mask_ = mask ? std::move(*mask) : DenseMask(static_cast<int>(hy.seq_len), true);
+            plan_ = plan ? *plan
+                         : select_plan(*mask_, hw_preset("b200"), hy.seq_len, hy.heads, hy.bs, hy.head_size, PlanMode::B200);
+            if (plan_->kind == KernelKind::BlockWise) bsr_ = build_bsr(*mask_, plan_->block_m, plan_->block_n);
+            else rw_ = build_rowwise(*mask_);
+        }
+    }
+    ~GpuBackend() override {
+        cudaStreamSynchronize(st_);
+        cudaEventDestroy(e0_);
+        cudaEventDestroy(e1_);
+        cudaStreamDestroy(st_);
+    }
+
+    double measure(const OpGraph& g, const FusionScheme&, const Segment& seg, const Setting& s) override {
+        check_graph(g);
+        const __half* in = activation(seg.begin);
+        return time_best([&] { exec_segment(seg, s, in, scratch_out_.data()); });
+    }
+    double end_to_end(const OpGraph& g, const FusionScheme& scheme, const ParamAssignment& a) override {
+        check_graph(g);
+        return time_best([&] { run_scheme(scheme, a); });
+    }
+    std::string id() const override { return "b200"; }
+    double accept_margin() const override { return 0.01; }
+
+    // Full chain under a scheme/assignment; the final activation copied to host (fp32).
+    std::vector<float> run_chain(const OpGraph& g, const FusionScheme& scheme, const ParamAssignment& a) {
+        check_graph(g);
+        const __half* y = run_scheme(scheme, a);
+        const std::size_t cnt = static_cast<std::size_t>(g_.nodes.back().rows * g_.nodes.back().cols);
+        std::vector<__half> h(cnt);
+        cuda_check(cudaMemcpyAsync(h.data(), y, cnt * 2, cudaMemcpyDeviceToHost, st_), "D2H");
+        cuda_check(cudaStreamSynchronize(st_), "sync");
+        std::vector<float> out(cnt);
+        for (std::size_t i = 0; i < cnt; ++i) out[i] = __half2float(h[i]);
+        return out;
+    }
+    const std::optional<KernelPlan>& plan() const { return plan_; }
+
+private:
+    struct DevNode {
+        DeviceBuffer<__half> w_nk, aux;
+        DeviceBuffer<float> bias, gamma, beta;
+    };
+
+    void check_graph(const OpGraph& g) const {
+        if (g.name != g_.name || g.size() != g_.size() || g.hyper.bs != g_.hyper.bs || g.hyper.seq_len != g_.hyper.seq_len)
+            throw backend_error("GpuBackend is bound to a different graph");
+    }
+
+    static DeviceBuffer<__half> to_dev_half(const std::vector<float>& v) {
+        std::vector<__half> h(v.size());
+        for (std::size_t i = 0; i < v.size(); ++i) h[i] = __float2half(v[i]);
+        DeviceBuffer<__half> d;
+        d.upload(h.data(), h.size());
+        return d;
+    }
+    static DeviceBuffer<float> to_dev(const std::vector<float>& v) {
+        DeviceBuffer<float> d;
+        d.upload(v.data(), v.size());
+        return d;
+    }
+
+    void upload(const GraphData& gd) {
+        rows_ = gd.rows;
+        std::int64_t widest = gd.in_cols;
+        nodes_.resize(g_.nodes.size());
+        for (const auto& n : g_.nodes) {
+            widest = std::max(widest, n.cols);
+            const auto& p = gd.params[static_cast<std::size_t>(n.id)];
+            DevNode& d = nodes_[static_cast<std::size_t>(n.id)];
+            if (n.kind == OpKind::Gemm) {  // inner x cols -> cols x inner (K-major)
+                std::vector<float> t(p.weight.size());
+                for (std::int64_t k = 0; k < n.inner; ++k)
+                    for (std::int64_t c = 0; c < n.cols; ++c) t[static_cast<std::size_t>(c * n.inner + k)] = p.weight[static_cast<std::size_t>(k * n.cols + c)];
+                d.w_nk = to_dev_half(t);
+            }
+            if (!p.bias.empty()) d.bias = to_dev(p.bias);
+            if (!p.gamma.empty()) { d.gamma = to_dev(p.gamma); d.beta = to_dev(p.beta); }
+            if (!p.aux.empty()) d.aux = to_dev_half(p.aux);
+        }
+        widest_ = widest;
+        input_ = to_dev_half(gd.input);
+        for (auto* b : {&ping_, &pong_, &mid_, &stage_, &scratch_out_})
+            b->resize(static_cast<std::size_t>(rows_ * widest_));
+        cuda_check(cudaDeviceSynchronize(), "upload");
+    }
+
+    // Activation feeding op idx along the unfused chain (default settings), memoised.
+    const __half* activation(int idx) {
+        if (acts_.empty()) acts_.emplace_back();  // slot 0 = the input
+        while (static_cast<int>(acts_.size()) <= idx) {
+            const int i = static_cast<int>(acts_.size());
+            const __half* src = i == 1 ? input_.data() : acts_.back().data();
+            DeviceBuffer<__half> out(static_cast<std::size_t>(rows_ * widest_));
+            const Segment one{i - 1, i};
+            exec_segment(one, default_setting(classify_segment(one, g_)), src, out.data());
+            acts_.push_back(std::move(out));
+        }
+        cuda_check(cudaStreamSynchronize(st_), "activation");
+        return idx == 0 ? input_.data() : acts_[static_cast<std::size_t>(idx)].data();
+    }
+
+    const __half* run_scheme(const FusionScheme& scheme, const ParamAssignment& a) {
+        const __half* x = input_.data();
+        bool flip = false;
+        for (const auto& seg : scheme.segments) {
+            const auto it = a.find(seg);
+            const Setting s = it != a.end() ? it->second : default_setting(classify_segment(seg, g_));
+            __half* y = flip ? pong_.data() : ping_.data();
+            exec_segment(seg, s, x, y);
+            x = y;
+            flip = !flip;
+        }
+        return x;
+    }
+
+    // ---- segment execution on the fused templates ----
+    // MI ops group into the epilogue order bias -> activation -> add -> layernorm; a run that
+    // breaks the order starts a new group (a further one-pass MI-chain launch).
+    struct Group {
+        sf_gemm_epilogue e{};
+        int rank = -1;
+    };
+    std::vector<Group> group_mi(int b, int e) const {
+        std::vector<Group> out;
+        for (int i = b; i < e; ++i) {
+            const OpNode& n = g_.nodes[static_cast<std::size_t>(i)];
+            const DevNode& d = nodes_[static_cast<std::size_t>(i)];
+            int rank;
+            switch (n.kind) {
+                case OpKind::Bias: rank = 0; break;
+                case OpKind::Gelu: case OpKind::Relu: rank = 1; break;
+                case OpKind::Add: rank = 2; break;
+                case OpKind::LayerNorm: rank = 3; break;
+                default: throw backend_error(std::string("no B200 template for MI op ") + to_string(n.kind));
+            }
+            if (out.empty() || rank <= out.back().rank) out.emplace_back();
+            Group& gp = out.back();
+            gp.rank = rank;
+            if (n.kind == OpKind::Bias) gp.e.bias = d.bias.data();
+            if (n.kind == OpKind::Gelu) gp.e.act = SF_ACT_GELU;
+            if (n.kind == OpKind::Relu) gp.e.act = SF_ACT_RELU;
+            if (n.kind == OpKind::Add) { gp.e.aux = d.aux.data(); gp.e.ldaux = n.cols; }
+            if (n.kind == OpKind::LayerNorm) { gp.e.ln_gamma = d.gamma.data(); gp.e.ln_beta = d.beta.data(); }
+        }
+        return out;
+    }
+
+    void mi(const std::vector<Group>& groups, std::size_t from, std::int64_t cols, const __half* x, __half* y) {
+        const __half* src = x;
+        for (std::size_t k = from; k < groups.size(); ++k) {
+            check(sf_mi_chain(static_cast<int32_t>(rows_), static_cast<int32_t>(cols), SF_F16, src, cols, &groups[k].e, y,
+                              cols, st_));
+            src = y;
+        }
+        if (src != y) cuda_check(cudaMemcpyAsync(y, x, static_cast<std::size_t>(rows_ * cols) * 2, cudaMemcpyDeviceToDevice, st_), "copy");
+    }
+
+    void gemm(int node, const Setting& s, const std::vector<Group>& post, const __half* x, __half* y) {
+        const OpNode& n = g_.nodes[static_cast<std::size_t>(node)];
+        sf_gemm_args a{};
+        a.M = static_cast<int32_t>(rows_); a.N = static_cast<int32_t>(n.cols); a.K = static_cast<int32_t>(n.inner);
+        a.dtype = SF_F16;
+        a.x = x; a.ldx = n.inner;
+        a.w = nodes_[static_cast<std::size_t>(node)].w_nk.data(); a.ldw = n.inner;
+        a.out = y; a.ldout = n.cols;
+        a.tile_n = (s.tile_n == 128 || s.tile_n == 256) ? s.tile_n : 0;
+        std::size_t used = 0;
+        if (!post.empty()) {
+            const bool ln = post[0].e.ln_gamma != nullptr;
+            const bool ln_fits = n.cols % 128 == 0 && n.cols <= 2048 && (a.tile_n != 256 || n.cols % 256 == 0);
+            if (!ln || ln_fits) {
+                a.epi = post[0].e;
+                used = 1;
+            }
+        }
+        if (a.epi.ln_gamma && a.tile_n == 128 && n.cols / 128 > 8) a.tile_n = 0;
+        check(sf_gemm_fused(&a, st_));
+        if (used < post.size()) mi(post, used, n.cols, y, y);
+    }
+
+    void exec_segment(const Segment& seg, const Setting& s, const __half* x, __half* y) {
+        if (g_.contains_mha(seg.begin, seg.end)) {
+            if (seg.length() != 1) throw backend_error("MhaFused segment must be a singleton");
+            exec_mha(x, y);
+            return;
+        }
+        std::vector<int> gemms;
+        for (int i = seg.begin; i < seg.end; ++i)
+            if (g_.nodes[static_cast<std::size_t>(i)].kind == OpKind::Gemm) gemms.push_back(i);
+        const std::int64_t in_cols = seg.begin == 0 ? g_.nodes.front().kind == OpKind::Gemm ? g_.nodes.front().inner : g_.nodes.front().cols
+                                                    : g_.nodes[static_cast<std::size_t>(seg.begin) - 1].cols;
+        if (gemms.empty()) {  // MiChain
+            mi(group_mi(seg.begin, seg.end), 0, in_cols, x, y);
+            return;
+        }
+        if (gemms.size() > 2) throw illegal_segment("segment holds more than two CI operators");
+        const __half* src = x;
+        if (gemms[0] > seg.begin) {  // pre-MI ops applied to a staged copy of the input
+            mi(group_mi(seg.begin, gemms[0]), 0, in_cols, x, stage_.data());
+            src = stage_.data();
+        }
+        if (gemms.size() == 1) {  // CiMi
+            gemm(gemms[0], s, group_mi(gemms[0] + 1, seg.end), src, y);
+        } else {  // CiCi: GEMM -> mid MI -> GEMM (intermediate in HBM)
+            gemm(gemms[0], s, group_mi(gemms[0] + 1, gemms[1]), src, mid_.data());
+            gemm(gemms[1], s, group_mi(gemms[1] + 1, seg.end), mid_.data(), y);
+        }
+    }
+
+    void exec_mha(const __half* x, __half* y) {
+        const auto& hy = g_.hyper;
+        const std::int64_t H = static_cast<std::int64_t>(hy.heads) * hy.head_size;
+        if (g_.nodes.front().rows != hy.bs * hy.seq_len) throw shape_error("activation shape incompatible with MHA reshape");
+        sf_attn_args a{static_cast<int32_t>(hy.bs), hy.heads, static_cast<int32_t>(hy.seq_len), hy.head_size, SF_F16,
+                       x, x, x, y, hy.seq_len * H, hy.head_size, H, hy.seq_len * H, hy.head_size, H, 0.f};
+        if (plan_->kind == KernelKind::BlockWise) check(sf_mha_blockwise(&a, &bsr_->device->d, nullptr, nullptr, st_));
+        else check(sf_mha_rowwise(&a, &rw_->device->d, st_));
+    }
+
+    template <typename F>
+    double time_best(F&& f) {
+        for (int i = 0; i < warmups_; ++i) f();
+        float best = std::numeric_limits<float>::infinity();
+        for (int i = 0; i < repeats_; ++i) {
+            cuda_check(cudaEventRecord(e0_, st_), "event");
+            f();
+            cuda_check(cudaEventRecord(e1_, st_), "event");
+            cuda_check(cudaEventSynchronize(e1_), "event");
+            float ms = 0.f;
+            cuda_check(cudaEventElapsedTime(&ms, e0_, e1_), "event");
+            best = std::min(best, ms);
+        }
+        return static_cast<double>(best) * 1e-3;  // seconds, like CpuBackend
+    }
+
+    OpGraph g_;
+    int warmups_, repeats_;
+    cudaStream_t st_{};
+    cudaEvent_t e0_{}, e1_{};
+    std::int64_t rows_ = 0, widest_ = 0;
+    std::vector<DevNode> nodes_;
+    DeviceBuffer<__half> input_, ping_, pong_, mid_, stage_, scratch_out_;
+    std::vector<DeviceBuffer<__half>> acts_;
+    std::optional<DenseMask> mask_;
+    std::optional<KernelPlan> plan_;
+    std::optional<BsrMask> bsr_;
+    std::optional<RowwiseMask> rw_;
+};
+
+}  // namespace sparsefuse

@@ -308,4 +308,33 @@ int ref_exec_segment(const char* model, int64_t bs, int64_t seq, int64_t hidden,
     });
 }
 
+// run_pipeline (search.hpp:514) on the reference SyntheticBackend (backend.hpp:516-671): the
+// canonical report line the C++ host API test prints for its own search.
+int ref_run_pipeline_synthetic(const char* model, int64_t bs, int64_t seq, uint64_t model_seed, uint64_t cfg_seed,
+                               int planted, char* out, int64_t cap) {
+    return guard([&] {
+        GraphHyper hy{bs, seq, 768, 12, 64, 0};
+        const OpGraph g = build_preset_graph(model, hy);
+        SyntheticCostModel m = SyntheticCostModel::random_model(model_seed);
+        if (planted) m.planted = SyntheticCostModel::Planted{{{0, 1}, {1, 5}, {5, 9}, {9, 12}}};
+        SyntheticBackend be(m);
+        SearchConfig cfg;
+        cfg.seed = cfg_seed;
+        TuningCache cache;
+        const TuningReport r = run_pipeline(g, hw_preset("a100"), DenseMask(static_cast<int>(seq), true), be, cfg, cache);
+        std::ostringstream o;
+        o.precision(17);
+        o << "code=" << r.code << ";hex=" << r.code_hex << ";e2e=" << r.end_to_end_s;
+        for (const auto& s : r.segments)
+            o << ";seg=" << s.seg.begin << "-" << s.seg.end << ":" << s.setting.key() << ":" << s.duration << ":"
+              << s.untuned;
+        const auto& t = r.stats;
+        o << ";stats=" << t.measure_calls << "," << t.sample_evals << "," << t.cache_hits << "," << t.e2e_calls << ","
+          << t.e2e_hits << "," << t.schemes_evaluated << "," << t.stage1_accepted << "," << t.stage2_iterations;
+        const std::string s = o.str();
+        std::strncpy(out, s.c_str(), static_cast<size_t>(cap - 1));
+        out[cap - 1] = '\0';
+    });
+}
+
 }  // extern "C"

@@ -86,7 +86,7 @@ class GemmEpilogue(C.Structure):
 class GemmArgs(C.Structure):
     _fields_ = [("M", C.c_int32), ("N", C.c_int32), ("K", C.c_int32), ("dtype", C.c_int32),
                 ("x", C.c_void_p), ("ldx", C.c_int64), ("w", C.c_void_p), ("ldw", C.c_int64),
-                ("out", C.c_void_p), ("ldout", C.c_int64), ("epi", GemmEpilogue)]
+                ("out", C.c_void_p), ("ldout", C.c_int64), ("epi", GemmEpilogue), ("tile_n", C.c_int32)]
 
 
 LAUNCH_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p)
@@ -101,6 +101,7 @@ SIGNATURES = {
     "sf_mask_generate": (C.c_int, [C.POINTER(MaskDesc), _I32, _P, _P]),
     "sf_mask_pack_u8": (C.c_int, [_P, _I32, _P, _P]),
     "sf_mask_count": (C.c_int, [_P, _I32, C.POINTER(_I64), _P]),
+    "sf_mask_or": (C.c_int, [_P, _P, _I32, _P]),
     "sf_bsr_build": (C.c_int, [_P, _I32, _I32, _I32, C.POINTER(BsrDev), _P]),
     "sf_bsr_free": (C.c_int, [C.POINTER(BsrDev), _P]),
     "sf_bsr_to_host": (C.c_int, [C.POINTER(BsrDev)] + [_P] * 8 + [_P]),

@@ -383,7 +383,16 @@ sf_status launch_gemm(const sf_gemm_args& a, cudaStream_t st) {
 template <typename T>
 sf_status gemm_dispatch(const sf_gemm_args& a, cudaStream_t st) {
     const bool ln = a.epi.ln_gamma != nullptr;
-    // widest tile that divides N (LN needs whole rows inside one <= 8-CTA cluster)
+    if (a.tile_n != 0 && a.tile_n != 128 && a.tile_n != 256) return fail(SF_INVALID_PARAMETER, "tile_n must be 0, 128 or 256");
+    if (a.tile_n == 128) {
+        if (ln && (a.N % 128 || a.N / 128 > kMaxCluster)) return fail(SF_SHAPE_ERROR, "LayerNorm row does not fit 128-wide tiles");
+        return ln ? launch_gemm<T, 128, true>(a, st) : launch_gemm<T, 128, false>(a, st);
+    }
+    if (a.tile_n == 256) {
+        if (ln && (a.N % 256 || a.N / 256 > kMaxCluster)) return fail(SF_SHAPE_ERROR, "LayerNorm row does not fit 256-wide tiles");
+        return ln ? launch_gemm<T, 256, true>(a, st) : launch_gemm<T, 256, false>(a, st);
+    }
+    // auto: widest tile that divides N (LN needs whole rows inside one <= 8-CTA cluster)
     if (ln) {
         if (a.N % 256 == 0 && a.N / 256 <= kMaxCluster) return launch_gemm<T, 256, true>(a, st);
         if (a.N % 128 == 0 && a.N / 128 <= kMaxCluster) return launch_gemm<T, 128, true>(a, st);

@@ -246,6 +246,23 @@ extern "C" sf_status sf_mask_pack_u8(const uint8_t* d_mask_u8, int32_t seq_len, 
     return SF_OK;
 }
 
+namespace sf {
+namespace {
+__global__ void or_kernel(const uint32_t* __restrict__ src, uint32_t* __restrict__ acc, int64_t total) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < total) acc[i] |= src[i];
+}
+}  // namespace
+}  // namespace sf
+
+extern "C" sf_status sf_mask_or(const uint32_t* d_src, uint32_t* d_acc, int32_t seq_len, void* stream) {
+    if (seq_len <= 0) return fail(SF_INVALID_PARAMETER, "seq_len must be positive");
+    const int64_t total = static_cast<int64_t>(seq_len) * sf_mask_words(seq_len);
+    or_kernel<<<static_cast<unsigned>(ceil_div(total, 256)), 256, 0, as_stream(stream)>>>(d_src, d_acc, total);
+    SF_LAUNCH_CHECK();
+    return SF_OK;
+}
+
 extern "C" sf_status sf_mask_count(const uint32_t* d_bits, int32_t seq_len, int64_t* count,
                                    void* stream) {
     cudaStream_t st = as_stream(stream);

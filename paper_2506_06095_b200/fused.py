@@ -29,7 +29,8 @@ def epilogue(bias=None, act: str = "none", aux=None, ln_gamma=None, ln_beta=None
 
 
 def gemm_fused(x: torch.Tensor, w_nk: torch.Tensor, out: Optional[torch.Tensor] = None, *, bias=None,
-               act: str = "none", aux=None, ln_gamma=None, ln_beta=None, out_pre_ln=None, stream=None) -> torch.Tensor:
+               act: str = "none", aux=None, ln_gamma=None, ln_beta=None, out_pre_ln=None, tile_n: int = 0,
+               stream=None) -> torch.Tensor:
     """out = LN(act(x @ w_nk.T + bias) + aux) — the CiMi template, one tcgen05 kernel."""
     M, K = x.shape
     N, K2 = w_nk.shape
@@ -41,7 +42,7 @@ def gemm_fused(x: torch.Tensor, w_nk: torch.Tensor, out: Optional[torch.Tensor] 
         if t.stride(1) != 1:
             raise _lib.ShapeError("GEMM operands must be row-major")
     a = GemmArgs(M, N, K, _dtype_code(x), x.data_ptr(), x.stride(0), w_nk.data_ptr(), w_nk.stride(0),
-                 out.data_ptr(), out.stride(0), epilogue(bias, act, aux, ln_gamma, ln_beta, out_pre_ln))
+                 out.data_ptr(), out.stride(0), epilogue(bias, act, aux, ln_gamma, ln_beta, out_pre_ln), tile_n)
     check(lib().sf_gemm_fused(C.byref(a), _stream(stream)))
     return out
 
