@@ -2,22 +2,24 @@
 // Replaces block_sparse_sdpa (attention.hpp:71-172) for BSR tiles of block_m = 128 query rows
 // and block_n in {16, 32, 64} key columns, head_size 64, fp16/bf16.
 //
-// One CTA per (128-row block, b*h slice); 192 threads, 2 CTAs per SM:
-//   warp 0     producer. Lane 0 issues TMA: the Q tile once (128 x 64, 128B-swizzled), then per
+// One CTA per (128-row block, b*h slice); 320 threads, 2 CTAs per SM:
+//   warp 0     producer (one thread): the Q tile once (128 x 64, 128B-swizzled TMA), then per
 //              step the K and V rows of G = 64/block_n load-list column blocks, GATHERED into one
 //              contiguous 64-key stage (4-D tensor maps over (d, n, h, b) read Q/K/V in any
-//              (b,h,i) stride layout in place, e.g. the fused-QKV activation). The packed bit
-//              tiles of the step's PART tiles are bulk-copied from the BSR pool into the same
-//              stage (one transaction barrier); full tiles need no bits.
+//              (b,h,i) stride layout in place, e.g. the fused-QKV activation), plus the packed bit
+//              tiles of the step's PART tiles bulk-copied from the BSR pool (full tiles need no
+//              bits). kStages-deep ring, one transaction barrier per stage.
 //   warp 1     TMEM allocator + MMA issuer (one elected thread):
-//                S_j = Q K_j^T   tcgen05.mma M=128 N=64 K=16 x4 -> TMEM S[j%2] (fp32)
-//                O  += P_j V_j   tcgen05.mma M=128 N=64 K=16 x4 -> TMEM O (fp32, accumulated
-//                                across steps), V read as an MN-major B operand from the stage
-//   warps 2-5  softmax, one thread per query row (TMEM lane): tcgen05.ld S_j, masked row max,
-//              p = 2^(s*scale*log2e - m) with a lazily updated max m (O in TMEM is rescaled only
-//              when the row max grows by more than 2^8, FA4-style, so P <= 256 fits fp16),
-//              P_j (fp16) written 128B-swizzled to smem as the A operand of P.V. 16-column groups
-//              masked for all 32 rows of a warp skip their exp/max work entirely.
+//                S_j = Q K_j^T   tcgen05.mma (SS) M=128 N=64 K=16 x4 -> TMEM S[j%2] (fp32)
+//                O  += P_j V_j   tcgen05.mma (TS) M=128 N=64 K=16 x4, A = P_j read straight from
+//                                TMEM P[j%2] (fp16 pairs), B = V as an MN-major operand from the
+//                                TMA stage; O accumulates in TMEM. No P round trip through smem.
+//   warps 2-9  softmax, two threads per query row (TMEM lane; 32 columns each, the row max is
+//              exchanged through smem per step): tcgen05.ld S_j, masked row max, p = 2^(s*scale*
+//              log2e - m) with a lazily updated max m (O is rescaled in TMEM only when the row max
+//              grows by more than 2^8, FA4-style, so P <= 256 fits fp16), P_j packed to fp16 and
+//              tcgen05.st back into TMEM. 16-column groups masked for all 32 rows of a warp skip
+//              their exp/max work.
 //   epilogue   out = O / l; rows that never saw a valid score are exactly zero
 //              (attention.hpp:160-166).
 // Only the BSR load set is iterated: empty tiles are never touched (attention.hpp:104-109).
@@ -29,16 +31,20 @@ namespace sf {
 namespace {
 
 constexpr int kBM = 128, kD = 64, kNS = 64;  // query rows, head size, keys per step
-constexpr int kThreads = 192;
-constexpr int kStages = 3;
-constexpr int kMaxLoads = 1024;  // load-list entries per row block staged in smem
+constexpr int kThreads = 320;                // producer, MMA, 8 softmax warps
+constexpr int kStages = 5;
+// TMEM columns: S[s] at 64*s (fp32), P[s] at 128 + 32*s (packed fp16 pairs), O at 192. P gets its
+// own buffers: an in-flight P.V MMA may still read P_j while the next S MMA is writing, so P
+// must not alias S. S_{j+2}'s commit covers P_j V_j, so P[j%2] is free again at step j+2.
+constexpr int kSBuf = 2;
+constexpr uint32_t kPCol = 128, kOCol = 192;
+constexpr int kMaxLoads = 512;               // load-list entries per row block (n <= 8192 at bn 16)
 constexpr int kQBytes = kBM * kD * 2;
-constexpr int kKVBytes = kNS * kD * 2;  // one 64-key stage of K (or V)
-constexpr int kPBytes = kBM * kNS * 2;
-constexpr int kMaskBytes = kBM * 8;     // one 64-bit mask row per query row per stage
-constexpr float kRescaleLog2 = 8.0f;    // lazy-rescale threshold (P <= 2^8)
-constexpr int kSmem = 1024 + kQBytes + 2 * kStages * kKVBytes + 2 * kPBytes + kStages * kMaskBytes +
-                      kMaxLoads * 8 + 256;
+constexpr int kKVBytes = kNS * kD * 2;       // one 64-key stage of K (or V)
+constexpr int kMaskBytes = kBM * 8;          // 64 bits per query row per stage
+constexpr float kRescaleLog2 = 8.0f;         // lazy-rescale threshold (P <= 2^8)
+constexpr int kSmem = 1024 + kQBytes + 2 * kStages * kKVBytes + kStages * kMaskBytes + kMaxLoads * 8 +
+                      6 * kBM * 4 + 512;
 
 struct AttnParams {
     CUtensorMap tq, tk, tv;  // 4-D (d, n, h, b) maps; boxes {64,128,1,1} / {64,bn,1,1}
@@ -81,6 +87,18 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* m, uin
         : "memory");
 }
 
+__device__ __forceinline__ void named_sync(uint32_t id, uint32_t n) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void st_shared_f32(uint32_t addr, float v) {
+    asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
+}
+__device__ __forceinline__ float ld_shared_f32(uint32_t addr) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
+    return v;
+}
+
 template <typename T>
 __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_constant__ AttnParams p) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -88,18 +106,18 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
     unsigned char* sQ = sm;
     unsigned char* sK = sQ + kQBytes;
     unsigned char* sV = sK + kStages * kKVBytes;
-    unsigned char* sP = sV + kStages * kKVBytes;
-    uint64_t* sMask = reinterpret_cast<uint64_t*>(sP + 2 * kPBytes);  // [kStages][128]
-    int32_t* s_col = reinterpret_cast<int32_t*>(sMask + kStages * kBM);
+    unsigned char* sMask = sV + kStages * kKVBytes;  // [kStages][1 KB]: packed part-tile bits
+    int32_t* s_col = reinterpret_cast<int32_t*>(sMask + kStages * kMaskBytes);
     int32_t* s_tile = s_col + kMaxLoads;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(s_tile + kMaxLoads);
+    float* s_red = reinterpret_cast<float*>(s_tile + kMaxLoads);  // [3][2][128]: max exchange x2, final l
+    uint64_t* bars = reinterpret_cast<uint64_t*>(s_red + 6 * kBM);
     uint64_t* q_full = bars;
-    uint64_t* kv_full = bars + 1;
-    uint64_t* kv_empty = kv_full + kStages;
-    uint64_t* s_full = kv_empty + kStages;  // [2]
-    uint64_t* p_full = s_full + 2;          // [2]
-    uint64_t* o_full = p_full + 2;          // [2]: P.V step j completes o_full[j&1] (a parity wait
-                                            // is only unambiguous within one phase of lag)
+    uint64_t* kv_full = q_full + 1;          // [kStages]
+    uint64_t* kv_empty = kv_full + kStages;  // [kStages]
+    uint64_t* s_full = kv_empty + kStages;   // [kSBuf]
+    uint64_t* p_full = s_full + kSBuf;       // [kSBuf]
+    uint64_t* o_full = p_full + kSBuf;       // [2]: P.V step j completes o_full[j&1] (parity waits are
+                                             // unambiguous only within one phase of lag)
     uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(o_full + 2);
 
     const uint32_t warp = tc::warp_id();
@@ -124,9 +142,9 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
             tc::mbar_init(&kv_full[s], 1);
             tc::mbar_init(&kv_empty[s], 1);
         }
-        for (int s = 0; s < 2; ++s) {
+        for (int s = 0; s < kSBuf; ++s) {
             tc::mbar_init(&s_full[s], 1);
-            tc::mbar_init(&p_full[s], 128);
+            tc::mbar_init(&p_full[s], 256);
         }
         tc::mbar_init(&o_full[0], 1);
         tc::mbar_init(&o_full[1], 1);
@@ -136,7 +154,8 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
     tc::fence_before_sync();
     __syncthreads();
     tc::fence_after_sync();
-    const uint32_t tmem = *tmem_ptr;  // S[0] @ +0, S[1] @ +64, O @ +128
+    const uint32_t tmem = *tmem_ptr;
+    const uint32_t tO = tmem + kOCol;
 
     if (warp == 0) {
         // ------------------------------------------------------------------ producer
@@ -160,10 +179,9 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
                     const int col = (e < L ? s_col[e] : s_col[0]) * bn;  // pad: valid, fully masked
                     tma_load_4d(sK + s * kKVBytes + g * chunk, &p.tk, &kv_full[s], 0, col, hh, b);
                     tma_load_4d(sV + s * kKVBytes + g * chunk, &p.tv, &kv_full[s], 0, col, hh, b);
-                    if (e < L && s_tile[e] >= 0)  // the part tile's packed bits (bsr pool) -> stage
-                        tc::bulk_load(reinterpret_cast<unsigned char*>(sMask) + s * kMaskBytes + g * p.tile_bytes,
-                                      p.pool + static_cast<int64_t>(s_tile[e]) * p.tile_bytes, p.tile_bytes,
-                                      &kv_full[s]);
+                    if (e < L && s_tile[e] >= 0)
+                        tc::bulk_load(sMask + s * kMaskBytes + g * p.tile_bytes,
+                                      p.pool + static_cast<int64_t>(s_tile[e]) * p.tile_bytes, p.tile_bytes, &kv_full[s]);
                 }
                 if (++s == kStages) { s = 0; ph ^= 1; }
             }
@@ -172,7 +190,7 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
         // ------------------------------------------------------------------ MMA issuer
         constexpr bool bf = std::is_same<T, __nv_bfloat16>::value;
         constexpr uint32_t idesc_s = tc::idesc_f16(kBM, kNS, bf, 0, 0);  // Q (K-major) x K (K-major)
-        constexpr uint32_t idesc_o = tc::idesc_f16(kBM, kD, bf, 0, 1);   // P (K-major) x V (MN-major)
+        constexpr uint32_t idesc_o = tc::idesc_f16(kBM, kD, bf, 0, 1);   // P (TMEM) x V (MN-major)
         if (tc::elect_one() && nsteps > 0) {
             const uint32_t q0 = tc::smem_u32(sQ);
             tc::mbar_wait(q_full, 0);
@@ -183,44 +201,49 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
                 const uint32_t k0 = tc::smem_u32(sK + s * kKVBytes);
 #pragma unroll
                 for (int k = 0; k < kD / 16; ++k)
-                    tc::mma_f16_ss(tmem + (j & 1) * 64, tc::sdesc_sw128(q0 + 32 * k), tc::sdesc_sw128(k0 + 32 * k),
+                    tc::mma_f16_ss(tmem + 64 * (j % kSBuf), tc::sdesc_sw128(q0 + 32 * k), tc::sdesc_sw128(k0 + 32 * k),
                                    idesc_s, k != 0);
-                tc::mma_commit(&s_full[j & 1]);
+                tc::mma_commit(&s_full[j % kSBuf]);
             };
-            issue_s(0);
-            if (nsteps > 1) issue_s(1);
+            for (int j = 0; j < kSBuf && j < nsteps; ++j) issue_s(j);
             for (int j = 0; j < nsteps; ++j) {
                 const int s = j % kStages;
-                tc::mbar_wait(&p_full[j & 1], (j >> 1) & 1);  // P_j in smem, S[j&1] consumed, O rescaled
+                const int sb = j % kSBuf;
+                tc::mbar_wait(&p_full[sb], (j / kSBuf) & 1);  // P_j in TMEM (S_j consumed), O rescaled
                 tc::fence_after_sync();
-                const uint32_t pa = tc::smem_u32(sP + (j & 1) * kPBytes);
                 const uint32_t v0 = tc::smem_u32(sV + s * kKVBytes);
 #pragma unroll
-                for (int k = 0; k < kNS / 16; ++k)
-                    tc::mma_f16_ss(tmem + 128, tc::sdesc_sw128(pa + 32 * k), tc::sdesc_sw128_mn(v0 + 2048 * k),
-                                   idesc_o, (j | k) != 0);
+                for (int k = 0; k < kNS / 16; ++k)  // P_j: 64 keys = 32 packed columns, 8 per K=16
+                    tc::mma_f16_ts(tO, tmem + kPCol + 32 * sb + 8 * k, tc::sdesc_sw128_mn(v0 + 2048 * k), idesc_o,
+                                   (j | k) != 0);
                 tc::mma_commit(&o_full[j & 1]);
                 tc::mma_commit(&kv_empty[s]);
-                if (j + 2 < nsteps) issue_s(j + 2);
+                if (j + kSBuf < nsteps) issue_s(j + kSBuf);
             }
         }
     } else {
         // ------------------------------------------------------------------ softmax / epilogue
+        // Two threads per query row: warps 2-5 own columns 0-31 of the step, warps 6-9 columns
+        // 32-63, of TMEM lane quarter warp%4. The row max is exchanged through smem with a
+        // 64-thread named barrier per lane quarter; row sums stay per-half until the end.
         const uint32_t q = warp & 3;
+        const int half = static_cast<int>(warp - 2) >> 2;
         const int r = static_cast<int>(q * 32 + lane);
         const uint32_t trow = tmem + ((q * 32) << 16);
+        const uint32_t bar_id = 1 + q;
+        const uint32_t red = tc::smem_u32(s_red);
         const float sl2 = p.scale_log2;
         float m = -INFINITY, l = 0.f;
-        unsigned char* prow_base = sP + r * 128;
-        const int rsw = r & 7;
         for (int j = 0; j < nsteps; ++j) {
             const int st = j % kStages;
+            const int sb = j % kSBuf;
             tc::mbar_wait(&kv_full[st], (j / kStages) & 1);
-            // this row's 64 mask bits: full tile -> ones, part tile -> staged pool row, pad -> 0
-            uint64_t bits = 0;
+            // this thread's 32 mask bits: full tile -> ones, part tile -> staged pool row, pad -> 0
+            uint32_t bits;
             {
                 const int bn = p.bn;
-                const unsigned char* mrow = reinterpret_cast<const unsigned char*>(sMask) + st * kMaskBytes + r * (bn >> 3);
+                const unsigned char* mrow = sMask + st * kMaskBytes + r * (bn >> 3);
+                uint64_t all = 0;
                 for (int g = 0; g < p.G; ++g) {
                     const int e = j * p.G + g;
                     const int t = e < L ? s_tile[e] : -2;
@@ -233,37 +256,39 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
                                       : (bn == 32 ? *reinterpret_cast<const uint32_t*>(tp)
                                                   : *reinterpret_cast<const uint64_t*>(tp));
                     }
-                    bits |= gb << (g * bn);
+                    all |= gb << (g * bn);
                 }
+                bits = static_cast<uint32_t>(all >> (32 * half));
             }
-            tc::mbar_wait(&s_full[j & 1], (j >> 1) & 1);
+            tc::mbar_wait(&s_full[sb], (j / kSBuf) & 1);
             tc::fence_after_sync();
-            uint32_t lo[32], hi[32];
-            tc::tmem_ld32(trow + (j & 1) * 64, lo);
-            tc::tmem_ld32(trow + (j & 1) * 64 + 32, hi);
-            // warp-uniform activity of the four 16-column groups
-            uint32_t gact = 0;
-#pragma unroll
-            for (int g = 0; g < 4; ++g)
-                if (__any_sync(0xffffffffu, ((bits >> (16 * g)) & 0xffffull) != 0)) gact |= 1u << g;
+            uint32_t raw[32];
+            tc::tmem_ld32(trow + 64 * sb + 32 * half, raw);
+            const bool act0 = __any_sync(0xffffffffu, (bits & 0xffffu) != 0);
+            const bool act1 = __any_sync(0xffffffffu, (bits >> 16) != 0);
             tc::tmem_ld_wait();
-            float sr[64];
+            float sr[32];
 #pragma unroll
-            for (int c = 0; c < 32; ++c) {
-                sr[c] = __uint_as_float(lo[c]) * sl2;
-                sr[c + 32] = __uint_as_float(hi[c]) * sl2;
+            for (int c = 0; c < 32; ++c) sr[c] = __uint_as_float(raw[c]) * sl2;
+            float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+            if (act0) {
+#pragma unroll
+                for (int c = 0; c < 16; ++c)
+                    if ((bits >> c) & 1u) mx4[c & 3] = fmaxf(mx4[c & 3], sr[c]);
             }
-            float mx = -INFINITY;
+            if (act1) {
 #pragma unroll
-            for (int g = 0; g < 4; ++g) {
-                if (!(gact & (1u << g))) continue;
-#pragma unroll
-                for (int c = 16 * g; c < 16 * g + 16; ++c)
-                    if ((bits >> c) & 1ull) mx = fmaxf(mx, sr[c]);
+                for (int c = 16; c < 32; ++c)
+                    if ((bits >> c) & 1u) mx4[c & 3] = fmaxf(mx4[c & 3], sr[c]);
             }
-            // lazy max update: rescale O / l only when the max grows by > 2^8 (or first time).
-            // tcgen05.ld/st are warp-collective, so the rescale is voted warp-uniformly and
-            // lanes that do not need it scale by 1.
+            float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
+            const uint32_t xch = red + 4u * ((j & 1) * 2 * kBM);  // [2 halves][128], double-buffered
+            st_shared_f32(xch + 4u * (half * kBM + r), mx);
+            named_sync(bar_id, 64);  // also orders both halves' S loads before any P store below
+            mx = fmaxf(mx, ld_shared_f32(xch + 4u * ((1 - half) * kBM + r)));
+            // lazy max update (identical in both halves): rescale O / l only when the max grows by
+            // > 2^8 (or first time). tcgen05.ld/st are warp-collective: the rescale is voted
+            // warp-uniformly and lanes that do not need it scale by 1.
             const bool upd = mx > m + kRescaleLog2 || (m == -INFINITY && mx > -INFINITY);
             const float m_new = upd ? mx : m;
             const bool resc = upd && m > -INFINITY && j > 0;
@@ -273,63 +298,57 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
                 tc::mbar_wait(&o_full[(j - 1) & 1], ((j - 1) >> 1) & 1);  // P_{j-1} V_{j-1} landed in O
                 tc::fence_after_sync();
                 uint32_t ov[32];
+                tc::tmem_ld32(tO + ((q * 32) << 16) + 32 * half, ov);
+                tc::tmem_ld_wait();
 #pragma unroll
-                for (int h2 = 0; h2 < 2; ++h2) {
-                    tc::tmem_ld32(trow + 128 + h2 * 32, ov);
-                    tc::tmem_ld_wait();
-#pragma unroll
-                    for (int e = 0; e < 32; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * a);
-                    tc::tmem_st32(trow + 128 + h2 * 32, ov);
-                }
-                tc::tmem_st_wait();
+                for (int e = 0; e < 32; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * a);
+                tc::tmem_st32(tO + ((q * 32) << 16) + 32 * half, ov);
             }
             m = m_new;
-            uint32_t pk[32];
-            float rs = 0.f;
+            uint32_t pk[16];
+            float rs4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-            for (int g = 0; g < 4; ++g) {
-                if (!(gact & (1u << g)) || m == -INFINITY) {
+            for (int g = 0; g < 2; ++g) {
+                if (!(g ? act1 : act0) || m == -INFINITY) {
 #pragma unroll
                     for (int c = 8 * g; c < 8 * g + 8; ++c) pk[c] = 0u;
                     continue;
                 }
 #pragma unroll
                 for (int c = 16 * g; c < 16 * g + 16; c += 2) {
-                    const float p0 = ((bits >> c) & 1ull) ? ex2(sr[c] - m) : 0.f;
-                    const float p1 = ((bits >> (c + 1)) & 1ull) ? ex2(sr[c + 1] - m) : 0.f;
-                    rs += p0 + p1;
+                    const float p0 = ((bits >> c) & 1u) ? ex2(sr[c] - m) : 0.f;
+                    const float p1 = ((bits >> (c + 1)) & 1u) ? ex2(sr[c + 1] - m) : 0.f;
+                    rs4[(c >> 1) & 3] += p0 + p1;
                     pk[c >> 1] = pack2<T>(p0, p1);
                 }
             }
-            l += rs;
-            // P_j row -> smem, 128B-swizzled K-major A operand (row r: 8 chunks of 16 B)
-            unsigned char* prow = prow_base + (j & 1) * kPBytes;
-#pragma unroll
-            for (int c = 0; c < 8; ++c)
-                *reinterpret_cast<uint4*>(prow + ((c ^ rsw) << 4)) =
-                    make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
-            tc::fence_proxy_async();
+            l += (rs4[0] + rs4[1]) + (rs4[2] + rs4[3]);
+            // P_j (this half: keys 32h..32h+31 = packed columns 16h..16h+15) into P[sb] in TMEM
+            tc::tmem_st16(trow + kPCol + 32 * sb + 16 * half, pk);
+            tc::tmem_st_wait();
             tc::fence_before_sync();
-            tc::mbar_arrive(&p_full[j & 1]);
+            tc::mbar_arrive(&p_full[sb]);
         }
-        // ---- epilogue: out = O / l; rows without a valid column stay exactly zero
+        // ---- epilogue: out = O / (l_half0 + l_half1); rows without a valid column stay zero
+        st_shared_f32(red + 4u * (4 * kBM + half * kBM + r), l);
+        named_sync(bar_id, 64);
+        l += ld_shared_f32(red + 4u * (4 * kBM + (1 - half) * kBM + r));
         const int64_t i = static_cast<int64_t>(br) * kBM + r;
-        uint32_t ov[2][32];
+        uint32_t ov[32];
         if (nsteps > 0) {
             tc::mbar_wait(&o_full[(nsteps - 1) & 1], ((nsteps - 1) >> 1) & 1);
             tc::fence_after_sync();
-            tc::tmem_ld32(trow + 128, ov[0]);
-            tc::tmem_ld32(trow + 128 + 32, ov[1]);
+            tc::tmem_ld32(tO + ((q * 32) << 16) + 32 * half, ov);
             tc::tmem_ld_wait();
         }
         if (i < p.n) {
             const float inv = l > 0.f ? 1.f / l : 0.f;
-            uint4* dst = reinterpret_cast<uint4*>(static_cast<T*>(p.o) + b * p.o_sb + hh * p.o_sh + i * p.o_sn);
+            uint4* dst = reinterpret_cast<uint4*>(static_cast<T*>(p.o) + b * p.o_sb + hh * p.o_sh + i * p.o_sn + 32 * half);
 #pragma unroll
-            for (int c = 0; c < 8; ++c) {
+            for (int c = 0; c < 4; ++c) {
                 float v[8];
 #pragma unroll
-                for (int e = 0; e < 8; ++e) v[e] = nsteps > 0 ? __uint_as_float(ov[c >> 2][(c & 3) * 8 + e]) * inv : 0.f;
+                for (int e = 0; e < 8; ++e) v[e] = nsteps > 0 ? __uint_as_float(ov[c * 8 + e]) * inv : 0.f;
                 dst[c] = make_uint4(pack2<T>(v[0], v[1]), pack2<T>(v[2], v[3]), pack2<T>(v[4], v[5]),
                                     pack2<T>(v[6], v[7]));
             }
