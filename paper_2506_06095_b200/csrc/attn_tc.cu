@@ -57,7 +57,13 @@ struct AttnParams {
     void* o;
     int64_t o_sb, o_sh, o_sn;
     float scale_log2;
+    unsigned long long* trace;  // optional clock64 trace of CTA (0,0) (sf_debug_attn_trace)
 };
+
+#define SF_TRACE(j, ev)                                                                   \
+    do {                                                                                  \
+        if (p.trace && blockIdx.x == 0 && blockIdx.y == 0 && (j) < 64) p.trace[(j) * 16 + (ev)] = clock64(); \
+    } while (0)
 
 __device__ __forceinline__ float ex2(float x) {
     float y;
@@ -76,6 +82,32 @@ template <>
 __device__ __forceinline__ uint32_t pack2<__nv_bfloat16>(float a, float b) {
     __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
     return *reinterpret_cast<uint32_t*>(&h);
+}
+
+// 2^x on a packed pair of 16-bit values (one MUFU op for two exponentials)
+template <typename T>
+__device__ __forceinline__ uint32_t ex2x2(uint32_t x);
+template <>
+__device__ __forceinline__ uint32_t ex2x2<__half>(uint32_t x) {
+    uint32_t y;
+    asm("ex2.approx.f16x2 %0, %1;" : "=r"(y) : "r"(x));
+    return y;
+}
+template <>
+__device__ __forceinline__ uint32_t ex2x2<__nv_bfloat16>(uint32_t x) {
+    uint32_t y;
+    asm("ex2.approx.ftz.bf16x2 %0, %1;" : "=r"(y) : "r"(x));
+    return y;
+}
+template <typename T>
+__device__ __forceinline__ float2 unpack2(uint32_t v);
+template <>
+__device__ __forceinline__ float2 unpack2<__half>(uint32_t v) {
+    return __half22float2(*reinterpret_cast<__half2*>(&v));
+}
+template <>
+__device__ __forceinline__ float2 unpack2<__nv_bfloat16>(uint32_t v) {
+    return __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&v));
 }
 
 __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* m, uint64_t* bar, int32_t c0, int32_t c1,
@@ -210,6 +242,7 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
                 const int s = j % kStages;
                 const int sb = j % kSBuf;
                 tc::mbar_wait(&p_full[sb], (j / kSBuf) & 1);  // P_j in TMEM (S_j consumed), O rescaled
+                SF_TRACE(j, 8);
                 tc::fence_after_sync();
                 const uint32_t v0 = tc::smem_u32(sV + s * kKVBytes);
 #pragma unroll
@@ -218,7 +251,16 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
                                    (j | k) != 0);
                 tc::mma_commit(&o_full[j & 1]);
                 tc::mma_commit(&kv_empty[s]);
+                SF_TRACE(j, 9);
                 if (j + kSBuf < nsteps) issue_s(j + kSBuf);
+                SF_TRACE(j, 10);
+                if (p.trace && blockIdx.x == 0 && blockIdx.y == 0 && j + kSBuf < nsteps) {
+                    // diagnosis only: observe this thread's own S commit (pure MMA-chain latency)
+                    tc::mbar_wait(&s_full[(j + kSBuf) % kSBuf], ((j + kSBuf) / kSBuf) & 1);
+                    SF_TRACE(j, 11);
+                    tc::mbar_wait(&o_full[j & 1], (j >> 1) & 1);
+                    SF_TRACE(j, 12);
+                }
             }
         }
     } else {
@@ -237,7 +279,10 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
         for (int j = 0; j < nsteps; ++j) {
             const int st = j % kStages;
             const int sb = j % kSBuf;
+            const bool tr = warp == 2 && lane == 0;
+            if (tr) SF_TRACE(j, 0);
             tc::mbar_wait(&kv_full[st], (j / kStages) & 1);
+            if (tr) SF_TRACE(j, 1);
             // this thread's 32 mask bits: full tile -> ones, part tile -> staged pool row, pad -> 0
             uint32_t bits;
             {
@@ -261,30 +306,33 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
                 bits = static_cast<uint32_t>(all >> (32 * half));
             }
             tc::mbar_wait(&s_full[sb], (j / kSBuf) & 1);
+            if (tr) SF_TRACE(j, 2);
             tc::fence_after_sync();
             uint32_t raw[32];
             tc::tmem_ld32(trow + 64 * sb + 32 * half, raw);
             const bool act0 = __any_sync(0xffffffffu, (bits & 0xffffu) != 0);
             const bool act1 = __any_sync(0xffffffffu, (bits >> 16) != 0);
             tc::tmem_ld_wait();
+            // masked cells -> -inf once: they drop out of the max and ex2(-inf) = 0 later
             float sr[32];
 #pragma unroll
-            for (int c = 0; c < 32; ++c) sr[c] = __uint_as_float(raw[c]) * sl2;
+            for (int c = 0; c < 32; ++c) sr[c] = (bits & (1u << c)) ? __uint_as_float(raw[c]) : -INFINITY;
             float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
             if (act0) {
 #pragma unroll
-                for (int c = 0; c < 16; ++c)
-                    if ((bits >> c) & 1u) mx4[c & 3] = fmaxf(mx4[c & 3], sr[c]);
+                for (int c = 0; c < 16; ++c) mx4[c & 3] = fmaxf(mx4[c & 3], sr[c]);
             }
             if (act1) {
 #pragma unroll
-                for (int c = 16; c < 32; ++c)
-                    if ((bits >> c) & 1u) mx4[c & 3] = fmaxf(mx4[c & 3], sr[c]);
+                for (int c = 16; c < 32; ++c) mx4[c & 3] = fmaxf(mx4[c & 3], sr[c]);
             }
-            float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
+            // max of the raw scores, then scaled: scale > 0 commutes with max (log2 domain)
+            float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * sl2;
             const uint32_t xch = red + 4u * ((j & 1) * 2 * kBM);  // [2 halves][128], double-buffered
             st_shared_f32(xch + 4u * (half * kBM + r), mx);
+            if (tr) SF_TRACE(j, 3);
             named_sync(bar_id, 64);  // also orders both halves' S loads before any P store below
+            if (tr) SF_TRACE(j, 4);
             mx = fmaxf(mx, ld_shared_f32(xch + 4u * ((1 - half) * kBM + r)));
             // lazy max update (identical in both halves): rescale O / l only when the max grows by
             // > 2^8 (or first time). tcgen05.ld/st are warp-collective: the rescale is voted
@@ -316,8 +364,8 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
                 }
 #pragma unroll
                 for (int c = 16 * g; c < 16 * g + 16; c += 2) {
-                    const float p0 = ((bits >> c) & 1u) ? ex2(sr[c] - m) : 0.f;
-                    const float p1 = ((bits >> (c + 1)) & 1u) ? ex2(sr[c + 1] - m) : 0.f;
+                    const float p0 = ex2(fmaf(sr[c], sl2, -m));  // masked: ex2(-inf) = 0
+                    const float p1 = ex2(fmaf(sr[c + 1], sl2, -m));
                     rs4[(c >> 1) & 3] += p0 + p1;
                     pk[c >> 1] = pack2<T>(p0, p1);
                 }
@@ -328,6 +376,7 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
             tc::tmem_st_wait();
             tc::fence_before_sync();
             tc::mbar_arrive(&p_full[sb]);
+            if (tr) SF_TRACE(j, 6);
         }
         // ---- epilogue: out = O / (l_half0 + l_half1); rows without a valid column stay zero
         st_shared_f32(red + 4u * (4 * kBM + half * kBM + r), l);
@@ -385,6 +434,8 @@ sf_status make_tmap_4d(CUtensorMap* map, const void* base, int n, int h, int bs,
 
 }  // namespace
 
+unsigned long long* g_attn_trace = nullptr;
+
 sf_status attn_tc(const sf_attn_args& a, const sf_bsr_dev& b, cudaStream_t st, bool probe_only) {
     const bool shape_ok = b.block_m == kBM && (b.block_n == 16 || b.block_n == 32 || b.block_n == 64) &&
                           a.head_size == kD && b.n_cols <= kMaxLoads;
@@ -415,6 +466,7 @@ sf_status attn_tc(const sf_attn_args& a, const sf_bsr_dev& b, cudaStream_t st, b
     p.o_sh = a.o_sh;
     p.o_sn = a.o_sn;
     p.scale_log2 = a.scale * 1.4426950408889634f;
+    p.trace = g_attn_trace;
     auto kern = bf ? attn_tc_kernel<__nv_bfloat16> : attn_tc_kernel<__half>;
     SF_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
     dim3 grid(b.n_rows, static_cast<unsigned>(a.bs) * a.h);
@@ -424,3 +476,10 @@ sf_status attn_tc(const sf_attn_args& a, const sf_bsr_dev& b, cudaStream_t st, b
 }
 
 }  // namespace sf
+
+// Debug hook (not part of the boundary): record clock64 timestamps of CTA (0,0) of subsequent
+// tcgen05 attention launches into a device buffer of >= 64*16 uint64 (NULL disables).
+extern "C" sf_status sf_debug_attn_trace(void* dev_buf) {
+    sf::g_attn_trace = static_cast<unsigned long long*>(dev_buf);
+    return SF_OK;
+}

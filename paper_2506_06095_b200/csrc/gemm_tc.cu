@@ -42,16 +42,17 @@ struct GemmParams {
     const float* gamma;
     const float* beta;
     void* out_pre_ln;
+    int32_t mc;  // non-LN: CTAs per cluster along M sharing (multicasting) the weight tile
 };
 
 template <int BN, bool LN>
 struct Cfg {
     static constexpr int STAGES = BN == 256 ? 4 : 6;
-    static constexpr int EPI_WARPS = LN ? 4 : 8;
+    static constexpr int EPI_WARPS = LN ? 8 : 16;  // per lane quarter: 2 (LN) or 4 column groups
     static constexpr int THREADS = 128 + 32 * EPI_WARPS;
     static constexpr int A_BYTES = BM * BK * 2;
     static constexpr int B_BYTES = BN * BK * 2;
-    static constexpr int RED_FLOATS = LN ? 2 * 2 * kMaxCluster * BM : 0;
+    static constexpr int RED_FLOATS = LN ? 2 * 2 * kMaxCluster * 2 * BM : 0;  // [par][pass][cta][half][row]
     static constexpr int SMEM = STAGES * (A_BYTES + B_BYTES) + 1024 /*align*/ + 256 /*barriers*/ + RED_FLOATS * 4;
     static constexpr int TMEM_COLS = 2 * BN;  // two accumulator buffers
 };
@@ -69,10 +70,64 @@ __device__ __forceinline__ uint32_t pack2<__nv_bfloat16>(float a, float b) {
     return *reinterpret_cast<uint32_t*>(&h);
 }
 
+// erf via Abramowitz & Stegun 7.1.26 (|error| <= 1.5e-7, far below the fp16 output rounding):
+// branch-free, one MUFU reciprocal + one MUFU exp2 + 7 FMAs instead of erff's ~20-instruction,
+// divergent two-regime evaluation. The exact-erf GELU semantics of the reference are kept.
+__device__ __forceinline__ float erf_as(float x) {
+    const float z = fabsf(x);
+    float t;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(t) : "f"(fmaf(0.3275911f, z, 1.0f)));
+    float poly = fmaf(1.061405429f, t, -1.453152027f);
+    poly = fmaf(poly, t, 1.421413741f);
+    poly = fmaf(poly, t, -0.284496736f);
+    poly = fmaf(poly, t, 0.254829592f);
+    poly *= t;
+    float e;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(-z * z * 1.4426950408889634f));
+    return copysignf(fmaf(-poly, e, 1.0f), x);
+}
+
 __device__ __forceinline__ float act_fn(float x, int act) {
-    if (act == SF_ACT_GELU) return 0.5f * x * (1.0f + erff(x * 0.7071067811865475f));  // backend.hpp:128-131
-    if (act == SF_ACT_RELU) return x > 0.f ? x : 0.f;                                  // backend.hpp:132-134
+    if (act == SF_ACT_GELU) return 0.5f * x * (1.0f + erf_as(x * 0.7071067811865475f));  // backend.hpp:128-131
+    if (act == SF_ACT_RELU) return x > 0.f ? x : 0.f;                                    // backend.hpp:132-134
     return x;
+}
+
+// residual values of row `row`, columns [col, col+32) (issued one chunk ahead of their use)
+template <typename T>
+__device__ __forceinline__ void load_aux(const GemmParams& p, bool ok, int64_t row, int64_t col, uint4 (&a)[4]) {
+    if (!p.aux || !ok) return;
+    const uint4* a4 = reinterpret_cast<const uint4*>(static_cast<const T*>(p.aux) + row * p.ldaux + col);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) a[j] = __ldg(a4 + j);
+}
+
+// 32 consecutive values: bias -> act -> + prefetched residual.
+template <typename T>
+__device__ __forceinline__ void epi_chunk_pre(const GemmParams& p, const uint32_t (&r)[32], int64_t col,
+                                              const uint4 (&aux)[4], float (&x)[32]) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) x[j] = __uint_as_float(r[j]);
+    if (p.bias) {
+        const float4* b4 = reinterpret_cast<const float4*>(p.bias + col);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const float4 b = __ldg(b4 + j);
+            x[4 * j] += b.x; x[4 * j + 1] += b.y; x[4 * j + 2] += b.z; x[4 * j + 3] += b.w;
+        }
+    }
+    if (p.act) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) x[j] = act_fn(x[j], p.act);
+    }
+    if (p.aux) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const T* h = reinterpret_cast<const T*>(&aux[j]);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) x[8 * j + e] += DT<T>::to_f(h[e]);
+        }
+    }
 }
 
 // 32 consecutive values of row `row`, columns [col, col+32): bias -> act -> +aux.
@@ -140,7 +195,11 @@ __global__ void __launch_bounds__(Cfg<BN, LN>::THREADS, 1) gemm_fused_kernel(con
     const int n_tiles = (p.N + BN - 1) / BN;
     const int m_tiles = (p.M + BM - 1) / BM;
     const uint32_t nct = LN ? gridDim.x : 1;  // cluster spans the row: cluster dims == (N/BN, 1, 1)
-    const uint32_t me = LN ? tc::cluster_rank() : 0;
+    // CTAs that share operand tiles through TMA multicast: the LN row cluster shares the
+    // activation tile; plain GEMMs pair CTAs along M that share the weight tile
+    const uint32_t csz = LN ? nct : static_cast<uint32_t>(p.mc);
+    const uint32_t me = csz > 1 ? tc::cluster_rank() : 0;
+    const uint16_t cmask = static_cast<uint16_t>((1u << csz) - 1u);
 
     // tile i of this CTA -> (m_blk, n_blk)
     auto tile_of = [&](int i, int& mb, int& nb) -> bool {
@@ -149,10 +208,12 @@ __global__ void __launch_bounds__(Cfg<BN, LN>::THREADS, 1) gemm_fused_kernel(con
             nb = blockIdx.x;
             return mb < m_tiles;
         } else {
-            const int t = blockIdx.x + i * gridDim.x;
-            mb = t / n_tiles;
-            nb = t - mb * n_tiles;
-            return t < m_tiles * n_tiles;
+            // cluster c walks tiles t = c + i * n_clusters; its CTAs take consecutive m blocks
+            const int t = static_cast<int>(blockIdx.x / csz) + i * static_cast<int>(gridDim.x / csz);
+            const int mg = t / n_tiles;
+            nb = t - mg * n_tiles;
+            mb = mg * static_cast<int>(csz) + static_cast<int>(me);
+            return t < (m_tiles / static_cast<int>(csz)) * n_tiles;
         }
     };
 
@@ -161,20 +222,20 @@ __global__ void __launch_bounds__(Cfg<BN, LN>::THREADS, 1) gemm_fused_kernel(con
         tc::prefetch_tmap(&p.tb);
         for (int s = 0; s < C::STAGES; ++s) {
             tc::mbar_init(&full[s], 1);
-            tc::mbar_init(&empty[s], 1);
+            tc::mbar_init(&empty[s], csz);  // consumed by every CTA that receives the stage
         }
         for (int b = 0; b < 2; ++b) {
             tc::mbar_init(&tfull[b], 1);
             tc::mbar_init(&tempty[b], 32 * C::EPI_WARPS);
         }
-        if (LN && nct > 1)
-            for (int b = 0; b < 4; ++b) tc::mbar_init(&lnb[b], 128 * (nct - 1));
+        if (LN)  // every epilogue thread of every cluster CTA arrives once per (tile, pass)
+            for (int b = 0; b < 4; ++b) tc::mbar_init(&lnb[b], 32 * C::EPI_WARPS * nct);
         tc::fence_barrier_init();
     }
     if (warp == 1) tc::tmem_alloc<C::TMEM_COLS>(tmem_ptr);
     tc::fence_before_sync();
     __syncthreads();
-    if (LN && nct > 1) tc::cluster_sync_all();  // peers' barriers are initialised before any remote arrive
+    if (csz > 1) tc::cluster_sync_all();  // peers' barriers are initialised before any remote traffic
     tc::fence_after_sync();
     const uint32_t tmem = *tmem_ptr;
 
@@ -188,9 +249,22 @@ __global__ void __launch_bounds__(Cfg<BN, LN>::THREADS, 1) gemm_fused_kernel(con
             for (int i = 0; tile_of(i, mb, nb); ++i) {
                 for (int kb = 0; kb < nk; ++kb) {
                     tc::mbar_wait(&empty[s], ph ^ 1);
-                    tc::mbar_expect_tx(&full[s], C::A_BYTES + C::B_BYTES);
-                    tc::tma_load_2d_hint(sA + s * C::A_BYTES, &p.ta, &full[s], kb * BK, mb * BM, pol_a);
-                    tc::tma_load_2d(sB + s * C::B_BYTES, &p.tb, &full[s], kb * BK, nb * BN);
+                    tc::mbar_expect_tx(&full[s], C::A_BYTES + C::B_BYTES);  // full A and B arrive in every CTA
+                    if (LN && csz > 1) {
+                        // row cluster: k-blocks round-robin over the CTAs, each multicasting A
+                        if (static_cast<uint32_t>(kb) % csz == me)
+                            tc::tma_load_2d_mc(sA + s * C::A_BYTES, &p.ta, &full[s], kb * BK, mb * BM, cmask);
+                        tc::tma_load_2d(sB + s * C::B_BYTES, &p.tb, &full[s], kb * BK, nb * BN);
+                    } else if (csz > 1) {
+                        // M pair: own A; each CTA loads 1/csz of the weight rows and multicasts them
+                        const int rows = BN / static_cast<int>(csz);
+                        tc::tma_load_2d_hint(sA + s * C::A_BYTES, &p.ta, &full[s], kb * BK, mb * BM, pol_a);
+                        tc::tma_load_2d_mc(sB + s * C::B_BYTES + me * rows * 128, &p.tb, &full[s], kb * BK,
+                                           nb * BN + static_cast<int>(me) * rows, cmask);
+                    } else {
+                        tc::tma_load_2d_hint(sA + s * C::A_BYTES, &p.ta, &full[s], kb * BK, mb * BM, pol_a);
+                        tc::tma_load_2d(sB + s * C::B_BYTES, &p.tb, &full[s], kb * BK, nb * BN);
+                    }
                     if (++s == C::STAGES) { s = 0; ph ^= 1; }
                 }
             }
@@ -216,7 +290,8 @@ __global__ void __launch_bounds__(Cfg<BN, LN>::THREADS, 1) gemm_fused_kernel(con
                     for (int k = 0; k < BK / 16; ++k)
                         tc::mma_f16_ss(d, tc::sdesc_sw128(a0 + 32 * k), tc::sdesc_sw128(b0 + 32 * k), idesc,
                                        (kb | k) != 0);
-                    tc::mma_commit(&empty[s]);
+                    if (csz > 1) tc::mma_commit_mc(&empty[s], cmask);  // free the stage in every sharer
+                    else tc::mma_commit(&empty[s]);
                     if (++s == C::STAGES) { s = 0; ph ^= 1; }
                 }
                 tc::mma_commit(&tfull[acc]);
@@ -227,10 +302,12 @@ __global__ void __launch_bounds__(Cfg<BN, LN>::THREADS, 1) gemm_fused_kernel(con
         const uint32_t q = warp & 3;
         const int r_local = static_cast<int>(q * 32 + lane);
         constexpr int CHUNKS = BN / 32;
-        // non-LN: 8 warps, each lane quarter split in two column halves
-        const int half = LN ? 0 : static_cast<int>((warp - 4) >> 2);
-        const int c_begin = LN ? 0 : half * (CHUNKS / 2);
-        const int c_end = LN ? CHUNKS : c_begin + CHUNKS / 2;
+        // each TMEM lane quarter (32 rows) is split into GROUPS column groups of CHUNKS/GROUPS
+        // 32-column chunks; `half` (the group index) is 0/1 for the LayerNorm variant
+        constexpr int GROUPS = C::EPI_WARPS / 4;
+        const int half = static_cast<int>((warp - 4) >> 2);
+        const int c_begin = half * (CHUNKS / GROUPS);
+        const int c_end = c_begin + CHUNKS / GROUPS;
         int mb, nb;
         for (int i = 0; tile_of(i, mb, nb); ++i) {
             const int acc = i & 1;
@@ -257,55 +334,68 @@ __global__ void __launch_bounds__(Cfg<BN, LN>::THREADS, 1) gemm_fused_kernel(con
                 }
             } else {
                 const int par = i & 1;
-                // pass 1: x = acc + bias (+act) + aux, kept in TMEM; partial Σx
+                // pass 1: x = acc + bias (+act) + aux, kept in TMEM; partial Σx. The residual
+                // values of the next chunk are in flight while this chunk is processed.
                 float sum = 0.f;
-                for (int c = 0; c < CHUNKS; ++c) {
+                uint4 aux_cur[4], aux_nxt[4];
+                load_aux<T>(p, row_ok, row, n0 + c_begin * 32, aux_cur);
+                for (int c = c_begin; c < c_end; ++c) {
+                    if (c + 1 < c_end) load_aux<T>(p, row_ok, row, n0 + (c + 1) * 32, aux_nxt);
                     tc::tmem_ld32(taddr + c * 32, r);
                     tc::tmem_ld_wait();
-                    if (row_ok) epi_chunk<T>(p, r, row, n0 + c * 32, x);
+                    if (row_ok) epi_chunk_pre<T>(p, r, n0 + c * 32, aux_cur, x);
                     else
 #pragma unroll
                         for (int j = 0; j < 32; ++j) x[j] = 0.f;
+                    float s4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
                     for (int j = 0; j < 32; ++j) {
-                        sum += x[j];
+                        s4[j & 3] += x[j];
                         r[j] = __float_as_uint(x[j]);
                     }
+                    sum += (s4[0] + s4[1]) + (s4[2] + s4[3]);
                     tc::tmem_st32(taddr + c * 32, r);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) aux_cur[j] = aux_nxt[j];
                 }
                 tc::tmem_st_wait();
+                // Row reduction over the 2 column halves x nct cluster CTAs: every epilogue thread
+                // of every CTA writes its partial into every CTA's slot array (peers through
+                // DSMEM) and arrives on that CTA's barrier; one wait then covers all partials.
                 auto exchange = [&](float v, int pass) -> float {
-                    float* slot = red + ((par * 2 + pass) * kMaxCluster) * BM;
-                    slot[me * BM + r_local] = v;
-                    if (nct == 1) return v;
+                    float* slot = red + ((par * 2 + pass) * nct) * 2 * BM;  // [cta][half][row]
+                    const int mine = (static_cast<int>(me) * 2 + half) * BM + r_local;
+                    slot[mine] = v;
                     for (uint32_t c = 0; c < nct; ++c)
-                        if (c != me) tc::st_dsmem_f32(&slot[me * BM + r_local], c, v);
+                        if (c != me) tc::st_dsmem_f32(&slot[mine], c, v);
                     for (uint32_t c = 0; c < nct; ++c)
                         if (c != me) tc::mbar_arrive_cluster(&lnb[par * 2 + pass], c);
+                    tc::mbar_arrive(&lnb[par * 2 + pass]);
                     tc::mbar_wait_cluster(&lnb[par * 2 + pass], (i >> 1) & 1);
                     float t = 0.f;
-                    for (uint32_t c = 0; c < nct; ++c) t += slot[c * BM + r_local];
+                    for (uint32_t c = 0; c < 2 * nct; ++c) t += slot[c * BM + r_local];
                     return t;
                 };
                 const float mean = exchange(sum, 0) / static_cast<float>(p.N);
                 // pass 2: Σ(x - mean)^2
-                float sq = 0.f;
-                for (int c = 0; c < CHUNKS; ++c) {
+                float sq4[4] = {0.f, 0.f, 0.f, 0.f};
+                for (int c = c_begin; c < c_end; ++c) {
                     tc::tmem_ld32(taddr + c * 32, r);
                     tc::tmem_ld_wait();
 #pragma unroll
                     for (int j = 0; j < 32; ++j) {
                         const float d = __uint_as_float(r[j]) - mean;
-                        sq += d * d;
+                        sq4[j & 3] = fmaf(d, d, sq4[j & 3]);
                     }
                 }
+                const float sq = (sq4[0] + sq4[1]) + (sq4[2] + sq4[3]);
                 const float inv = 1.0f / sqrtf(exchange(sq, 1) / static_cast<float>(p.N) + kLnEps);
                 // pass 3: normalise, store
                 float y[32];
-                for (int c = 0; c < CHUNKS; ++c) {
+                for (int c = c_begin; c < c_end; ++c) {
                     tc::tmem_ld32(taddr + c * 32, r);
                     tc::tmem_ld_wait();
-                    if (c == CHUNKS - 1) {
+                    if (c == c_end - 1) {
                         tc::fence_before_sync();
                         tc::mbar_arrive(&tempty[acc]);
                     }
@@ -324,7 +414,7 @@ __global__ void __launch_bounds__(Cfg<BN, LN>::THREADS, 1) gemm_fused_kernel(con
     }
     tc::fence_before_sync();
     __syncthreads();
-    if (LN && nct > 1) tc::cluster_sync_all();  // no CTA exits while a peer may still write its smem
+    if (csz > 1) tc::cluster_sync_all();  // no CTA exits while a peer may still write its smem
     if (warp == 1) tc::tmem_dealloc<C::TMEM_COLS>(tmem);
 }
 
@@ -345,7 +435,12 @@ sf_status launch_gemm(const sf_gemm_args& a, cudaStream_t st) {
     GemmParams p{};
     const bool bf = std::is_same<T, __nv_bfloat16>::value;
     SF_TRY(make_tmap_2d(&p.ta, a.x, a.M, a.K, a.ldx, BK, BM, bf));
-    SF_TRY(make_tmap_2d(&p.tb, a.w, a.N, a.K, a.ldw, BK, BN, bf));
+    const int m_tiles = static_cast<int>(ceil_div(a.M, BM)), n_tiles = static_cast<int>(ceil_div(a.N, BN));
+    // plain GEMMs: pairs of CTAs along M share the weight tile by multicast (halves the per-CTA
+    // weight traffic through L2) when the M tiles pair up and the grid has more than one wave
+    const int mc = (!LN && m_tiles % 2 == 0 && m_tiles * n_tiles >= 2 * num_sms()) ? 2 : 1;
+    SF_TRY(make_tmap_2d(&p.tb, a.w, a.N, a.K, a.ldw, BK, BN / mc, bf));
+    p.mc = mc;
     p.M = a.M; p.N = a.N; p.K = a.K;
     p.out = a.out; p.ldout = a.ldout;
     p.bias = static_cast<const float*>(a.epi.bias);
@@ -356,7 +451,6 @@ sf_status launch_gemm(const sf_gemm_args& a, cudaStream_t st) {
     p.out_pre_ln = a.epi.out_pre_ln;
     auto kern = gemm_fused_kernel<T, BN, LN>;
     SF_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM));
-    const int m_tiles = static_cast<int>(ceil_div(a.M, BM)), n_tiles = static_cast<int>(ceil_div(a.N, BN));
     cudaLaunchConfig_t cfg{};
     cfg.blockDim = dim3(Cf::THREADS);
     cfg.dynamicSmemBytes = Cf::SMEM;
@@ -373,7 +467,16 @@ sf_status launch_gemm(const sf_gemm_args& a, cudaStream_t st) {
         cfg.attrs = attr;
         cfg.numAttrs = 1;
     } else {
-        cfg.gridDim = dim3(std::min(m_tiles * n_tiles, num_sms()));
+        const int ctas = std::min(m_tiles * n_tiles, num_sms()) / mc * mc;
+        cfg.gridDim = dim3(std::max(ctas, mc));
+        if (mc > 1) {
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = static_cast<unsigned>(mc);
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+        }
     }
     SF_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, p));
     SF_LAUNCH_CHECK();
