@@ -248,6 +248,9 @@ typedef struct sf_gemm_epilogue {
     void* out_pre_ln;        /* optional second output: the pre-LN row (residual stream) */
 } sf_gemm_epilogue;
 
+#define SF_TILE_AUTO 0
+#define SF_TILE_PAIR 1
+
 typedef struct sf_gemm_args {
     int32_t M, N, K;
     int32_t dtype;           /* sf_dtype of X, W, out */
@@ -255,7 +258,9 @@ typedef struct sf_gemm_args {
     const void* w; int64_t ldw;   /* (N x K) row-major */
     void* out; int64_t ldout;
     sf_gemm_epilogue epi;
-    int32_t tile_n;          /* output tile width: 0 = auto, 128 or 256 (a tuning knob, params.hpp) */
+    int32_t tile_n;          /* output tiling (a tuning knob, params.hpp): SF_TILE_AUTO, 128 or 256
+                                (one CTA per 128 x tile_n tile) or SF_TILE_PAIR (two-SM CTA pairs,
+                                256 x 256 tiles, tcgen05 cta_group::2) */
 } sf_gemm_args;
 
 /* CiMi template (backend.hpp:240-264): tcgen05 GEMM + fused epilogue. */

@@ -1,0 +1,152 @@
+// epilogue.cuh — pieces shared by the CiMi GEMM kernels (gemm_tc.cu: one CTA per tile,
+// gemm2_tc.cu: CTA pairs): kernel parameters and the register-level MI epilogue
+// (bias -> GELU/ReLU -> +aux, backend.hpp:111-167).
+#pragma once
+
+#include "tc.cuh"
+
+namespace sf {
+
+constexpr int BM = 128, BK = 64;
+constexpr float kLnEps = 1e-5f;  // backend.hpp:111
+constexpr int kMaxCluster = 8;
+
+struct GemmParams {
+    CUtensorMap ta;  // X: rows M, cols K
+    CUtensorMap tb;  // W: rows N, cols K
+    int32_t M, N, K;
+    void* out;
+    int64_t ldout;
+    const float* bias;
+    int32_t act;
+    const void* aux;
+    int64_t ldaux;
+    const float* gamma;
+    const float* beta;
+    void* out_pre_ln;
+    int32_t mc;   // single-CTA non-LN: CTAs per cluster along M sharing (multicasting) the weight tile
+    int32_t nct;  // pair kernel, LN: n-tiles per row (cluster = 2 x nct CTAs)
+};
+
+template <typename T>
+__device__ __forceinline__ uint32_t pack2(float a, float b);
+template <>
+__device__ __forceinline__ uint32_t pack2<__half>(float a, float b) {
+    __half2 h = __floats2half2_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h);
+}
+template <>
+__device__ __forceinline__ uint32_t pack2<__nv_bfloat16>(float a, float b) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h);
+}
+
+// erf via Abramowitz & Stegun 7.1.26 (|error| <= 1.5e-7, far below the fp16 output rounding):
+// branch-free, one MUFU reciprocal + one MUFU exp2 + 7 FMAs instead of erff's ~20-instruction,
+// divergent two-regime evaluation. The exact-erf GELU semantics of the reference are kept.
+__device__ __forceinline__ float erf_as(float x) {
+    const float z = fabsf(x);
+    float t;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(t) : "f"(fmaf(0.3275911f, z, 1.0f)));
+    float poly = fmaf(1.061405429f, t, -1.453152027f);
+    poly = fmaf(poly, t, 1.421413741f);
+    poly = fmaf(poly, t, -0.284496736f);
+    poly = fmaf(poly, t, 0.254829592f);
+    poly *= t;
+    float e;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(-z * z * 1.4426950408889634f));
+    return copysignf(fmaf(-poly, e, 1.0f), x);
+}
+
+__device__ __forceinline__ float act_fn(float x, int act) {
+    if (act == SF_ACT_GELU) return 0.5f * x * (1.0f + erf_as(x * 0.7071067811865475f));  // backend.hpp:128-131
+    if (act == SF_ACT_RELU) return x > 0.f ? x : 0.f;                                    // backend.hpp:132-134
+    return x;
+}
+
+// residual values of row `row`, columns [col, col+32) (issued one chunk ahead of their use)
+template <typename T>
+__device__ __forceinline__ void load_aux(const GemmParams& p, bool ok, int64_t row, int64_t col, uint4 (&a)[4]) {
+    if (!p.aux || !ok) return;
+    const uint4* a4 = reinterpret_cast<const uint4*>(static_cast<const T*>(p.aux) + row * p.ldaux + col);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) a[j] = __ldg(a4 + j);
+}
+
+// 32 consecutive values: bias -> act -> + prefetched residual.
+template <typename T>
+__device__ __forceinline__ void epi_chunk_pre(const GemmParams& p, const uint32_t (&r)[32], int64_t col,
+                                              const uint4 (&aux)[4], float (&x)[32]) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) x[j] = __uint_as_float(r[j]);
+    if (p.bias) {
+        const float4* b4 = reinterpret_cast<const float4*>(p.bias + col);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const float4 b = __ldg(b4 + j);
+            x[4 * j] += b.x; x[4 * j + 1] += b.y; x[4 * j + 2] += b.z; x[4 * j + 3] += b.w;
+        }
+    }
+    if (p.act) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) x[j] = act_fn(x[j], p.act);
+    }
+    if (p.aux) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const T* h = reinterpret_cast<const T*>(&aux[j]);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) x[8 * j + e] += DT<T>::to_f(h[e]);
+        }
+    }
+}
+
+// 32 consecutive values of row `row`, columns [col, col+32): bias -> act -> +aux.
+template <typename T>
+__device__ __forceinline__ void epi_chunk(const GemmParams& p, const uint32_t (&r)[32], int64_t row, int64_t col,
+                                          float (&x)[32]) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) x[j] = __uint_as_float(r[j]);
+    if (p.bias) {
+        const float4* b4 = reinterpret_cast<const float4*>(p.bias + col);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const float4 b = __ldg(b4 + j);
+            x[4 * j] += b.x; x[4 * j + 1] += b.y; x[4 * j + 2] += b.z; x[4 * j + 3] += b.w;
+        }
+    }
+    if (p.act) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) x[j] = act_fn(x[j], p.act);
+    }
+    if (p.aux) {
+        const uint4* a4 = reinterpret_cast<const uint4*>(static_cast<const T*>(p.aux) + row * p.ldaux + col);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const uint4 u = __ldg(a4 + j);
+            const T* h = reinterpret_cast<const T*>(&u);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) x[8 * j + e] += DT<T>::to_f(h[e]);
+        }
+    }
+}
+
+template <typename T>
+__device__ __forceinline__ void store_chunk(void* base, int64_t ld, int64_t row, int64_t col, const float (&x)[32]) {
+    uint4* o = reinterpret_cast<uint4*>(static_cast<T*>(base) + row * ld + col);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        uint4 u;
+        u.x = pack2<T>(x[8 * j + 0], x[8 * j + 1]);
+        u.y = pack2<T>(x[8 * j + 2], x[8 * j + 3]);
+        u.z = pack2<T>(x[8 * j + 4], x[8 * j + 5]);
+        u.w = pack2<T>(x[8 * j + 6], x[8 * j + 7]);
+        o[j] = u;
+    }
+}
+
+sf_status gemm_pair_dispatch(const sf_gemm_args& a, bool ln, cudaStream_t st);  // gemm2_tc.cu
+bool gemm_pair_supported(const sf_gemm_args& a, bool ln);
+int num_sms();
+
+}  // namespace sf

@@ -28,6 +28,9 @@ def epilogue(bias=None, act: str = "none", aux=None, ln_gamma=None, ln_beta=None
                         _ptr(ln_gamma), _ptr(ln_beta), _ptr(out_pre_ln))
 
 
+TILE_AUTO, TILE_PAIR = 0, 1  # sf_gemm_args.tile_n: SF_TILE_AUTO / SF_TILE_PAIR (or 128 / 256)
+
+
 def gemm_fused(x: torch.Tensor, w_nk: torch.Tensor, out: Optional[torch.Tensor] = None, *, bias=None,
                act: str = "none", aux=None, ln_gamma=None, ln_beta=None, out_pre_ln=None, tile_n: int = 0,
                stream=None) -> torch.Tensor:

@@ -6,6 +6,7 @@ import pytest
 
 pytestmark = pytest.mark.gpu
 MAX_ABS, MEAN_REL = 2e-2, 1e-3
+PAIR = 1  # SF_TILE_PAIR: two-SM CTA-pair tiles (tcgen05 cta_group::2)
 
 
 def parity(out, ref, max_abs=MAX_ABS, mean_rel=MEAN_REL):
@@ -36,27 +37,32 @@ def fz():
 
 @pytest.mark.parametrize("M,N,K", [(128, 256, 64), (256, 768, 768), (300, 512, 192), (1024, 2304, 768),
                                    (512, 768, 3072), (128, 96, 64)])
-def test_gemm_plain(fz, oracle, M, N, K):
+@pytest.mark.parametrize("tile", [0, PAIR])
+def test_gemm_plain(fz, oracle, M, N, K, tile):
+    if tile == PAIR and M <= 128:
+        pytest.skip("CTA pairs need M > 128")
     x = r16(oracle.random_matrix(M, K, 1))
     w = r16(oracle.random_matrix(K, N, 2, -1 / np.sqrt(K), 1 / np.sqrt(K)))  # GraphData Gemm init (backend.hpp:80-81)
-    out = fz.gemm_fused(dev(x), dev(w.T))
+    out = fz.gemm_fused(dev(x), dev(w.T), tile_n=tile)
     parity(out, oracle.gemm(x, w, threads=8))
 
 
 @pytest.mark.parametrize("act", ["gelu", "relu"])
-def test_gemm_bias_act(fz, oracle, act):
+@pytest.mark.parametrize("tile", [0, 128, PAIR])
+def test_gemm_bias_act(fz, oracle, act, tile):
     import torch
     M, N, K = 512, 3072, 768
     x = r16(oracle.random_matrix(M, K, 3))
     w = r16(oracle.random_matrix(K, N, 4, -1 / np.sqrt(K), 1 / np.sqrt(K)))
     b = oracle.random_matrix(1, N, 5, -0.5, 0.5)[0]
     ref = oracle.gelu(oracle.bias(oracle.gemm(x, w, 8), b)) if act == "gelu" else oracle.relu(oracle.bias(oracle.gemm(x, w, 8), b))
-    out = fz.gemm_fused(dev(x), dev(w.T), bias=dev(b, torch.float32), act=act)
+    out = fz.gemm_fused(dev(x), dev(w.T), bias=dev(b, torch.float32), act=act, tile_n=tile)
     parity(out, ref)
 
 
-@pytest.mark.parametrize("N,K", [(768, 768), (768, 3072), (512, 256), (256, 128)])
-def test_gemm_bias_add_layernorm(fz, oracle, N, K):
+@pytest.mark.parametrize("N,K", [(768, 768), (768, 3072), (512, 256), (256, 128), (1024, 256)])
+@pytest.mark.parametrize("tile", [0, PAIR])
+def test_gemm_bias_add_layernorm(fz, oracle, N, K, tile):
     import torch
     M = 384
     x = r16(oracle.random_matrix(M, K, 6))
@@ -69,23 +75,51 @@ def test_gemm_bias_add_layernorm(fz, oracle, N, K):
     ref = oracle.layernorm(pre, g, be)
     pre_dev = torch.empty((M, N), dtype=torch.float16, device="cuda")
     out = fz.gemm_fused(dev(x), dev(w.T), bias=dev(b, torch.float32), aux=dev(aux), ln_gamma=dev(g, torch.float32),
-                        ln_beta=dev(be, torch.float32), out_pre_ln=pre_dev)
+                        ln_beta=dev(be, torch.float32), out_pre_ln=pre_dev, tile_n=tile)
     parity(out, ref)
     parity(pre_dev, pre)
 
 
-def test_mi_chain(fz, oracle):
+@pytest.mark.parametrize("ln", [False, True])
+@pytest.mark.parametrize("tile", [0, 256, PAIR])
+def test_gemm_large_multi_tile(fz, ln, tile):
+    """cfg2-sized GEMM (several tiles per persistent CTA / pair, accumulator double buffering and
+    barrier phase wrap-around) against a torch fp32 reference of the same op."""
     import torch
-    M, N = 1000, 768
+    g = torch.Generator(device="cuda").manual_seed(7)
+    M, N, K = 16384, 768, 768
+    x = torch.randn(M, K, device="cuda", generator=g).half()
+    w = (torch.randn(N, K, device="cuda", generator=g) / K ** 0.5).half()
+    b = torch.randn(N, device="cuda", generator=g) * 0.5
+    aux = torch.randn(M, N, device="cuda", generator=g).half()
+    pre = x.float() @ w.float().T + b + aux.float()
+    kw = dict(bias=b, aux=aux, tile_n=tile)
+    if ln:
+        gam = 0.5 + torch.rand(N, device="cuda", generator=g)
+        bet = torch.rand(N, device="cuda", generator=g) - 0.5
+        ref = torch.nn.functional.layer_norm(pre, (N,), gam, bet, eps=1e-5)
+        kw.update(ln_gamma=gam, ln_beta=bet)
+    else:
+        ref = pre
+    out = fz.gemm_fused(x, w, **kw)
+    parity(out, ref.cpu().numpy())
+
+
+@pytest.mark.parametrize("M,N", [(1000, 768), (37, 100), (9, 4096), (64, 7), (300, 1024), (50, 3072)])
+@pytest.mark.parametrize("ln", [True, False])
+def test_mi_chain(fz, oracle, M, N, ln):
+    import torch
     x = r16(oracle.random_matrix(M, N, 12))
     b = oracle.random_matrix(1, N, 13, -0.5, 0.5)[0]
     aux = r16(oracle.random_matrix(M, N, 14))
     g = 0.5 + oracle.random_matrix(1, N, 15, 0, 1)[0]
     be = oracle.random_matrix(1, N, 16, -0.5, 0.5)[0]
-    ref = oracle.layernorm(oracle.add(oracle.gelu(oracle.bias(x, b)), aux), g, be)
-    out = fz.mi_chain(dev(x), bias=dev(b, torch.float32), act="gelu", aux=dev(aux), ln_gamma=dev(g, torch.float32),
-                      ln_beta=dev(be, torch.float32))
-    parity(out, ref)
+    ref = oracle.add(oracle.gelu(oracle.bias(x, b)), aux)
+    kw = dict(bias=dev(b, torch.float32), act="gelu", aux=dev(aux))
+    if ln:
+        ref = oracle.layernorm(ref, g, be)
+        kw.update(ln_gamma=dev(g, torch.float32), ln_beta=dev(be, torch.float32))
+    parity(fz.mi_chain(dev(x), **kw), ref)
 
 
 def test_gemm_shape_errors(fz):
