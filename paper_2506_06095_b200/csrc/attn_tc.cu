@@ -60,10 +60,18 @@ struct AttnParams {
     unsigned long long* trace;  // optional clock64 trace of CTA (0,0) (sf_debug_attn_trace)
 };
 
+// clock64 timeline of CTA (0,0) for tools/attn_trace.py; compiled in only with -DSF_ATTN_TRACE
+// (the predicated stores otherwise cost issue slots in the softmax loop)
+#ifdef SF_ATTN_TRACE
 #define SF_TRACE(j, ev)                                                                   \
     do {                                                                                  \
         if (p.trace && blockIdx.x == 0 && blockIdx.y == 0 && (j) < 64) p.trace[(j) * 16 + (ev)] = clock64(); \
     } while (0)
+#else
+#define SF_TRACE(j, ev) \
+    do {                \
+    } while (0)
+#endif
 
 __device__ __forceinline__ float ex2(float x) {
     float y;
@@ -84,30 +92,39 @@ __device__ __forceinline__ uint32_t pack2<__nv_bfloat16>(float a, float b) {
     return *reinterpret_cast<uint32_t*>(&h);
 }
 
-// 2^x on a packed pair of 16-bit values (one MUFU op for two exponentials)
-template <typename T>
-__device__ __forceinline__ uint32_t ex2x2(uint32_t x);
-template <>
-__device__ __forceinline__ uint32_t ex2x2<__half>(uint32_t x) {
-    uint32_t y;
-    asm("ex2.approx.f16x2 %0, %1;" : "=r"(y) : "r"(x));
-    return y;
+// sm_100 packed fp32 (FFMA2 / FADD2) and three-input max (FMNMX3)
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+    float2 d;
+    asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
+        "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+        "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+        : "=f"(d.x), "=f"(d.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+    return d;
 }
-template <>
-__device__ __forceinline__ uint32_t ex2x2<__nv_bfloat16>(uint32_t x) {
-    uint32_t y;
-    asm("ex2.approx.ftz.bf16x2 %0, %1;" : "=r"(y) : "r"(x));
-    return y;
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+    float2 d;
+    asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
+        "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+        "add.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+        : "=f"(d.x), "=f"(d.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+    return d;
 }
-template <typename T>
-__device__ __forceinline__ float2 unpack2(uint32_t v);
-template <>
-__device__ __forceinline__ float2 unpack2<__half>(uint32_t v) {
-    return __half22float2(*reinterpret_cast<__half2*>(&v));
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+    float d;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+    return d;
 }
-template <>
-__device__ __forceinline__ float2 unpack2<__nv_bfloat16>(uint32_t v) {
-    return __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&v));
+__device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ uint32_t lds_u16(uint32_t addr) {
+    uint16_t v;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(addr));
+    return v;
 }
 
 __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* m, uint64_t* bar, int32_t c0, int32_t c1,
@@ -131,8 +148,10 @@ __device__ __forceinline__ float ld_shared_f32(uint32_t addr) {
     return v;
 }
 
-template <typename T>
+template <typename T, int BN>
 __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_constant__ AttnParams p) {
+    constexpr int G = kNS / BN;          // column tiles gathered per 64-key step
+    constexpr int TB = kBM * BN / 8;     // packed bytes of one part tile (pool stride)
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     unsigned char* sQ = sm;
@@ -159,7 +178,10 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
     const int b = bh / p.h, hh = bh % p.h;
     const int l0 = p.load_row_ptr[br];
     const int L = p.load_row_ptr[br + 1] - l0;
-    const int nsteps = (L + p.G - 1) / p.G;
+    const int nsteps = (L + G - 1) / G;
+    const uint32_t s_col_a = tc::smem_u32(s_col), s_tile_a = tc::smem_u32(s_tile);
+    auto col_at = [&](int e) { return static_cast<int>(lds_u32(s_col_a + 4u * e)); };
+    auto tile_at = [&](int e) { return static_cast<int>(lds_u32(s_tile_a + 4u * e)); };
 
     for (int i = threadIdx.x; i < L; i += kThreads) {
         s_col[i] = p.load_col_idx[l0 + i];
@@ -192,7 +214,7 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
     if (warp == 0) {
         // ------------------------------------------------------------------ producer
         if (nsteps > 0 && tc::elect_one()) {
-            const int bn = p.bn;
+            constexpr int bn = BN;
             tc::mbar_expect_tx(q_full, kQBytes);
             tma_load_4d(sQ, &p.tq, q_full, 0, br * kBM, hh, b);
             const int chunk = bn * kD * 2;
@@ -201,19 +223,22 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
             for (int j = 0; j < nsteps; ++j) {
                 tc::mbar_wait(&kv_empty[s], ph ^ 1);
                 int parts = 0;
-                for (int g = 0; g < p.G; ++g) {
-                    const int e = j * p.G + g;
-                    parts += (e < L && s_tile[e] >= 0);
+#pragma unroll
+                for (int g = 0; g < G; ++g) {
+                    const int e = j * G + g;
+                    parts += (e < L && tile_at(e) >= 0);
                 }
-                tc::mbar_expect_tx(&kv_full[s], 2 * kKVBytes + parts * p.tile_bytes);
-                for (int g = 0; g < p.G; ++g) {
-                    const int e = j * p.G + g;
-                    const int col = (e < L ? s_col[e] : s_col[0]) * bn;  // pad: valid, fully masked
+                tc::mbar_expect_tx(&kv_full[s], 2 * kKVBytes + parts * TB);
+#pragma unroll
+                for (int g = 0; g < G; ++g) {
+                    const int e = j * G + g;
+                    const int col = col_at(e < L ? e : 0) * bn;  // pad: valid, fully masked
                     tma_load_4d(sK + s * kKVBytes + g * chunk, &p.tk, &kv_full[s], 0, col, hh, b);
                     tma_load_4d(sV + s * kKVBytes + g * chunk, &p.tv, &kv_full[s], 0, col, hh, b);
-                    if (e < L && s_tile[e] >= 0)
-                        tc::bulk_load(sMask + s * kMaskBytes + g * p.tile_bytes,
-                                      p.pool + static_cast<int64_t>(s_tile[e]) * p.tile_bytes, p.tile_bytes, &kv_full[s]);
+                    const int t = e < L ? tile_at(e) : -2;
+                    if (t >= 0)
+                        tc::bulk_load(sMask + s * kMaskBytes + g * TB, p.pool + static_cast<int64_t>(t) * TB, TB,
+                                      &kv_full[s]);
                 }
                 if (++s == kStages) { s = 0; ph ^= 1; }
             }
@@ -254,6 +279,7 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
                 SF_TRACE(j, 9);
                 if (j + kSBuf < nsteps) issue_s(j + kSBuf);
                 SF_TRACE(j, 10);
+#ifdef SF_ATTN_TRACE
                 if (p.trace && blockIdx.x == 0 && blockIdx.y == 0 && j + kSBuf < nsteps) {
                     // diagnosis only: observe this thread's own S commit (pure MMA-chain latency)
                     tc::mbar_wait(&s_full[(j + kSBuf) % kSBuf], ((j + kSBuf) / kSBuf) & 1);
@@ -261,6 +287,7 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
                     tc::mbar_wait(&o_full[j & 1], (j >> 1) & 1);
                     SF_TRACE(j, 12);
                 }
+#endif
             }
         }
     } else {
@@ -283,27 +310,27 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
             if (tr) SF_TRACE(j, 0);
             tc::mbar_wait(&kv_full[st], (j / kStages) & 1);
             if (tr) SF_TRACE(j, 1);
-            // this thread's 32 mask bits: full tile -> ones, part tile -> staged pool row, pad -> 0
-            uint32_t bits;
+            // this thread's 32 mask bits (keys 32h..32h+31 of the step): full tile -> ones, part
+            // tile -> its staged pool row, padding -> 0. Only this half's tiles are read.
+            uint32_t bits = 0;
             {
-                const int bn = p.bn;
-                const unsigned char* mrow = sMask + st * kMaskBytes + r * (bn >> 3);
-                uint64_t all = 0;
-                for (int g = 0; g < p.G; ++g) {
-                    const int e = j * p.G + g;
-                    const int t = e < L ? s_tile[e] : -2;
-                    uint64_t gb = 0;
-                    if (t == -1) {
-                        gb = bn >= 64 ? ~0ull : ((1ull << bn) - 1ull);
-                    } else if (t >= 0) {
-                        const unsigned char* tp = mrow + g * p.tile_bytes;
-                        gb = bn == 16 ? *reinterpret_cast<const uint16_t*>(tp)
-                                      : (bn == 32 ? *reinterpret_cast<const uint32_t*>(tp)
-                                                  : *reinterpret_cast<const uint64_t*>(tp));
+                const uint32_t mb = tc::smem_u32(sMask + st * kMaskBytes);
+                if constexpr (BN == 16) {
+#pragma unroll
+                    for (int gg = 0; gg < 2; ++gg) {
+                        const int g = 2 * half + gg, e = j * G + g;
+                        const int t = e < L ? tile_at(e) : -2;
+                        const uint32_t b16 = t == -1 ? 0xffffu : (t >= 0 ? lds_u16(mb + g * TB + r * 2) : 0u);
+                        bits |= b16 << (16 * gg);
                     }
-                    all |= gb << (g * bn);
+                } else if constexpr (BN == 32) {
+                    const int e = j * G + half;
+                    const int t = e < L ? tile_at(e) : -2;
+                    bits = t == -1 ? ~0u : (t >= 0 ? lds_u32(mb + half * TB + r * 4) : 0u);
+                } else {
+                    const int t = j < L ? tile_at(j) : -2;
+                    bits = t == -1 ? ~0u : (t >= 0 ? lds_u32(mb + r * 8 + 4 * half) : 0u);
                 }
-                bits = static_cast<uint32_t>(all >> (32 * half));
             }
             tc::mbar_wait(&s_full[sb], (j / kSBuf) & 1);
             if (tr) SF_TRACE(j, 2);
@@ -320,11 +347,11 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
             float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
             if (act0) {
 #pragma unroll
-                for (int c = 0; c < 16; ++c) mx4[c & 3] = fmaxf(mx4[c & 3], sr[c]);
+                for (int c = 0; c < 16; c += 2) mx4[(c >> 1) & 3] = fmax3(mx4[(c >> 1) & 3], sr[c], sr[c + 1]);
             }
             if (act1) {
 #pragma unroll
-                for (int c = 16; c < 32; ++c) mx4[c & 3] = fmaxf(mx4[c & 3], sr[c]);
+                for (int c = 16; c < 32; c += 2) mx4[(c >> 1) & 3] = fmax3(mx4[(c >> 1) & 3], sr[c], sr[c + 1]);
             }
             // max of the raw scores, then scaled: scale > 0 commutes with max (log2 domain)
             float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * sl2;
@@ -354,7 +381,8 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
             }
             m = m_new;
             uint32_t pk[16];
-            float rs4[4] = {0.f, 0.f, 0.f, 0.f};
+            float2 rs2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+            const float2 sl2x2 = make_float2(sl2, sl2), negm = make_float2(-m, -m);
 #pragma unroll
             for (int g = 0; g < 2; ++g) {
                 if (!(g ? act1 : act0) || m == -INFINITY) {
@@ -364,13 +392,13 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
                 }
 #pragma unroll
                 for (int c = 16 * g; c < 16 * g + 16; c += 2) {
-                    const float p0 = ex2(fmaf(sr[c], sl2, -m));  // masked: ex2(-inf) = 0
-                    const float p1 = ex2(fmaf(sr[c + 1], sl2, -m));
-                    rs4[(c >> 1) & 3] += p0 + p1;
-                    pk[c >> 1] = pack2<T>(p0, p1);
+                    const float2 arg = ffma2(make_float2(sr[c], sr[c + 1]), sl2x2, negm);
+                    const float2 pp = make_float2(ex2(arg.x), ex2(arg.y));  // masked: ex2(-inf) = 0
+                    rs2[(c >> 1) & 1] = fadd2(rs2[(c >> 1) & 1], pp);
+                    pk[c >> 1] = pack2<T>(pp.x, pp.y);
                 }
             }
-            l += (rs4[0] + rs4[1]) + (rs4[2] + rs4[3]);
+            l += (rs2[0].x + rs2[0].y) + (rs2[1].x + rs2[1].y);
             // P_j (this half: keys 32h..32h+31 = packed columns 16h..16h+15) into P[sb] in TMEM
             tc::tmem_st16(trow + kPCol + 32 * sb + 16 * half, pk);
             tc::tmem_st_wait();
@@ -467,7 +495,11 @@ sf_status attn_tc(const sf_attn_args& a, const sf_bsr_dev& b, cudaStream_t st, b
     p.o_sn = a.o_sn;
     p.scale_log2 = a.scale * 1.4426950408889634f;
     p.trace = g_attn_trace;
-    auto kern = bf ? attn_tc_kernel<__nv_bfloat16> : attn_tc_kernel<__half>;
+    void (*kern)(AttnParams) = nullptr;
+    if (b.block_n == 16) kern = bf ? attn_tc_kernel<__nv_bfloat16, 16> : attn_tc_kernel<__half, 16>;
+    else if (b.block_n == 32) kern = bf ? attn_tc_kernel<__nv_bfloat16, 32> : attn_tc_kernel<__half, 32>;
+    else kern = bf ? attn_tc_kernel<__nv_bfloat16, 64> : attn_tc_kernel<__half, 64>;
+    if (b.tile_bytes != kBM * b.block_n / 8) return fail(SF_PLAN_ERROR, "BSR tile_bytes does not match block shape");
     SF_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
     dim3 grid(b.n_rows, static_cast<unsigned>(a.bs) * a.h);
     kern<<<grid, kThreads, kSmem, st>>>(p);

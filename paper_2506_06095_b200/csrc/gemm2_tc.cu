@@ -15,7 +15,8 @@
 //   warps 4..           epilogue on this CTA's 128 accumulator lanes; per-warp release of the
 //                       accumulator to the leader's tempty barrier (remote arrive from the peer).
 // LayerNorm: the cluster is (2 x nct) CTAs — nct pairs along the row — and each CTA exchanges
-// per-row partial sums with the nct CTAs holding the same rows (ranks px + 2y), as in gemm_tc.cu.
+// per-row (mean, M2) partials with the nct CTAs holding the same rows (ranks px + 2y): one DSMEM
+// exchange per tile, one remote arrive per warp and peer.
 #include <algorithm>
 #include <cstring>
 
@@ -34,7 +35,8 @@ struct Cfg2 {
     static constexpr int THREADS = 128 + 32 * EPI_WARPS;
     static constexpr int A_BYTES = BM * BK * 2;         // 16 KB
     static constexpr int B_BYTES = (BN2 / 2) * BK * 2;  // 16 KB
-    static constexpr int RED_FLOATS = LN ? 2 * 2 * kMaxNct * 2 * BM : 0;  // [par][pass][y][half][row]
+    // LN: (mean, M2) partials [par][y][grp][row] as float2, then this CTA's bias/gamma/beta slice
+    static constexpr int RED_FLOATS = LN ? 2 * kMaxNct * 2 * BM * 2 + 3 * BN2 : 0;
     static constexpr int SMEM = STAGES * (A_BYTES + B_BYTES) + 1024 + 256 + RED_FLOATS * 4;
     static constexpr int TMEM_COLS = 2 * BN2;  // double-buffered 128 x 256 fp32 accumulators
 };
@@ -50,7 +52,7 @@ __global__ void __launch_bounds__(Cfg2<LN>::THREADS, 1) gemm2_kernel(const __gri
     uint64_t* empty = full + C::STAGES;
     uint64_t* tfull = empty + C::STAGES;  // [2]
     uint64_t* tempty = tfull + 2;        // [2] (leader's are used)
-    uint64_t* lnb = tempty + 2;          // [2 parity][2 pass]
+    uint64_t* lnb = tempty + 2;          // [2 parity]
     uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(lnb + 4);
     float* red = reinterpret_cast<float*>(smem + C::STAGES * (C::A_BYTES + C::B_BYTES) + 256);
 
@@ -89,11 +91,21 @@ __global__ void __launch_bounds__(Cfg2<LN>::THREADS, 1) gemm2_kernel(const __gri
             tc::mbar_init(&tfull[b], 1);
             tc::mbar_init(&tempty[b], 2 * C::EPI_WARPS);  // one arrive per epilogue warp of both CTAs
         }
-        if (LN)
-            for (int b = 0; b < 4; ++b) tc::mbar_init(&lnb[b], 32 * C::EPI_WARPS * nct);
+        if (LN)  // one arrive per epilogue warp of every CTA holding these rows
+            for (int b = 0; b < 2; ++b) tc::mbar_init(&lnb[b], C::EPI_WARPS * nct);
         tc::fence_barrier_init();
     }
     if (warp == 1) tc::tmem_alloc2<C::TMEM_COLS>(tmem_ptr);
+    float2* part = reinterpret_cast<float2*>(red);                 // [2][nct][2][BM]
+    float* sprm = red + 2 * kMaxNct * 2 * BM * 2;                  // [3][BN2]: bias, gamma, beta
+    if constexpr (LN) {  // the n-tile is fixed per CTA in LN mode: stage its epilogue vectors once
+        const int c0 = static_cast<int>(blockIdx.y % nct) * BN2;
+        for (int t = threadIdx.x; t < BN2; t += blockDim.x) {
+            sprm[t] = p.bias ? p.bias[c0 + t] : 0.f;
+            sprm[BN2 + t] = p.gamma[c0 + t];
+            sprm[2 * BN2 + t] = p.beta[c0 + t];
+        }
+    }
     tc::fence_before_sync();
     __syncthreads();
     tc::cluster_sync_all();
@@ -103,7 +115,9 @@ __global__ void __launch_bounds__(Cfg2<LN>::THREADS, 1) gemm2_kernel(const __gri
     if (warp == 0) {
         // ------------------------------------------------------------------ TMA producer (both CTAs)
         if (tc::elect_one()) {
-            const uint64_t pol_a = tc::policy_evict_first();
+            // X rows are re-read by the n_tiles pairs working on the same row block at about the
+            // same time: evict_first made them miss in L2 (5x DRAM re-reads measured)
+            const uint64_t pol_a = tc::policy_evict_normal();
             const uint64_t pol_b = tc::policy_evict_last();
             const uint32_t full0 = tc::mapa_u32(&full[0], leader);
             int s = 0;
@@ -189,8 +203,13 @@ __global__ void __launch_bounds__(Cfg2<LN>::THREADS, 1) gemm2_kernel(const __gri
                     store_chunk<T>(p.out, p.ldout, row, col, x);
                 }
             } else {
+                // LayerNorm over the row split across nct CTAs x GROUPS warps: each thread owns
+                // one row and 128 columns. Pass 1: x = acc + bias + aux back into TMEM, local sum;
+                // pass 2: local M2 about the local mean; one exchange of (mean, M2) partials and a
+                // Chan combination (numerically the two-pass variance); pass 3: normalise, store.
                 const int par = i & 1;
                 const uint32_t my_y = rank >> 1;
+                constexpr float kCols = 32.f * (CHUNKS / GROUPS);
                 float sum = 0.f;
                 uint4 aux_cur[4], aux_nxt[4];
                 load_aux<T>(p, row_ok, row, n0 + c_begin * 32, aux_cur);
@@ -198,10 +217,27 @@ __global__ void __launch_bounds__(Cfg2<LN>::THREADS, 1) gemm2_kernel(const __gri
                     if (c + 1 < c_end) load_aux<T>(p, row_ok, row, n0 + (c + 1) * 32, aux_nxt);
                     tc::tmem_ld32(taddr + c * 32, r);
                     tc::tmem_ld_wait();
-                    if (row_ok) epi_chunk_pre<T>(p, r, n0 + c * 32, aux_cur, x);
-                    else
+                    const float4* b4 = reinterpret_cast<const float4*>(sprm + c * 32);
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) x[j] = 0.f;
+                    for (int j = 0; j < 8; ++j) {
+                        const float4 b = b4[j];
+                        x[4 * j] = __uint_as_float(r[4 * j]) + b.x;
+                        x[4 * j + 1] = __uint_as_float(r[4 * j + 1]) + b.y;
+                        x[4 * j + 2] = __uint_as_float(r[4 * j + 2]) + b.z;
+                        x[4 * j + 3] = __uint_as_float(r[4 * j + 3]) + b.w;
+                    }
+                    if (p.act) {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) x[j] = act_fn(x[j], p.act);
+                    }
+                    if (p.aux) {
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            const T* h = reinterpret_cast<const T*>(&aux_cur[j]);
+#pragma unroll
+                            for (int e = 0; e < 8; ++e) x[8 * j + e] += DT<T>::to_f(h[e]);
+                        }
+                    }
                     float s4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
                     for (int j = 0; j < 32; ++j) {
@@ -214,33 +250,43 @@ __global__ void __launch_bounds__(Cfg2<LN>::THREADS, 1) gemm2_kernel(const __gri
                     for (int j = 0; j < 4; ++j) aux_cur[j] = aux_nxt[j];
                 }
                 tc::tmem_st_wait();
-                auto exchange = [&](float v, int pass) -> float {
-                    float* slot = red + ((par * 2 + pass) * nct) * 2 * BM;  // [y][grp][row]
-                    const int mine = (static_cast<int>(my_y) * 2 + grp) * BM + r_local;
-                    slot[mine] = v;
-                    for (uint32_t y = 0; y < nct; ++y)
-                        if (y != my_y) tc::st_dsmem_f32(&slot[mine], px + 2 * y, v);
-                    for (uint32_t y = 0; y < nct; ++y)
-                        if (y != my_y) tc::mbar_arrive_cluster(&lnb[par * 2 + pass], px + 2 * y);
-                    tc::mbar_arrive(&lnb[par * 2 + pass]);
-                    tc::mbar_wait_cluster(&lnb[par * 2 + pass], (i >> 1) & 1);
-                    float t = 0.f;
-                    for (uint32_t c = 0; c < 2 * nct; ++c) t += slot[c * BM + r_local];
-                    return t;
-                };
-                const float mean = exchange(sum, 0) / static_cast<float>(p.N);
-                float sq4[4] = {0.f, 0.f, 0.f, 0.f};
+                const float lmean = sum / kCols;
+                float m4[4] = {0.f, 0.f, 0.f, 0.f};
                 for (int c = c_begin; c < c_end; ++c) {
                     tc::tmem_ld32(taddr + c * 32, r);
                     tc::tmem_ld_wait();
 #pragma unroll
                     for (int j = 0; j < 32; ++j) {
-                        const float d = __uint_as_float(r[j]) - mean;
-                        sq4[j & 3] = fmaf(d, d, sq4[j & 3]);
+                        const float d = __uint_as_float(r[j]) - lmean;
+                        m4[j & 3] = fmaf(d, d, m4[j & 3]);
                     }
                 }
-                const float sq = (sq4[0] + sq4[1]) + (sq4[2] + sq4[3]);
-                const float inv = 1.0f / sqrtf(exchange(sq, 1) / static_cast<float>(p.N) + kLnEps);
+                const float2 mine = make_float2(lmean, (m4[0] + m4[1]) + (m4[2] + m4[3]));
+                // exchange: every lane writes its row's partial into each row-sharing CTA, then one
+                // arrive per warp and peer (release.cluster after the warp's stores)
+                float2* slot = part + par * (kMaxNct * 2 * BM);
+                const int my_idx = (static_cast<int>(my_y) * 2 + grp) * BM + r_local;
+                slot[my_idx] = mine;
+                for (uint32_t yy = 0; yy < nct; ++yy)
+                    if (yy != my_y) tc::st_dsmem_f32x2(&slot[my_idx], px + 2 * yy, mine);
+                __syncwarp();
+                if (lane == 0) {
+                    for (uint32_t yy = 0; yy < nct; ++yy)
+                        if (yy != my_y) tc::mbar_arrive_cluster(&lnb[par], px + 2 * yy);
+                    tc::mbar_arrive(&lnb[par]);
+                }
+                tc::mbar_wait_cluster(&lnb[par], (i >> 1) & 1);
+                const int parts = static_cast<int>(2 * nct);
+                float msum = 0.f;
+                for (int j = 0; j < parts; ++j) msum += slot[j * BM + r_local].x;
+                const float mean = msum / static_cast<float>(parts);
+                float m2 = 0.f;
+                for (int j = 0; j < parts; ++j) {
+                    const float2 v = slot[j * BM + r_local];
+                    const float d = v.x - mean;
+                    m2 += v.y + kCols * d * d;
+                }
+                const float inv = 1.0f / sqrtf(m2 / static_cast<float>(p.N) + kLnEps);
                 float y[32];
                 for (int c = c_begin; c < c_end; ++c) {
                     __syncwarp();
@@ -249,10 +295,19 @@ __global__ void __launch_bounds__(Cfg2<LN>::THREADS, 1) gemm2_kernel(const __gri
                     if (c == c_end - 1) release(acc);
                     if (!row_ok) continue;
                     const int64_t col = n0 + c * 32;
+                    const float4* g4 = reinterpret_cast<const float4*>(sprm + BN2 + c * 32);
+                    const float4* e4 = reinterpret_cast<const float4*>(sprm + 2 * BN2 + c * 32);
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        x[j] = __uint_as_float(r[j]);
-                        y[j] = (x[j] - mean) * inv * __ldg(p.gamma + col + j) + __ldg(p.beta + col + j);
+                    for (int j = 0; j < 8; ++j) {
+                        const float4 g = g4[j], e = e4[j];
+                        x[4 * j] = __uint_as_float(r[4 * j]);
+                        x[4 * j + 1] = __uint_as_float(r[4 * j + 1]);
+                        x[4 * j + 2] = __uint_as_float(r[4 * j + 2]);
+                        x[4 * j + 3] = __uint_as_float(r[4 * j + 3]);
+                        y[4 * j] = (x[4 * j] - mean) * inv * g.x + e.x;
+                        y[4 * j + 1] = (x[4 * j + 1] - mean) * inv * g.y + e.y;
+                        y[4 * j + 2] = (x[4 * j + 2] - mean) * inv * g.z + e.z;
+                        y[4 * j + 3] = (x[4 * j + 3] - mean) * inv * g.w + e.w;
                     }
                     store_chunk<T>(p.out, p.ldout, row, col, y);
                     if (p.out_pre_ln) store_chunk<T>(p.out_pre_ln, p.ldout, row, col, x);

@@ -114,6 +114,11 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
     return p;
 }
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
 __device__ __forceinline__ uint64_t policy_evict_last() {
     uint64_t p;
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
@@ -304,6 +309,14 @@ __device__ __forceinline__ void st_dsmem_f32(float* local_addr, uint32_t cta, fl
         "mapa.shared::cluster.u32 ra, %0, %1;\n\t"
         "st.shared::cluster.f32 [ra], %2;\n\t}" ::"r"(smem_u32(local_addr)),
         "r"(cta), "f"(v)
+        : "memory");
+}
+__device__ __forceinline__ void st_dsmem_f32x2(float2* local_addr, uint32_t cta, float2 v) {
+    asm volatile(
+        "{\n\t.reg .b32 ra;\n\t"
+        "mapa.shared::cluster.u32 ra, %0, %1;\n\t"
+        "st.shared::cluster.v2.f32 [ra], {%2, %3};\n\t}" ::"r"(smem_u32(local_addr)),
+        "r"(cta), "f"(v.x), "f"(v.y)
         : "memory");
 }
 __device__ __forceinline__ float ld_dsmem_f32(const float* local_addr, uint32_t cta) {
