@@ -10,6 +10,8 @@ import os
 from pathlib import Path
 
 LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libsf_b200.so"
+if os.environ.get("SF_B200_LIB"):  # alternative build of the same sources (e.g. trace-instrumented)
+    LIB_PATH = Path(os.environ["SF_B200_LIB"]).resolve()
 
 
 class SfError(RuntimeError):

@@ -14,6 +14,9 @@ constexpr int kMaxCluster = 8;
 struct GemmParams {
     CUtensorMap ta;  // X: rows M, cols K
     CUtensorMap tb;  // W: rows N, cols K
+    CUtensorMap tc;    // out: rows M, cols N; 32 x 32 boxes, 64-byte swizzle (TMA-store epilogue)
+    CUtensorMap taux;  // residual (aux), same boxes (TMA-load epilogue)
+    CUtensorMap tpre;  // out_pre_ln, same boxes
     int32_t M, N, K;
     void* out;
     int64_t ldout;
@@ -26,6 +29,7 @@ struct GemmParams {
     void* out_pre_ln;
     int32_t mc;   // single-CTA non-LN: CTAs per cluster along M sharing (multicasting) the weight tile
     int32_t nct;  // pair kernel, LN: n-tiles per row (cluster = 2 x nct CTAs)
+    unsigned long long* trace;  // optional clock64 timeline of pair 0 (built with -DSF_GEMM_TRACE)
 };
 
 template <typename T>
@@ -104,7 +108,7 @@ __device__ __forceinline__ void epi_chunk_pre(const GemmParams& p, const uint32_
 // 32 consecutive values of row `row`, columns [col, col+32): bias -> act -> +aux.
 template <typename T>
 __device__ __forceinline__ void epi_chunk(const GemmParams& p, const uint32_t (&r)[32], int64_t row, int64_t col,
-                                          float (&x)[32]) {
+                                          float (&x)[32], bool with_aux = true) {
 #pragma unroll
     for (int j = 0; j < 32; ++j) x[j] = __uint_as_float(r[j]);
     if (p.bias) {
@@ -119,7 +123,7 @@ __device__ __forceinline__ void epi_chunk(const GemmParams& p, const uint32_t (&
 #pragma unroll
         for (int j = 0; j < 32; ++j) x[j] = act_fn(x[j], p.act);
     }
-    if (p.aux) {
+    if (p.aux && with_aux) {
         const uint4* a4 = reinterpret_cast<const uint4*>(static_cast<const T*>(p.aux) + row * p.ldaux + col);
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
@@ -128,6 +132,21 @@ __device__ __forceinline__ void epi_chunk(const GemmParams& p, const uint32_t (&
 #pragma unroll
             for (int e = 0; e < 8; ++e) x[8 * j + e] += DT<T>::to_f(h[e]);
         }
+    }
+}
+
+// 32 consecutive values of row r (0..31) into a warp's 32 x 32 staging box in the SWIZZLE_64B
+// layout TMA expects: 16-byte chunk j of row r at r*64 + ((j ^ ((r >> 1) & 3)) * 16). A warp's
+// 8-lane phases then hit 8 distinct 16-byte bank groups (conflict-free).
+template <typename T>
+__device__ __forceinline__ void stage_chunk(uint32_t sbase, int r, const float (&x)[32]) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const uint32_t a = sbase + static_cast<uint32_t>(r) * 64u + ((static_cast<uint32_t>(j) ^ ((r >> 1) & 3)) << 4);
+        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(pack2<T>(x[8 * j], x[8 * j + 1])),
+                     "r"(pack2<T>(x[8 * j + 2], x[8 * j + 3])), "r"(pack2<T>(x[8 * j + 4], x[8 * j + 5])),
+                     "r"(pack2<T>(x[8 * j + 6], x[8 * j + 7]))
+                     : "memory");
     }
 }
 

@@ -23,21 +23,39 @@
 #include "epilogue.cuh"
 
 namespace sf {
+extern unsigned long long* g_gemm_trace;
 namespace {
 
 constexpr int BN2 = 256;  // pair tile N; each CTA holds BN2/2 rows of W
 constexpr int kMaxNct = 4;  // LN cluster 2 x nct <= 8 CTAs (portable cluster size)
 
+// clock64 timeline of the leader CTA of pair 0 (tools/gemm_trace.py); -DSF_GEMM_TRACE only
+#ifdef SF_GEMM_TRACE
+#define GTRACE(i, ev)                                                                              \
+    do {                                                                                           \
+        if (p.trace && blockIdx.y == 0 && px == 0 && (i) < 64) p.trace[(i) * 8 + (ev)] = clock64(); \
+    } while (0)
+#else
+#define GTRACE(i, ev) \
+    do {              \
+    } while (0)
+#endif
+
 template <bool LN>
 struct Cfg2 {
-    static constexpr int STAGES = 6;
+    static constexpr int STAGES = LN ? 5 : 6;
     static constexpr int EPI_WARPS = LN ? 8 : 16;
     static constexpr int THREADS = 128 + 32 * EPI_WARPS;
     static constexpr int A_BYTES = BM * BK * 2;         // 16 KB
     static constexpr int B_BYTES = (BN2 / 2) * BK * 2;  // 16 KB
     // LN: (mean, M2) partials [par][y][grp][row] as float2, then this CTA's bias/gamma/beta slice
     static constexpr int RED_FLOATS = LN ? 2 * kMaxNct * 2 * BM * 2 + 3 * BN2 : 0;
-    static constexpr int SMEM = STAGES * (A_BYTES + B_BYTES) + 1024 + 256 + RED_FLOATS * 4;
+    // 32 x 32 fp16 staging boxes per epilogue warp (64-byte swizzle): the residual tile arrives by
+    // TMA load and the output leaves by TMA store through them (LN: a second box for out_pre_ln)
+    static constexpr int NBOX = LN ? 2 : 1;
+    static constexpr int STG_BYTES = EPI_WARPS * NBOX * 2048;
+    static constexpr int BAR_BYTES = 512;
+    static constexpr int SMEM = STAGES * (A_BYTES + B_BYTES) + STG_BYTES + 1024 + BAR_BYTES + RED_FLOATS * 4;
     static constexpr int TMEM_COLS = 2 * BN2;  // double-buffered 128 x 256 fp32 accumulators
 };
 
@@ -48,13 +66,15 @@ __global__ void __launch_bounds__(Cfg2<LN>::THREADS, 1) gemm2_kernel(const __gri
     unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     unsigned char* sA = smem;
     unsigned char* sB = smem + C::STAGES * C::A_BYTES;
-    uint64_t* full = reinterpret_cast<uint64_t*>(sB + C::STAGES * C::B_BYTES);
+    unsigned char* sStg = sB + C::STAGES * C::B_BYTES;  // [EPI_WARPS][NBOX][2 KB], 1024-aligned
+    uint64_t* full = reinterpret_cast<uint64_t*>(sStg + C::STG_BYTES);
     uint64_t* empty = full + C::STAGES;
     uint64_t* tfull = empty + C::STAGES;  // [2]
     uint64_t* tempty = tfull + 2;        // [2] (leader's are used)
     uint64_t* lnb = tempty + 2;          // [2 parity]
-    uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(lnb + 4);
-    float* red = reinterpret_cast<float*>(smem + C::STAGES * (C::A_BYTES + C::B_BYTES) + 256);
+    uint64_t* abar = lnb + 4;            // [EPI_WARPS]: residual box landed
+    uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(abar + C::EPI_WARPS);
+    float* red = reinterpret_cast<float*>(smem + C::STAGES * (C::A_BYTES + C::B_BYTES) + C::STG_BYTES + C::BAR_BYTES);
 
     const uint32_t warp = tc::warp_id();
     const uint32_t lane = threadIdx.x & 31;
@@ -83,6 +103,8 @@ __global__ void __launch_bounds__(Cfg2<LN>::THREADS, 1) gemm2_kernel(const __gri
     if (warp == 0 && lane == 0) {
         tc::prefetch_tmap(&p.ta);
         tc::prefetch_tmap(&p.tb);
+        tc::prefetch_tmap(&p.tc);
+        if (p.aux) tc::prefetch_tmap(&p.taux);
         for (int s = 0; s < C::STAGES; ++s) {
             tc::mbar_init(&full[s], 1);
             tc::mbar_init(&empty[s], 1);
@@ -93,6 +115,7 @@ __global__ void __launch_bounds__(Cfg2<LN>::THREADS, 1) gemm2_kernel(const __gri
         }
         if (LN)  // one arrive per epilogue warp of every CTA holding these rows
             for (int b = 0; b < 2; ++b) tc::mbar_init(&lnb[b], C::EPI_WARPS * nct);
+        for (int w = 0; w < C::EPI_WARPS; ++w) tc::mbar_init(&abar[w], 1);
         tc::fence_barrier_init();
     }
     if (warp == 1) tc::tmem_alloc2<C::TMEM_COLS>(tmem_ptr);
@@ -128,6 +151,7 @@ __global__ void __launch_bounds__(Cfg2<LN>::THREADS, 1) gemm2_kernel(const __gri
                 const int brow = nb * BN2 + static_cast<int>(px) * (BN2 / 2);
                 for (int kb = 0; kb < nk; ++kb) {
                     tc::mbar_wait(&empty[s], ph ^ 1);
+                    if (kb == 0) GTRACE(i, 0);
                     if (px == 0) tc::mbar_expect_tx(&full[s], 2 * (C::A_BYTES + C::B_BYTES));
                     tc::tma_load_2d_pair(sA + s * C::A_BYTES, &p.ta, full0 + 8u * s, kb * BK, arow, pol_a);
                     tc::tma_load_2d_pair(sB + s * C::B_BYTES, &p.tb, full0 + 8u * s, kb * BK, brow, pol_b);
@@ -146,10 +170,12 @@ __global__ void __launch_bounds__(Cfg2<LN>::THREADS, 1) gemm2_kernel(const __gri
             for (int i = 0; tile_of(i, mp, nb); ++i) {
                 const int acc = i & 1;
                 tc::mbar_wait_cluster(&tempty[acc], ((i >> 1) & 1) ^ 1);  // both epilogues drained it
+                GTRACE(i, 1);
                 tc::fence_after_sync();
                 const uint32_t d = tmem + acc * BN2;
                 for (int kb = 0; kb < nk; ++kb) {
                     tc::mbar_wait(&full[s], ph);
+                    if (kb == 0) GTRACE(i, 2);
                     tc::fence_after_sync();
                     const uint32_t a0 = tc::smem_u32(sA + s * C::A_BYTES);
                     const uint32_t b0 = tc::smem_u32(sB + s * C::B_BYTES);
@@ -161,6 +187,7 @@ __global__ void __launch_bounds__(Cfg2<LN>::THREADS, 1) gemm2_kernel(const __gri
                     if (++s == C::STAGES) { s = 0; ph ^= 1; }
                 }
                 tc::mma2_commit_mc(&tfull[acc], pair_mask);
+                GTRACE(i, 3);
             }
         }
     } else if (warp >= 4) {
@@ -180,10 +207,47 @@ __global__ void __launch_bounds__(Cfg2<LN>::THREADS, 1) gemm2_kernel(const __gri
                 else tc::mbar_arrive_cluster(&tempty[acc], leader);
             }
         };
+        // this warp's staging boxes (box 0: residual in / output out; box 1: LN out_pre_ln)
+        unsigned char* const boxp = sStg + (warp - 4) * (C::NBOX * 2048u);
+        const uint32_t box = tc::smem_u32(boxp);
+        uint64_t* const my_abar = &abar[warp - 4];
+        uint32_t aph = 0;
+        auto aux_issue = [&](int col, int row0) {  // lane 0: residual box -> box 0 once its last store read it
+            if (lane == 0) {
+                tc::bulk_wait_read<0>();
+                tc::mbar_expect_tx(my_abar, 2048);
+                tc::tma_load_2d(boxp, &p.taux, my_abar, col, row0);
+            }
+        };
+        auto aux_add = [&](float (&xx)[32]) {  // wait for the box and add this lane's row of it
+            tc::mbar_wait(my_abar, aph);
+            aph ^= 1;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                uint4 u;
+                const uint32_t ad = box + lane * 64u + ((static_cast<uint32_t>(j) ^ ((lane >> 1) & 3)) << 4);
+                asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(u.x), "=r"(u.y), "=r"(u.z), "=r"(u.w) : "r"(ad));
+                const T* h = reinterpret_cast<const T*>(&u);
+#pragma unroll
+                for (int e = 0; e < 8; ++e) xx[8 * j + e] += DT<T>::to_f(h[e]);
+            }
+        };
+        auto store_box = [&](int k, const CUtensorMap* map, const float (&xx)[32], int col, int row0, bool waited) {
+            if (!waited && lane == 0) tc::bulk_wait_read<0>();
+            __syncwarp();
+            stage_chunk<T>(box + k * 2048u, static_cast<int>(lane), xx);
+            tc::fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) {
+                tc::tma_store_2d(map, boxp + k * 2048u, col, row0);
+                tc::bulk_commit();
+            }
+        };
         int mp, nb;
         for (int i = 0; tile_of(i, mp, nb); ++i) {
             const int acc = i & 1;
             tc::mbar_wait(&tfull[acc], (i >> 1) & 1);
+            if (warp == 4 && lane == 0) GTRACE(i, 4);
             tc::fence_after_sync();
             const uint32_t taddr = tmem + acc * BN2 + ((q * 32) << 16);
             const int64_t row = static_cast<int64_t>(2 * mp + static_cast<int>(px)) * BM + r_local;
@@ -191,17 +255,28 @@ __global__ void __launch_bounds__(Cfg2<LN>::THREADS, 1) gemm2_kernel(const __gri
             const int n0 = nb * BN2;
             uint32_t r[32];
             float x[32];
+            const int row0 = (2 * mp + static_cast<int>(px)) * BM + static_cast<int>(q) * 32;
             if constexpr (!LN) {
+                // each 32-row x 32-column chunk: the residual box (if any) arrives by TMA while the
+                // accumulator is read; registers -> swizzled staging box -> one TMA store
+                // (coalesced full-line traffic; rows >= M / cols >= N are clipped by the TMA unit)
                 for (int c = c_begin; c < c_end; ++c) {
+                    const int col = n0 + c * 32;
+                    const bool in_range = col < p.N;  // warp-uniform
+                    if (p.aux && in_range) aux_issue(col, row0);
                     __syncwarp();
                     tc::tmem_ld32(taddr + c * 32, r);
                     tc::tmem_ld_wait();
-                    if (c == c_end - 1) release(acc);
-                    const int64_t col = n0 + c * 32;
-                    if (!row_ok || col >= p.N) continue;
-                    epi_chunk<T>(p, r, row, col, x);
-                    store_chunk<T>(p.out, p.ldout, row, col, x);
+                    if (c == c_end - 1) {
+                        release(acc);
+                        if (warp == 4 && lane == 0) GTRACE(i, 5);
+                    }
+                    if (!in_range) continue;
+                    epi_chunk<T>(p, r, row, col, x, false);
+                    if (p.aux) aux_add(x);
+                    store_box(0, &p.tc, x, col, row0, p.aux != nullptr);
                 }
+                if (warp == 4 && lane == 0) GTRACE(i, 6);
             } else {
                 // LayerNorm over the row split across nct CTAs x GROUPS warps: each thread owns
                 // one row and 128 columns. Pass 1: x = acc + bias + aux back into TMEM, local sum;
@@ -211,33 +286,24 @@ __global__ void __launch_bounds__(Cfg2<LN>::THREADS, 1) gemm2_kernel(const __gri
                 const uint32_t my_y = rank >> 1;
                 constexpr float kCols = 32.f * (CHUNKS / GROUPS);
                 float sum = 0.f;
-                uint4 aux_cur[4], aux_nxt[4];
-                load_aux<T>(p, row_ok, row, n0 + c_begin * 32, aux_cur);
                 for (int c = c_begin; c < c_end; ++c) {
-                    if (c + 1 < c_end) load_aux<T>(p, row_ok, row, n0 + (c + 1) * 32, aux_nxt);
+                    if (p.aux) aux_issue(n0 + c * 32, row0);
                     tc::tmem_ld32(taddr + c * 32, r);
                     tc::tmem_ld_wait();
                     const float4* b4 = reinterpret_cast<const float4*>(sprm + c * 32);
 #pragma unroll
                     for (int j = 0; j < 8; ++j) {
-                        const float4 b = b4[j];
-                        x[4 * j] = __uint_as_float(r[4 * j]) + b.x;
-                        x[4 * j + 1] = __uint_as_float(r[4 * j + 1]) + b.y;
-                        x[4 * j + 2] = __uint_as_float(r[4 * j + 2]) + b.z;
-                        x[4 * j + 3] = __uint_as_float(r[4 * j + 3]) + b.w;
+                        const float4 bb = b4[j];
+                        x[4 * j] = __uint_as_float(r[4 * j]) + bb.x;
+                        x[4 * j + 1] = __uint_as_float(r[4 * j + 1]) + bb.y;
+                        x[4 * j + 2] = __uint_as_float(r[4 * j + 2]) + bb.z;
+                        x[4 * j + 3] = __uint_as_float(r[4 * j + 3]) + bb.w;
                     }
                     if (p.act) {
 #pragma unroll
                         for (int j = 0; j < 32; ++j) x[j] = act_fn(x[j], p.act);
                     }
-                    if (p.aux) {
-#pragma unroll
-                        for (int j = 0; j < 4; ++j) {
-                            const T* h = reinterpret_cast<const T*>(&aux_cur[j]);
-#pragma unroll
-                            for (int e = 0; e < 8; ++e) x[8 * j + e] += DT<T>::to_f(h[e]);
-                        }
-                    }
+                    if (p.aux) aux_add(x);
                     float s4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
                     for (int j = 0; j < 32; ++j) {
@@ -246,8 +312,6 @@ __global__ void __launch_bounds__(Cfg2<LN>::THREADS, 1) gemm2_kernel(const __gri
                     }
                     sum += (s4[0] + s4[1]) + (s4[2] + s4[3]);
                     tc::tmem_st32(taddr + c * 32, r);
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) aux_cur[j] = aux_nxt[j];
                 }
                 tc::tmem_st_wait();
                 const float lmean = sum / kCols;
@@ -293,8 +357,7 @@ __global__ void __launch_bounds__(Cfg2<LN>::THREADS, 1) gemm2_kernel(const __gri
                     tc::tmem_ld32(taddr + c * 32, r);
                     tc::tmem_ld_wait();
                     if (c == c_end - 1) release(acc);
-                    if (!row_ok) continue;
-                    const int64_t col = n0 + c * 32;
+                    const int col = n0 + c * 32;
                     const float4* g4 = reinterpret_cast<const float4*>(sprm + BN2 + c * 32);
                     const float4* e4 = reinterpret_cast<const float4*>(sprm + 2 * BN2 + c * 32);
 #pragma unroll
@@ -309,12 +372,13 @@ __global__ void __launch_bounds__(Cfg2<LN>::THREADS, 1) gemm2_kernel(const __gri
                         y[4 * j + 2] = (x[4 * j + 2] - mean) * inv * g.z + e.z;
                         y[4 * j + 3] = (x[4 * j + 3] - mean) * inv * g.w + e.w;
                     }
-                    store_chunk<T>(p.out, p.ldout, row, col, y);
-                    if (p.out_pre_ln) store_chunk<T>(p.out_pre_ln, p.ldout, row, col, x);
+                    store_box(0, &p.tc, y, col, row0, false);
+                    if (p.out_pre_ln) store_box(1, &p.tpre, x, col, row0, true);
                 }
             }
         }
     }
+    if (warp >= 4 && lane == 0) tc::bulk_wait<0>();  // staged stores done before smem goes away
     tc::fence_before_sync();
     __syncthreads();
     tc::cluster_sync_all();  // the peer's MMAs / remote arrives are done before TMEM goes away
@@ -354,6 +418,9 @@ sf_status launch_pair(const sf_gemm_args& a, cudaStream_t st) {
     const bool bf = std::is_same<T, __nv_bfloat16>::value;
     SF_TRY(make_tmap_2d(&p.ta, a.x, a.M, a.K, a.ldx, BK, BM, bf));
     SF_TRY(make_tmap_2d(&p.tb, a.w, a.N, a.K, a.ldw, BK, BN2 / 2, bf));
+    SF_TRY(make_tmap_2d(&p.tc, a.out, a.M, a.N, a.ldout, 32, 32, bf, 64));
+    if (a.epi.aux) SF_TRY(make_tmap_2d(&p.taux, a.epi.aux, a.M, a.N, a.epi.ldaux, 32, 32, bf, 64));
+    if (a.epi.out_pre_ln) SF_TRY(make_tmap_2d(&p.tpre, a.epi.out_pre_ln, a.M, a.N, a.ldout, 32, 32, bf, 64));
     p.M = a.M; p.N = a.N; p.K = a.K;
     p.out = a.out; p.ldout = a.ldout;
     p.bias = static_cast<const float*>(a.epi.bias);
@@ -367,6 +434,7 @@ sf_status launch_pair(const sf_gemm_args& a, cudaStream_t st) {
     const int mp_tiles = static_cast<int>(ceil_div(a.M, 2 * BM));
     const int nct = LN ? n_tiles : 1;
     p.nct = nct;
+    p.trace = g_gemm_trace;
     auto kern = gemm2_kernel<T, LN>;
     SF_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM));
     SF_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
@@ -391,6 +459,8 @@ sf_status launch_pair(const sf_gemm_args& a, cudaStream_t st) {
 
 }  // namespace
 
+unsigned long long* g_gemm_trace = nullptr;
+
 bool gemm_pair_supported(const sf_gemm_args& a, bool ln) {
     if (a.M <= BM) return false;  // a pair would leave one SM idle
     if (ln) return a.N % BN2 == 0 && a.N / BN2 <= kMaxNct;
@@ -406,3 +476,10 @@ sf_status gemm_pair_dispatch(const sf_gemm_args& a, bool ln, cudaStream_t st) {
 }
 
 }  // namespace sf
+
+// Debug hook (not part of the boundary): clock64 timeline of pair 0 of subsequent CTA-pair GEMM
+// launches into a device buffer of >= 64*8 uint64 (only in builds with -DSF_GEMM_TRACE).
+extern "C" sf_status sf_debug_gemm_trace(void* dev_buf) {
+    sf::g_gemm_trace = static_cast<unsigned long long*>(dev_buf);
+    return SF_OK;
+}

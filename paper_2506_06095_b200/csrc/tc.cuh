@@ -102,6 +102,23 @@ __device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* m, 
         "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(cta_mask)
         : "memory");
 }
+// 2-D TMA store shared -> global of one box (bulk async-group; out-of-bounds parts are clipped)
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* m, const void* src, int32_t c0, int32_t c1) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                     reinterpret_cast<uint64_t>(m)),
+                 "r"(smem_u32(src)), "r"(c0), "r"(c1)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// wait until at most N committed bulk groups are still READING their shared-memory source
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait() {
+    asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
 // 1-D bulk copy global -> shared (16-byte aligned, size multiple of 16), complete_tx on `bar`
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
     asm volatile(
@@ -337,6 +354,6 @@ __device__ __forceinline__ float ld_dsmem_f32(const float* local_addr, uint32_t 
 // a box of box_cols x box_rows and 128-byte swizzle. Uses the driver entry point through the
 // runtime, so the library needs no -lcuda.
 sf_status make_tmap_2d(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint64_t row_stride_elems,
-                       uint32_t box_cols, uint32_t box_rows, bool bf16, bool swizzle128 = true);
+                       uint32_t box_cols, uint32_t box_rows, bool bf16, int swizzle_bytes = 128);
 
 }  // namespace sf
