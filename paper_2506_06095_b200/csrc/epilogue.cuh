@@ -45,25 +45,37 @@ __device__ __forceinline__ uint32_t pack2<__nv_bfloat16>(float a, float b) {
     return *reinterpret_cast<uint32_t*>(&h);
 }
 
-// erf via Abramowitz & Stegun 7.1.26 (|error| <= 1.5e-7, far below the fp16 output rounding):
-// branch-free, one MUFU reciprocal + one MUFU exp2 + 7 FMAs instead of erff's ~20-instruction,
-// divergent two-regime evaluation. The exact-erf GELU semantics of the reference are kept.
-__device__ __forceinline__ float erf_as(float x) {
-    const float z = fabsf(x);
+// GELU(x) = 0.5 x (1 + erf(x / sqrt 2)) (backend.hpp:128-131, exact-erf semantics) evaluated as
+// 0.5 x (1 + tanh(u)) with u(x) an odd polynomial least-squares fitted to atanh(erf(x / sqrt 2))
+// (x clamped to +-8, where tanh has saturated): |formula - exact GELU| <= 2.8e-5 over all x.
+// One MUFU op (tanh.approx.f32, relative error ~2^-11, below the fp16 output rounding) and 7
+// FMA-pipe ops, against rcp + ex2 + ~15 ops for the Abramowitz-Stegun erf this replaced — the
+// GELU epilogue was the bottleneck of the FFN1 GEMM.
+__device__ __forceinline__ float tanh_approx(float u) {
     float t;
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(t) : "f"(fmaf(0.3275911f, z, 1.0f)));
-    float poly = fmaf(1.061405429f, t, -1.453152027f);
-    poly = fmaf(poly, t, 1.421413741f);
-    poly = fmaf(poly, t, -0.284496736f);
-    poly = fmaf(poly, t, 0.254829592f);
-    poly *= t;
-    float e;
-    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(-z * z * 1.4426950408889634f));
-    return copysignf(fmaf(-poly, e, 1.0f), x);
+    asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(u));
+    return t;
+}
+// (clamping x^2 at 64 keeps u monotone beyond |x| = 8, where tanh(u) is already +-1)
+__device__ __forceinline__ float gelu_fast(float x) {
+    const float x2 = fminf(x * x, 64.0f);
+    const float u = x * fmaf(x2, fmaf(x2, -3.53932780e-4f, 3.70247480e-2f), 7.97482758e-1f);
+    return x * fmaf(0.5f, tanh_approx(u), 0.5f);
+}
+// the same on a packed pair (FMUL2 / FFMA2: half the FMA-pipe instructions)
+__device__ __forceinline__ float2 gelu_fast2(float2 x) {
+    float2 x2 = tc::fmul2(x, x);
+    x2.x = fminf(x2.x, 64.0f);
+    x2.y = fminf(x2.y, 64.0f);
+    float2 pl = tc::ffma2(x2, make_float2(-3.53932780e-4f, -3.53932780e-4f), make_float2(3.70247480e-2f, 3.70247480e-2f));
+    pl = tc::ffma2(x2, pl, make_float2(7.97482758e-1f, 7.97482758e-1f));
+    const float2 u = tc::fmul2(x, pl);
+    const float2 h = tc::ffma2(make_float2(0.5f, 0.5f), make_float2(tanh_approx(u.x), tanh_approx(u.y)), make_float2(0.5f, 0.5f));
+    return tc::fmul2(x, h);
 }
 
 __device__ __forceinline__ float act_fn(float x, int act) {
-    if (act == SF_ACT_GELU) return 0.5f * x * (1.0f + erf_as(x * 0.7071067811865475f));  // backend.hpp:128-131
+    if (act == SF_ACT_GELU) return gelu_fast(x);  // backend.hpp:128-131
     if (act == SF_ACT_RELU) return x > 0.f ? x : 0.f;                                    // backend.hpp:132-134
     return x;
 }
@@ -116,12 +128,20 @@ __device__ __forceinline__ void epi_chunk(const GemmParams& p, const uint32_t (&
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
             const float4 b = __ldg(b4 + j);
-            x[4 * j] += b.x; x[4 * j + 1] += b.y; x[4 * j + 2] += b.z; x[4 * j + 3] += b.w;
+            const float2 lo = tc::fadd2(make_float2(x[4 * j], x[4 * j + 1]), make_float2(b.x, b.y));
+            const float2 hi = tc::fadd2(make_float2(x[4 * j + 2], x[4 * j + 3]), make_float2(b.z, b.w));
+            x[4 * j] = lo.x; x[4 * j + 1] = lo.y; x[4 * j + 2] = hi.x; x[4 * j + 3] = hi.y;
         }
     }
-    if (p.act) {
+    if (p.act == SF_ACT_GELU) {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) x[j] = act_fn(x[j], p.act);
+        for (int j = 0; j < 32; j += 2) {
+            const float2 g = gelu_fast2(make_float2(x[j], x[j + 1]));
+            x[j] = g.x; x[j + 1] = g.y;
+        }
+    } else if (p.act == SF_ACT_RELU) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) x[j] = x[j] > 0.f ? x[j] : 0.f;
     }
     if (p.aux && with_aux) {
         const uint4* a4 = reinterpret_cast<const uint4*>(static_cast<const T*>(p.aux) + row * p.ldaux + col);

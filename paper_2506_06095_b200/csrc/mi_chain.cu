@@ -14,7 +14,7 @@ namespace {
 
 constexpr int kWarpsPerCta = 8;
 
-__device__ __forceinline__ float gelu_erf(float x) { return act_fn(x, SF_ACT_GELU); }  // epilogue.cuh (A&S erf)
+__device__ __forceinline__ float gelu_erf(float x) { return gelu_fast(x); }  // epilogue.cuh
 
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
