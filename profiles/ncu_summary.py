@@ -12,7 +12,10 @@ METRICS = {
     "us": "gpu__time_duration.sum",
     "dram_rd_MB": "dram__bytes_read.sum",
     "dram_wr_MB": "dram__bytes_write.sum",
-    "tensor_pct": "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+    # tcgen05 work shows up as tensor-memory (TMEM/UTC) activity; the legacy HMMA pipe counter
+    # (sm__pipe_tensor_cycles_active) stays near zero for tcgen05 kernels
+    "tc_active_pct": "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+    "tc_active_elapsed_pct": "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
     "dram_pct": "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
     "sm_pct": "sm__throughput.avg.pct_of_peak_sustained_elapsed",
     "xu_pct": "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
