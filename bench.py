@@ -188,45 +188,6 @@ def run_reference_arm(args, cfg):
 
 
 # ----------------------------------------------------------------------------------------------
-def kernel_breakdown(L, x, torch, reps=20):
-    """Each launch of one step timed alone (CUDA events, warm, min of reps): name -> ms."""
-    from paper_2506_06095_b200 import fused, sparsefuse as sf
-    W, s = L.W, L.s
-    H = s.hidden
-    ev = lambda: torch.cuda.Event(enable_timing=True)
-    parts = {}
-
-    def t(name, fn):
-        for _ in range(3):
-            fn()
-        best = 1e9
-        for _ in range(reps):
-            a, b = ev(), ev()
-            a.record(); fn(); b.record()
-            torch.cuda.synchronize()
-            best = min(best, a.elapsed_time(b))
-        parts[name] = best
-
-    src = x if L.model == "bert-layer" else L.h
-    if L.model != "bert-layer":
-        t("ln1_mi_chain", lambda: fused.mi_chain(x, L.h, ln_gamma=W["ln1_g"], ln_beta=W["ln1_b"]))
-    t("qkv_gemm", lambda: fused.gemm_fused(src, W["wqkv"], L.qkv, bias=W["bqkv"]))
-    q, k, v = L._heads(L.qkv, 0), L._heads(L.qkv, H), L._heads(L.qkv, 2 * H)
-    t("masked_mha", lambda: sf.mha(q, k, v, L.ctx, out=L._heads(L.attn, 0)))
-    if L.model == "bert-layer":
-        t("out_proj_gemm_ln", lambda: fused.gemm_fused(L.attn, W["wo"], L.x1, bias=W["bo"], aux=x, ln_gamma=W["ln1_g"],
-                                                       ln_beta=W["ln1_b"]))
-        t("ffn1_gemm_gelu", lambda: fused.gemm_fused(L.x1, W["w1"], L.f, bias=W["b1"], act="gelu"))
-        t("ffn2_gemm_ln", lambda: fused.gemm_fused(L.f, W["w2"], L.out, bias=W["b2"], aux=L.x1, ln_gamma=W["ln2_g"],
-                                                   ln_beta=W["ln2_b"]))
-    else:
-        t("out_proj_gemm_ln", lambda: fused.gemm_fused(L.attn, W["wo"], L.h2, bias=W["bo"], aux=x, ln_gamma=W["ln2_g"],
-                                                       ln_beta=W["ln2_b"], out_pre_ln=L.x1))
-        t("ffn1_gemm_act", lambda: fused.gemm_fused(L.h2, W["w1"], L.f, bias=W["b1"], act=L.act))
-        t("ffn2_gemm", lambda: fused.gemm_fused(L.f, W["w2"], L.out, bias=W["b2"], aux=L.x1))
-    return parts
-
-
 def work_model(cfg, nnz):
     """Algorithmic work per launch: flops for GEMMs, compulsory bytes
     and useful flops for the masked MHA."""
@@ -279,6 +240,7 @@ def main():
     # one step = one CUDA-graph replay of the layer's launches (no per-launch host overhead)
     launches0 = _lib.launch_count()
     L.capture(x)
+    L.capture(x, timed=True)  # + event-record nodes between launches: per-kernel device time
     per_step_launches = _lib.launch_count() - launches0 - L.kernels_per_step()  # capture warms once
     for _ in range(3):
         L.replay()
@@ -289,6 +251,7 @@ def main():
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
+    parts_sum = {}
     with ClockSampler(local) as clk:
         time.sleep(0.3)  # the sampler's first reading lands inside the timed region
         for a, b in evs:
@@ -297,6 +260,14 @@ def main():
             L.replay()
             b.record()
         torch.cuda.synchronize()
+        # per-kernel device times: the same K steps again through the instrumented graph (event
+        # nodes between the launches cost ~1 us each, so the headline above runs without them)
+        for _ in range(args.steps):
+            flush.zero_()
+            L.replay(timed=True)
+            torch.cuda.synchronize()
+            for k, v in L.kernel_ms().items():
+                parts_sum[k] = parts_sum.get(k, 0.0) + v
     launches = per_step_launches * args.steps
     if world > 1:
         torch.distributed.barrier()
@@ -360,8 +331,8 @@ def main():
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         e2e_ms = float(t.item())
 
-    # ---- per-kernel breakdown (each launch timed alone) and roofline of the dominant kernel ----
-    parts = kernel_breakdown(L, x, torch)
+    # ---- per-kernel breakdown (mean over the timed steps) and roofline of the dominant kernel ----
+    parts = {k: v / args.steps for k, v in parts_sum.items()}
     wm, mha_flops = work_model(cfg, nnz)
     pk = peaks()
     dom = max(parts, key=parts.get)
@@ -391,7 +362,8 @@ def main():
             "config": {"workload": cfg["desc"], "model": cfg["model"], "global_batch": cfg["bs"] * world,
                        "seq_len": cfg["seq"], "hidden": cfg["hidden"], "heads": cfg["heads"],
                        "parallelism": f"dp{world} (batch x heads sharded, no collective)",
-                       "l2": "flushed (256 MB write) between timed steps, outside the step events"},
+                       "l2": "flushed (256 MB write) between timed steps, outside the step events",
+                       "kernel_timing": "event-record nodes between the launches of an instrumented copy of the step's CUDA graph, K extra steps, mean"},
             "e2e": {"value": tokens / (e2e_ms / 1e3), "unit": "tokens/s",
                     "h2d_bytes_per_step": int(hx.numel() * 2), "d2h_bytes_per_step": int(hy[0].numel() * 2),
                     "copies": "pinned host buffers, H2D/D2H on copy streams overlapping adjacent steps' compute"},

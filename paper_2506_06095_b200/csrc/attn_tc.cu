@@ -2,26 +2,28 @@
 // Replaces block_sparse_sdpa (attention.hpp:71-172) for BSR tiles of block_m = 128 query rows
 // and block_n in {16, 32, 64} key columns, head_size 64, fp16/bf16.
 //
-// One CTA per (128-row block, b*h slice); 320 threads, 2 CTAs per SM:
-//   warp 0     producer (one thread): the Q tile once (128 x 64, 128B-swizzled TMA), then per
-//              step the K and V rows of G = 64/block_n load-list column blocks, GATHERED into one
-//              contiguous 64-key stage (4-D tensor maps over (d, n, h, b) read Q/K/V in any
-//              (b,h,i) stride layout in place, e.g. the fused-QKV activation), plus the packed bit
-//              tiles of the step's PART tiles bulk-copied from the BSR pool (full tiles need no
-//              bits). kStages-deep ring, one transaction barrier per stage.
+// Persistent: two CTAs per SM (grid = min(items, 2 x SMs)); a CTA walks its work items (128-row
+// block, b*h slice) round-robin, row blocks ranked by descending load count. Every role runs
+// ahead across item boundaries (Q is double-buffered, the K/V ring and the S/P/O TMEM buffers
+// continue), so the next item's loads and first QK^T overlap the current item's tail. 192 threads:
+//   warp 0     producer: Q of each item (128 x 64, 128B-swizzled TMA), then per step the K and V
+//              rows of G = 64/block_n load-list column blocks, GATHERED into one contiguous 64-key
+//              stage (4-D tensor maps over (d, n, h, b) read Q/K/V in any (b,h,i) stride layout in
+//              place, e.g. the fused-QKV activation), the packed bit tiles of the step's PART tiles
+//              bulk-copied from the BSR pool (full tiles need no bits) and the step's tile kinds.
+//              kStages-deep ring, one transaction barrier per stage.
 //   warp 1     TMEM allocator + MMA issuer (one elected thread):
 //                S_j = Q K_j^T   tcgen05.mma (SS) M=128 N=64 K=16 x4 -> TMEM S[j%2] (fp32)
 //                O  += P_j V_j   tcgen05.mma (TS) M=128 N=64 K=16 x4, A = P_j read straight from
 //                                TMEM P[j%2] (fp16 pairs), B = V as an MN-major operand from the
 //                                TMA stage; O accumulates in TMEM. No P round trip through smem.
-//   warps 2-9  softmax, two threads per query row (TMEM lane; 32 columns each, the row max is
-//              exchanged through smem per step): tcgen05.ld S_j, masked row max, p = 2^(s*scale*
-//              log2e - m) with a lazily updated max m (O is rescaled in TMEM only when the row max
-//              grows by more than 2^8, FA4-style, so P <= 256 fits fp16), P_j packed to fp16 and
-//              tcgen05.st back into TMEM. 16-column groups masked for all 32 rows of a warp skip
-//              their exp/max work.
-//   epilogue   out = O / l; rows that never saw a valid score are exactly zero
-//              (attention.hpp:160-166).
+//   warps 2-5  softmax, one thread per query row (TMEM lane), 64 columns per step: tcgen05.ld S_j,
+//              masked row max, p = 2^(s*scale*log2e - m) with a lazily updated max m (O is
+//              rescaled in TMEM only when the row max grows by more than 2^8, FA4-style, so
+//              P <= 256 fits fp16), P_j packed to fp16 and tcgen05.st back into TMEM. 16-column
+//              groups masked for all 32 rows of a warp skip their exp/max work.
+//   epilogue   (same warps, per item) out = O / l; rows that never saw a valid score are exactly
+//              zero (attention.hpp:160-166).
 // Only the BSR load set is iterated: empty tiles are never touched (attention.hpp:104-109).
 #include <algorithm>
 
@@ -31,41 +33,40 @@ namespace sf {
 namespace {
 
 constexpr int kBM = 128, kD = 64, kNS = 64;  // query rows, head size, keys per step
-constexpr int kThreads = 320;                // producer, MMA, 8 softmax warps
-constexpr int kStages = 5;
+constexpr int kThreads = 192;                // producer warp, MMA warp, 4 softmax warps
+constexpr int kStages = 4;                   // K/V ring depth (two CTAs per SM share 228 KB)
 // TMEM columns: S[s] at 64*s (fp32), P[s] at 128 + 32*s (packed fp16 pairs), O at 192. P gets its
 // own buffers: an in-flight P.V MMA may still read P_j while the next S MMA is writing, so P
 // must not alias S. S_{j+2}'s commit covers P_j V_j, so P[j%2] is free again at step j+2.
 constexpr int kSBuf = 2;
 constexpr uint32_t kPCol = 128, kOCol = 192;
-constexpr int kMaxLoads = 512;               // load-list entries per row block (n <= 8192 at bn 16)
+constexpr int kMaxRowBlocks = 64;            // n <= 8192 at block_m 128
 constexpr int kQBytes = kBM * kD * 2;
 constexpr int kKVBytes = kNS * kD * 2;       // one 64-key stage of K (or V)
 constexpr int kMaskBytes = kBM * 8;          // 64 bits per query row per stage
 constexpr float kRescaleLog2 = 8.0f;         // lazy-rescale threshold (P <= 2^8)
-constexpr int kSmem = 1024 + kQBytes + 2 * kStages * kKVBytes + kStages * kMaskBytes + kMaxLoads * 8 +
-                      6 * kBM * 4 + 512;
+constexpr int kSmem = 1024 + 2 * kQBytes + 2 * kStages * kKVBytes + kStages * kMaskBytes + kStages * 16 +
+                      kMaxRowBlocks * 4 + 256;
 
 struct AttnParams {
     CUtensorMap tq, tk, tv;  // 4-D (d, n, h, b) maps; boxes {64,128,1,1} / {64,bn,1,1}
-    int32_t n, h, bn, G;
+    int32_t n, h, bh, n_rows, n_items;
     const int32_t* load_row_ptr;
     const int32_t* load_col_idx;
     const int32_t* load_tile;
     const uint8_t* pool;
-    int32_t tile_bytes;
     void* o;
     int64_t o_sb, o_sh, o_sn;
     float scale_log2;
-    unsigned long long* trace;  // optional clock64 trace of CTA (0,0) (sf_debug_attn_trace)
+    unsigned long long* trace;  // optional clock64 trace of CTA 0 (sf_debug_attn_trace)
 };
 
-// clock64 timeline of CTA (0,0) for tools/attn_trace.py; compiled in only with -DSF_ATTN_TRACE
+// clock64 timeline of CTA 0 for tools/attn_trace.py; compiled in only with -DSF_ATTN_TRACE
 // (the predicated stores otherwise cost issue slots in the softmax loop)
 #ifdef SF_ATTN_TRACE
 #define SF_TRACE(j, ev)                                                                   \
     do {                                                                                  \
-        if (p.trace && blockIdx.x == 0 && blockIdx.y == 0 && (j) < 64) p.trace[(j) * 16 + (ev)] = clock64(); \
+        if (p.trace && blockIdx.x == 0 && (j) < 64) p.trace[(j) * 16 + (ev)] = clock64(); \
     } while (0)
 #else
 #define SF_TRACE(j, ev) \
@@ -92,6 +93,38 @@ __device__ __forceinline__ uint32_t pack2<__nv_bfloat16>(float a, float b) {
     return *reinterpret_cast<uint32_t*>(&h);
 }
 
+// 2^x for a pair on the FMA pipe (FA4's MUFU offload): x = j + f with j = rint(x) from the
+// 1.5*2^23 rounding trick, 2^f on [-0.5, 0.5] by a degree-4 Taylor polynomial (rel. error
+// < 5e-5, well under the fp16 spacing of P), and j added straight into the exponent field.
+// x is clamped at -125 so masked (-inf) cells give a tiny positive value that packs to 0.
+#ifndef SF_ATTN_EMU
+#define SF_ATTN_EMU 3
+#endif
+constexpr int kEmuPairs = SF_ATTN_EMU;  // of the 8 pairs in each 16-column group
+__device__ __forceinline__ float2 ex2_emu2(float2 x) {
+    x = make_float2(fmaxf(x.x, -125.f), fmaxf(x.y, -125.f));
+    const float2 t = tc::fadd2(x, make_float2(12582912.f, 12582912.f));
+    const float2 jf = tc::fadd2(t, make_float2(-12582912.f, -12582912.f));
+    const float2 f = tc::ffma2(jf, make_float2(-1.f, -1.f), x);
+    float2 p = tc::ffma2(make_float2(9.6181291e-3f, 9.6181291e-3f), f, make_float2(5.5504109e-2f, 5.5504109e-2f));
+    p = tc::ffma2(p, f, make_float2(2.4022651e-1f, 2.4022651e-1f));
+    p = tc::ffma2(p, f, make_float2(6.9314718e-1f, 6.9314718e-1f));
+    p = tc::ffma2(p, f, make_float2(1.f, 1.f));
+    return make_float2(__uint_as_float(__float_as_uint(p.x) + (__float_as_uint(t.x) << 23)),
+                       __uint_as_float(__float_as_uint(p.y) + (__float_as_uint(t.y) << 23)));
+}
+
+// v if bit `bit` of `bits` is set, else -inf. Written as and/setp/selp so ptxas lowers a run of
+// them to one R2P (7 predicates from a register byte) + one FSEL per element.
+__device__ __forceinline__ float mask_sel(uint32_t bits, uint32_t bit, float v) {
+    float o;
+    asm("{\n\t.reg .pred p;\n\t.reg .b32 t;\n\tand.b32 t, %1, %2;\n\tsetp.ne.b32 p, t, 0;\n\t"
+        "selp.f32 %0, %3, 0fFF800000, p;\n\t}"
+        : "=f"(o)
+        : "r"(bits), "r"(bit), "f"(v));
+    return o;
+}
+
 using tc::fadd2;
 using tc::ffma2;
 using tc::fmax3;
@@ -106,6 +139,11 @@ __device__ __forceinline__ uint32_t lds_u16(uint32_t addr) {
     asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(addr));
     return v;
 }
+__device__ __forceinline__ int4 lds_v4(uint32_t addr) {
+    int4 v;
+    asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+    return v;
+}
 
 __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* m, uint64_t* bar, int32_t c0, int32_t c1,
                                             int32_t c2, int32_t c3) {
@@ -116,17 +154,45 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* m, uin
         : "memory");
 }
 
-__device__ __forceinline__ void named_sync(uint32_t id, uint32_t n) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-__device__ __forceinline__ void st_shared_f32(uint32_t addr, float v) {
-    asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
-}
-__device__ __forceinline__ float ld_shared_f32(uint32_t addr) {
-    float v;
-    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
-    return v;
-}
+// The CTA's work items, in the order every role walks them. Item idx = blockIdx.x + k*gridDim.x
+// over (row-block rank, b*h) with row blocks ranked by descending load count, so the static
+// round robin hands the longest items out first (a cheap LPT schedule).
+struct Items {
+    const int32_t* lrp;
+    const int32_t* order;  // smem: row block of each rank
+    int bh_count, n_items, G;
+    __device__ __forceinline__ int count() const {
+        return blockIdx.x < n_items ? (n_items - 1 - static_cast<int>(blockIdx.x)) / static_cast<int>(gridDim.x) + 1 : 0;
+    }
+    __device__ __forceinline__ void get(int k, int& rb, int& bh, int& l0, int& L, int& nsteps) const {
+        const int idx = static_cast<int>(blockIdx.x) + k * static_cast<int>(gridDim.x);
+        rb = order[idx / bh_count];
+        bh = idx % bh_count;
+        l0 = lrp[rb];
+        L = lrp[rb + 1] - l0;
+        nsteps = (L + G - 1) / G;
+    }
+};
+
+// Flat walk over the steps of the CTA's non-empty items (the MMA issuer keeps two of these: the
+// S cursor runs kSBuf steps ahead of the P.V cursor).
+struct Cursor {
+    int k = -1, qi = -1, j = 0, ns = 0;
+    bool valid = false;
+    __device__ __forceinline__ bool next_item(const Items& it, int nitems) {
+        int rb, bh, l0, L;
+        do {
+            if (++k >= nitems) return valid = false;
+            it.get(k, rb, bh, l0, L, ns);
+        } while (ns == 0);
+        ++qi;
+        j = 0;
+        return valid = true;
+    }
+    __device__ __forceinline__ void advance(const Items& it, int nitems) {
+        if (++j == ns) next_item(it, nitems);
+    }
+};
 
 template <typename T, int BN>
 __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_constant__ AttnParams p) {
@@ -134,54 +200,54 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
     constexpr int TB = kBM * BN / 8;     // packed bytes of one part tile (pool stride)
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    unsigned char* sQ = sm;
-    unsigned char* sK = sQ + kQBytes;
+    unsigned char* sQ = sm;                               // [2] Q tiles (double-buffered across items)
+    unsigned char* sK = sQ + 2 * kQBytes;
     unsigned char* sV = sK + kStages * kKVBytes;
-    unsigned char* sMask = sV + kStages * kKVBytes;  // [kStages][1 KB]: packed part-tile bits
-    int32_t* s_col = reinterpret_cast<int32_t*>(sMask + kStages * kMaskBytes);
-    int32_t* s_tile = s_col + kMaxLoads;
-    float* s_red = reinterpret_cast<float*>(s_tile + kMaxLoads);  // [3][2][128]: max exchange x2, final l
-    uint64_t* bars = reinterpret_cast<uint64_t*>(s_red + 6 * kBM);
-    uint64_t* q_full = bars;
-    uint64_t* kv_full = q_full + 1;          // [kStages]
-    uint64_t* kv_empty = kv_full + kStages;  // [kStages]
-    uint64_t* s_full = kv_empty + kStages;   // [kSBuf]
-    uint64_t* p_full = s_full + kSBuf;       // [kSBuf]
-    uint64_t* o_full = p_full + kSBuf;       // [2]: P.V step j completes o_full[j&1] (parity waits are
-                                             // unambiguous only within one phase of lag)
+    unsigned char* sMask = sV + kStages * kKVBytes;        // [kStages][1 KB]: packed part-tile bits
+    int32_t* s_kind = reinterpret_cast<int32_t*>(sMask + kStages * kMaskBytes);  // [kStages][4]
+    int32_t* s_order = s_kind + 4 * kStages;                                      // [kMaxRowBlocks]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(s_order + kMaxRowBlocks);
+    uint64_t* q_full = bars;                  // [2]
+    uint64_t* q_empty = q_full + 2;           // [2]
+    uint64_t* kv_full = q_empty + 2;          // [kStages]
+    uint64_t* kv_empty = kv_full + kStages;   // [kStages]
+    uint64_t* s_full = kv_empty + kStages;    // [kSBuf]
+    uint64_t* p_full = s_full + kSBuf;        // [kSBuf]
+    uint64_t* o_full = p_full + kSBuf;        // [2]: P.V step g completes o_full[g&1] (parity waits are
+                                              // unambiguous only within one phase of lag)
     uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(o_full + 2);
 
     const uint32_t warp = tc::warp_id();
     const uint32_t lane = threadIdx.x & 31;
-    const int br = blockIdx.x;
-    const int bh = blockIdx.y;
-    const int b = bh / p.h, hh = bh % p.h;
-    const int l0 = p.load_row_ptr[br];
-    const int L = p.load_row_ptr[br + 1] - l0;
-    const int nsteps = (L + G - 1) / G;
-    const uint32_t s_col_a = tc::smem_u32(s_col), s_tile_a = tc::smem_u32(s_tile);
-    auto col_at = [&](int e) { return static_cast<int>(lds_u32(s_col_a + 4u * e)); };
-    auto tile_at = [&](int e) { return static_cast<int>(lds_u32(s_tile_a + 4u * e)); };
 
-    for (int i = threadIdx.x; i < L; i += kThreads) {
-        s_col[i] = p.load_col_idx[l0 + i];
-        s_tile[i] = p.load_tile[l0 + i];
+    // row blocks ranked by descending load count (ties by index)
+    if (static_cast<int>(threadIdx.x) < p.n_rows) {
+        const int r = threadIdx.x;
+        const int Lr = p.load_row_ptr[r + 1] - p.load_row_ptr[r];
+        int rank = 0;
+        for (int i = 0; i < p.n_rows; ++i) {
+            const int Li = p.load_row_ptr[i + 1] - p.load_row_ptr[i];
+            rank += (Li > Lr) || (Li == Lr && i < r);
+        }
+        s_order[rank] = r;
     }
     if (warp == 0 && lane == 0) {
         tc::prefetch_tmap(&p.tq);
         tc::prefetch_tmap(&p.tk);
         tc::prefetch_tmap(&p.tv);
-        tc::mbar_init(q_full, 1);
+        for (int i = 0; i < 2; ++i) {
+            tc::mbar_init(&q_full[i], 1);
+            tc::mbar_init(&q_empty[i], 1);
+            tc::mbar_init(&o_full[i], 1);
+        }
         for (int s = 0; s < kStages; ++s) {
             tc::mbar_init(&kv_full[s], 1);
             tc::mbar_init(&kv_empty[s], 1);
         }
         for (int s = 0; s < kSBuf; ++s) {
             tc::mbar_init(&s_full[s], 1);
-            tc::mbar_init(&p_full[s], 256);
+            tc::mbar_init(&p_full[s], 128);
         }
-        tc::mbar_init(&o_full[0], 1);
-        tc::mbar_init(&o_full[1], 1);
         tc::fence_barrier_init();
     }
     if (warp == 1) tc::tmem_alloc<256>(tmem_ptr);
@@ -190,37 +256,55 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
     tc::fence_after_sync();
     const uint32_t tmem = *tmem_ptr;
     const uint32_t tO = tmem + kOCol;
+    const Items items{p.load_row_ptr, s_order, p.bh, p.n_items, G};
+    const int nitems = items.count();
 
     if (warp == 0) {
-        // ------------------------------------------------------------------ producer
-        if (nsteps > 0 && tc::elect_one()) {
-            constexpr int bn = BN;
-            tc::mbar_expect_tx(q_full, kQBytes);
-            tma_load_4d(sQ, &p.tq, q_full, 0, br * kBM, hh, b);
-            const int chunk = bn * kD * 2;
-            int s = 0;
-            uint32_t ph = 0;
-            for (int j = 0; j < nsteps; ++j) {
-                tc::mbar_wait(&kv_empty[s], ph ^ 1);
-                int parts = 0;
+        // ------------------------------------------------------------------ producer (one warp)
+        // Lanes fetch 32 load-list entries at a time; lane 0 issues the TMA for each step.
+        int g = 0, qi = 0;
+        for (int k = 0; k < nitems; ++k) {
+            int rb, bh, l0, L, nsteps;
+            items.get(k, rb, bh, l0, L, nsteps);
+            if (nsteps == 0) continue;
+            const int b = bh / p.h, hh = bh % p.h;
+            if (lane == 0) {
+                tc::mbar_wait(&q_empty[qi & 1], ((qi >> 1) & 1) ^ 1);
+                tc::mbar_expect_tx(&q_full[qi & 1], kQBytes);
+                tma_load_4d(sQ + (qi & 1) * kQBytes, &p.tq, &q_full[qi & 1], 0, rb * kBM, hh, b);
+            }
+            ++qi;
+            for (int c = 0; c < L; c += 32) {
+                const int e = c + static_cast<int>(lane);
+                const int my_col = p.load_col_idx[l0 + (e < L ? e : 0)];  // pad: valid, fully masked
+                const int my_tile = e < L ? p.load_tile[l0 + e] : -2;
+                const int j1 = min(nsteps, (c + 32) / G);
+                for (int j = c / G; j < j1; ++j, ++g) {
+                    const int st = g % kStages;
+                    int parts = 0;
+                    int cols[G], tiles[G];
 #pragma unroll
-                for (int g = 0; g < G; ++g) {
-                    const int e = j * G + g;
-                    parts += (e < L && tile_at(e) >= 0);
-                }
-                tc::mbar_expect_tx(&kv_full[s], 2 * kKVBytes + parts * TB);
+                    for (int gg = 0; gg < G; ++gg) {
+                        cols[gg] = __shfl_sync(0xffffffffu, my_col, j * G + gg - c);
+                        tiles[gg] = __shfl_sync(0xffffffffu, my_tile, j * G + gg - c);
+                        parts += tiles[gg] >= 0;
+                    }
+                    if (lane == 0) {
+                        tc::mbar_wait(&kv_empty[st], ((g / kStages) & 1) ^ 1);
 #pragma unroll
-                for (int g = 0; g < G; ++g) {
-                    const int e = j * G + g;
-                    const int col = col_at(e < L ? e : 0) * bn;  // pad: valid, fully masked
-                    tma_load_4d(sK + s * kKVBytes + g * chunk, &p.tk, &kv_full[s], 0, col, hh, b);
-                    tma_load_4d(sV + s * kKVBytes + g * chunk, &p.tv, &kv_full[s], 0, col, hh, b);
-                    const int t = e < L ? tile_at(e) : -2;
-                    if (t >= 0)
-                        tc::bulk_load(sMask + s * kMaskBytes + g * TB, p.pool + static_cast<int64_t>(t) * TB, TB,
-                                      &kv_full[s]);
+                        for (int gg = 0; gg < G; ++gg) s_kind[4 * st + gg] = tiles[gg];
+                        tc::mbar_expect_tx(&kv_full[st], 2 * kKVBytes + parts * TB);  // release: s_kind
+#pragma unroll
+                        for (int gg = 0; gg < G; ++gg) {
+                            const int col = cols[gg] * BN;
+                            tma_load_4d(sK + st * kKVBytes + gg * BN * kD * 2, &p.tk, &kv_full[st], 0, col, hh, b);
+                            tma_load_4d(sV + st * kKVBytes + gg * BN * kD * 2, &p.tv, &kv_full[st], 0, col, hh, b);
+                            if (tiles[gg] >= 0)
+                                tc::bulk_load(sMask + st * kMaskBytes + gg * TB,
+                                              p.pool + static_cast<int64_t>(tiles[gg]) * TB, TB, &kv_full[st]);
+                        }
+                    }
                 }
-                if (++s == kStages) { s = 0; ph ^= 1; }
             }
         }
     } else if (warp == 1) {
@@ -228,187 +312,219 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
         constexpr bool bf = std::is_same<T, __nv_bfloat16>::value;
         constexpr uint32_t idesc_s = tc::idesc_f16(kBM, kNS, bf, 0, 0);  // Q (K-major) x K (K-major)
         constexpr uint32_t idesc_o = tc::idesc_f16(kBM, kD, bf, 0, 1);   // P (TMEM) x V (MN-major)
-        if (tc::elect_one() && nsteps > 0) {
-            const uint32_t q0 = tc::smem_u32(sQ);
-            tc::mbar_wait(q_full, 0);
-            auto issue_s = [&](int j) {
-                const int s = j % kStages;
-                tc::mbar_wait(&kv_full[s], (j / kStages) & 1);
+        if (tc::elect_one()) {
+            Cursor cs, cp;
+            cs.next_item(items, nitems);
+            cp.next_item(items, nitems);
+            int gS = 0;
+            auto issue_s = [&]() {
+                if (cs.j == 0) {
+                    tc::mbar_wait(&q_full[cs.qi & 1], (cs.qi >> 1) & 1);
+                    tc::fence_after_sync();
+                }
+                const int s = gS % kStages;
+                SF_TRACE(gS, 13);
+                tc::mbar_wait(&kv_full[s], (gS / kStages) & 1);
+                SF_TRACE(gS, 14);
                 tc::fence_after_sync();
+                const uint32_t q0 = tc::smem_u32(sQ + (cs.qi & 1) * kQBytes);
                 const uint32_t k0 = tc::smem_u32(sK + s * kKVBytes);
 #pragma unroll
                 for (int k = 0; k < kD / 16; ++k)
-                    tc::mma_f16_ss(tmem + 64 * (j % kSBuf), tc::sdesc_sw128(q0 + 32 * k), tc::sdesc_sw128(k0 + 32 * k),
+                    tc::mma_f16_ss(tmem + 64 * (gS % kSBuf), tc::sdesc_sw128(q0 + 32 * k), tc::sdesc_sw128(k0 + 32 * k),
                                    idesc_s, k != 0);
-                tc::mma_commit(&s_full[j % kSBuf]);
+                tc::mma_commit(&s_full[gS % kSBuf]);
+                if (cs.j == cs.ns - 1) tc::mma_commit(&q_empty[cs.qi & 1]);  // last S of the item: Q free
+                ++gS;
+                cs.advance(items, nitems);
             };
-            for (int j = 0; j < kSBuf && j < nsteps; ++j) issue_s(j);
-            for (int j = 0; j < nsteps; ++j) {
-                const int s = j % kStages;
-                const int sb = j % kSBuf;
-                tc::mbar_wait(&p_full[sb], (j / kSBuf) & 1);  // P_j in TMEM (S_j consumed), O rescaled
-                SF_TRACE(j, 8);
+            for (int j = 0; j < kSBuf && cs.valid; ++j) issue_s();
+            for (int g = 0; cp.valid; ++g) {
+                const int s = g % kStages;
+                const int sb = g % kSBuf;
+                tc::mbar_wait(&p_full[sb], (g / kSBuf) & 1);  // P_g in TMEM (S_g consumed), O rescaled
+                SF_TRACE(g, 8);
                 tc::fence_after_sync();
                 const uint32_t v0 = tc::smem_u32(sV + s * kKVBytes);
 #pragma unroll
-                for (int k = 0; k < kNS / 16; ++k)  // P_j: 64 keys = 32 packed columns, 8 per K=16
+                for (int k = 0; k < kNS / 16; ++k)  // P_g: 64 keys = 32 packed columns, 8 per K=16
                     tc::mma_f16_ts(tO, tmem + kPCol + 32 * sb + 8 * k, tc::sdesc_sw128_mn(v0 + 2048 * k), idesc_o,
-                                   (j | k) != 0);
-                tc::mma_commit(&o_full[j & 1]);
+                                   (cp.j | k) != 0);
+                tc::mma_commit(&o_full[g & 1]);
                 tc::mma_commit(&kv_empty[s]);
-                SF_TRACE(j, 9);
-                if (j + kSBuf < nsteps) issue_s(j + kSBuf);
-                SF_TRACE(j, 10);
-#ifdef SF_ATTN_TRACE
-                if (p.trace && blockIdx.x == 0 && blockIdx.y == 0 && j + kSBuf < nsteps) {
-                    // diagnosis only: observe this thread's own S commit (pure MMA-chain latency)
-                    tc::mbar_wait(&s_full[(j + kSBuf) % kSBuf], ((j + kSBuf) / kSBuf) & 1);
-                    SF_TRACE(j, 11);
-                    tc::mbar_wait(&o_full[j & 1], (j >> 1) & 1);
-                    SF_TRACE(j, 12);
-                }
-#endif
+                SF_TRACE(g, 9);
+                if (cs.valid) issue_s();
+                SF_TRACE(g, 10);
+                cp.advance(items, nitems);
             }
         }
     } else {
         // ------------------------------------------------------------------ softmax / epilogue
-        // Two threads per query row: warps 2-5 own columns 0-31 of the step, warps 6-9 columns
-        // 32-63, of TMEM lane quarter warp%4. The row max is exchanged through smem with a
-        // 64-thread named barrier per lane quarter; row sums stay per-half until the end.
-        const uint32_t q = warp & 3;
-        const int half = static_cast<int>(warp - 2) >> 2;
+        // One thread per query row (TMEM lane), all 64 columns of the step.
+        const uint32_t q = warp & 3;  // TMEM lane quarter this warp may access
         const int r = static_cast<int>(q * 32 + lane);
         const uint32_t trow = tmem + ((q * 32) << 16);
-        const uint32_t bar_id = 1 + q;
-        const uint32_t red = tc::smem_u32(s_red);
         const float sl2 = p.scale_log2;
-        float m = -INFINITY, l = 0.f;
-        for (int j = 0; j < nsteps; ++j) {
-            const int st = j % kStages;
-            const int sb = j % kSBuf;
-            const bool tr = warp == 2 && lane == 0;
-            if (tr) SF_TRACE(j, 0);
-            tc::mbar_wait(&kv_full[st], (j / kStages) & 1);
-            if (tr) SF_TRACE(j, 1);
-            // this thread's 32 mask bits (keys 32h..32h+31 of the step): full tile -> ones, part
-            // tile -> its staged pool row, padding -> 0. Only this half's tiles are read.
-            uint32_t bits = 0;
-            {
-                const uint32_t mb = tc::smem_u32(sMask + st * kMaskBytes);
-                if constexpr (BN == 16) {
+        const uint32_t kind_a = tc::smem_u32(s_kind);
+        int g = 0;
+        for (int k = 0; k < nitems; ++k) {
+            int rb, bh, l0, L, nsteps;
+            items.get(k, rb, bh, l0, L, nsteps);
+            float m = -INFINITY, l = 0.f;
+            for (int j = 0; j < nsteps; ++j, ++g) {
+                const int st = g % kStages;
+                const int sb = g % kSBuf;
+                const bool tr = warp == 2 && lane == 0 && k == 0;
+                if (tr) SF_TRACE(j, 0);
+                tc::mbar_wait(&kv_full[st], (g / kStages) & 1);
+                if (tr) SF_TRACE(j, 1);
+                // this row's 64 mask bits: full tile -> ones, part tile -> its staged pool row,
+                // padding -> 0
+                uint32_t bits[2];
+                {
+                    const int4 kd = lds_v4(kind_a + 16u * st);
+                    const int kinds[4] = {kd.x, kd.y, kd.z, kd.w};
+                    const uint32_t mb = tc::smem_u32(sMask + st * kMaskBytes);
+                    if constexpr (BN == 16) {
 #pragma unroll
-                    for (int gg = 0; gg < 2; ++gg) {
-                        const int g = 2 * half + gg, e = j * G + g;
-                        const int t = e < L ? tile_at(e) : -2;
-                        const uint32_t b16 = t == -1 ? 0xffffu : (t >= 0 ? lds_u16(mb + g * TB + r * 2) : 0u);
-                        bits |= b16 << (16 * gg);
+                        for (int w = 0; w < 2; ++w) {
+                            uint32_t v = 0;
+#pragma unroll
+                            for (int gg = 0; gg < 2; ++gg) {
+                                const int t = kinds[2 * w + gg];
+                                const uint32_t b16 =
+                                    t == -1 ? 0xffffu : (t >= 0 ? lds_u16(mb + (2 * w + gg) * TB + r * 2) : 0u);
+                                v |= b16 << (16 * gg);
+                            }
+                            bits[w] = v;
+                        }
+                    } else if constexpr (BN == 32) {
+#pragma unroll
+                        for (int w = 0; w < 2; ++w) {
+                            const int t = kinds[w];
+                            bits[w] = t == -1 ? ~0u : (t >= 0 ? lds_u32(mb + w * TB + r * 4) : 0u);
+                        }
+                    } else {
+                        const int t = kinds[0];
+#pragma unroll
+                        for (int w = 0; w < 2; ++w) bits[w] = t == -1 ? ~0u : (t >= 0 ? lds_u32(mb + r * 8 + 4 * w) : 0u);
                     }
-                } else if constexpr (BN == 32) {
-                    const int e = j * G + half;
-                    const int t = e < L ? tile_at(e) : -2;
-                    bits = t == -1 ? ~0u : (t >= 0 ? lds_u32(mb + half * TB + r * 4) : 0u);
-                } else {
-                    const int t = j < L ? tile_at(j) : -2;
-                    bits = t == -1 ? ~0u : (t >= 0 ? lds_u32(mb + r * 8 + 4 * half) : 0u);
                 }
-            }
-            tc::mbar_wait(&s_full[sb], (j / kSBuf) & 1);
-            if (tr) SF_TRACE(j, 2);
-            tc::fence_after_sync();
-            uint32_t raw[32];
-            tc::tmem_ld32(trow + 64 * sb + 32 * half, raw);
-            const bool act0 = __any_sync(0xffffffffu, (bits & 0xffffu) != 0);
-            const bool act1 = __any_sync(0xffffffffu, (bits >> 16) != 0);
-            tc::tmem_ld_wait();
-            // masked cells -> -inf once: they drop out of the max and ex2(-inf) = 0 later
-            float sr[32];
-#pragma unroll
-            for (int c = 0; c < 32; ++c) sr[c] = (bits & (1u << c)) ? __uint_as_float(raw[c]) : -INFINITY;
-            float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-            if (act0) {
-#pragma unroll
-                for (int c = 0; c < 16; c += 2) mx4[(c >> 1) & 3] = fmax3(mx4[(c >> 1) & 3], sr[c], sr[c + 1]);
-            }
-            if (act1) {
-#pragma unroll
-                for (int c = 16; c < 32; c += 2) mx4[(c >> 1) & 3] = fmax3(mx4[(c >> 1) & 3], sr[c], sr[c + 1]);
-            }
-            // max of the raw scores, then scaled: scale > 0 commutes with max (log2 domain)
-            float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * sl2;
-            const uint32_t xch = red + 4u * ((j & 1) * 2 * kBM);  // [2 halves][128], double-buffered
-            st_shared_f32(xch + 4u * (half * kBM + r), mx);
-            if (tr) SF_TRACE(j, 3);
-            named_sync(bar_id, 64);  // also orders both halves' S loads before any P store below
-            if (tr) SF_TRACE(j, 4);
-            mx = fmaxf(mx, ld_shared_f32(xch + 4u * ((1 - half) * kBM + r)));
-            // lazy max update (identical in both halves): rescale O / l only when the max grows by
-            // > 2^8 (or first time). tcgen05.ld/st are warp-collective: the rescale is voted
-            // warp-uniformly and lanes that do not need it scale by 1.
-            const bool upd = mx > m + kRescaleLog2 || (m == -INFINITY && mx > -INFINITY);
-            const float m_new = upd ? mx : m;
-            const bool resc = upd && m > -INFINITY && j > 0;
-            if (__any_sync(0xffffffffu, resc)) {
-                const float a = resc ? ex2(m - m_new) : 1.f;
-                l *= a;
-                tc::mbar_wait(&o_full[(j - 1) & 1], ((j - 1) >> 1) & 1);  // P_{j-1} V_{j-1} landed in O
+                tc::mbar_wait(&s_full[sb], (g / kSBuf) & 1);
+                if (tr) SF_TRACE(j, 2);
                 tc::fence_after_sync();
-                uint32_t ov[32];
-                tc::tmem_ld32(tO + ((q * 32) << 16) + 32 * half, ov);
+                uint32_t raw0[32], raw1[32];
+                tc::tmem_ld32(trow + 64 * sb, raw0);
+                tc::tmem_ld32(trow + 64 * sb + 32, raw1);
+                bool act[4];
+#pragma unroll
+                for (int a = 0; a < 4; ++a) act[a] = __any_sync(0xffffffffu, ((bits[a >> 1] >> (16 * (a & 1))) & 0xffffu) != 0);
                 tc::tmem_ld_wait();
+                // masked cells -> -inf once: they drop out of the max and 2^(-inf) = 0 later
+                float sr[64];
 #pragma unroll
-                for (int e = 0; e < 32; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * a);
-                tc::tmem_st32(tO + ((q * 32) << 16) + 32 * half, ov);
-            }
-            m = m_new;
-            uint32_t pk[16];
-            float2 rs2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-            const float2 sl2x2 = make_float2(sl2, sl2), negm = make_float2(-m, -m);
+                for (int a = 0; a < 4; ++a) {
+                    const uint32_t* rw = a < 2 ? raw0 : raw1;
+                    const uint32_t bw = bits[a >> 1];
 #pragma unroll
-            for (int g = 0; g < 2; ++g) {
-                if (!(g ? act1 : act0) || m == -INFINITY) {
-#pragma unroll
-                    for (int c = 8 * g; c < 8 * g + 8; ++c) pk[c] = 0u;
-                    continue;
+                    for (int c = 0; c < 16; ++c) {
+                        const int cc = 16 * (a & 1) + c;
+                        sr[16 * a + c] = mask_sel(bw, 1u << cc, __uint_as_float(rw[cc]));
+                    }
                 }
+                float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-                for (int c = 16 * g; c < 16 * g + 16; c += 2) {
-                    const float2 arg = ffma2(make_float2(sr[c], sr[c + 1]), sl2x2, negm);
-                    const float2 pp = make_float2(ex2(arg.x), ex2(arg.y));  // masked: ex2(-inf) = 0
-                    rs2[(c >> 1) & 1] = fadd2(rs2[(c >> 1) & 1], pp);
-                    pk[c >> 1] = pack2<T>(pp.x, pp.y);
+                for (int a = 0; a < 4; ++a) {
+                    if (act[a]) {
+#pragma unroll
+                        for (int c = 16 * a; c < 16 * a + 16; c += 4)
+                            mx4[(c >> 2) & 3] = fmax3(mx4[(c >> 2) & 3], fmax3(sr[c], sr[c + 1], sr[c + 2]), sr[c + 3]);
+                    }
+                }
+                // max of the raw scores, then scaled: scale > 0 commutes with max (log2 domain)
+                const float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * sl2;
+                if (tr) SF_TRACE(j, 3);
+                // lazy max update: rescale O / l only when the max grows by > 2^8 (or first time).
+                // tcgen05.ld/st are warp-collective: the rescale is voted warp-uniformly and lanes
+                // that do not need it scale by 1.
+                const bool upd = mx > m + kRescaleLog2 || (m == -INFINITY && mx > -INFINITY);
+                const float m_new = upd ? mx : m;
+                const bool resc = upd && m > -INFINITY && j > 0;
+                if (__any_sync(0xffffffffu, resc)) {
+                    const float a = resc ? ex2(m - m_new) : 1.f;
+                    l *= a;
+                    tc::mbar_wait(&o_full[(g - 1) & 1], ((g - 1) >> 1) & 1);  // P_{g-1} V_{g-1} landed in O
+                    tc::fence_after_sync();
+#pragma unroll
+                    for (int h2 = 0; h2 < 2; ++h2) {
+                        uint32_t ov[32];
+                        tc::tmem_ld32(tO + ((q * 32) << 16) + 32 * h2, ov);
+                        tc::tmem_ld_wait();
+#pragma unroll
+                        for (int e = 0; e < 32; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * a);
+                        tc::tmem_st32(tO + ((q * 32) << 16) + 32 * h2, ov);
+                    }
+                }
+                m = m_new;
+                uint32_t pk[32];
+                float2 rs2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+                const float2 sl2x2 = make_float2(sl2, sl2), negm = make_float2(-m, -m);
+#pragma unroll
+                for (int a = 0; a < 4; ++a) {
+                    if (!act[a] || m == -INFINITY) {
+#pragma unroll
+                        for (int c = 8 * a; c < 8 * a + 8; ++c) pk[c] = 0u;
+                        continue;
+                    }
+#pragma unroll
+                    for (int c = 16 * a; c < 16 * a + 16; c += 2) {
+                        const float2 arg = ffma2(make_float2(sr[c], sr[c + 1]), sl2x2, negm);
+                        // the last kEmuPairs pairs of each group on the FMA pipe, the rest on MUFU
+                    const float2 pp = ((c >> 1) & 7) >= 8 - kEmuPairs ? ex2_emu2(arg)
+                                                                      : make_float2(ex2(arg.x), ex2(arg.y));
+                        rs2[(c >> 1) & 1] = fadd2(rs2[(c >> 1) & 1], pp);
+                        pk[c >> 1] = pack2<T>(pp.x, pp.y);
+                    }
+                }
+                l += (rs2[0].x + rs2[0].y) + (rs2[1].x + rs2[1].y);
+                // P_g (64 keys = 32 packed columns) into P[sb] in TMEM
+                tc::tmem_st32(trow + kPCol + 32 * sb, pk);
+                tc::tmem_st_wait();
+                tc::fence_before_sync();
+                tc::mbar_arrive(&p_full[sb]);
+                if (tr) SF_TRACE(j, 6);
+            }
+            // ---- epilogue: out = O / l; rows without a valid column stay zero
+            const int b = bh / p.h, hh = bh % p.h;
+            const int64_t i = static_cast<int64_t>(rb) * kBM + r;
+            if (nsteps > 0) {
+                tc::mbar_wait(&o_full[(g - 1) & 1], ((g - 1) >> 1) & 1);
+                tc::fence_after_sync();
+            }
+            const float inv = (nsteps > 0 && l > 0.f) ? 1.f / l : 0.f;
+            uint4* dst = reinterpret_cast<uint4*>(static_cast<T*>(p.o) + b * p.o_sb + hh * p.o_sh + i * p.o_sn);
+#pragma unroll
+            for (int h2 = 0; h2 < 2; ++h2) {
+                uint32_t ov[32];
+                if (nsteps > 0) {
+                    tc::tmem_ld32(tO + ((q * 32) << 16) + 32 * h2, ov);
+                    tc::tmem_ld_wait();
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) ov[e] = 0u;
+                }
+                if (i < p.n) {
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        float v[8];
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) v[e] = __uint_as_float(ov[c * 8 + e]) * inv;
+                        dst[4 * h2 + c] = make_uint4(pack2<T>(v[0], v[1]), pack2<T>(v[2], v[3]), pack2<T>(v[4], v[5]),
+                                                     pack2<T>(v[6], v[7]));
+                    }
                 }
             }
-            l += (rs2[0].x + rs2[0].y) + (rs2[1].x + rs2[1].y);
-            // P_j (this half: keys 32h..32h+31 = packed columns 16h..16h+15) into P[sb] in TMEM
-            tc::tmem_st16(trow + kPCol + 32 * sb + 16 * half, pk);
-            tc::tmem_st_wait();
-            tc::fence_before_sync();
-            tc::mbar_arrive(&p_full[sb]);
-            if (tr) SF_TRACE(j, 6);
-        }
-        // ---- epilogue: out = O / (l_half0 + l_half1); rows without a valid column stay zero
-        st_shared_f32(red + 4u * (4 * kBM + half * kBM + r), l);
-        named_sync(bar_id, 64);
-        l += ld_shared_f32(red + 4u * (4 * kBM + (1 - half) * kBM + r));
-        const int64_t i = static_cast<int64_t>(br) * kBM + r;
-        uint32_t ov[32];
-        if (nsteps > 0) {
-            tc::mbar_wait(&o_full[(nsteps - 1) & 1], ((nsteps - 1) >> 1) & 1);
-            tc::fence_after_sync();
-            tc::tmem_ld32(tO + ((q * 32) << 16) + 32 * half, ov);
-            tc::tmem_ld_wait();
-        }
-        if (i < p.n) {
-            const float inv = l > 0.f ? 1.f / l : 0.f;
-            uint4* dst = reinterpret_cast<uint4*>(static_cast<T*>(p.o) + b * p.o_sb + hh * p.o_sh + i * p.o_sn + 32 * half);
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                float v[8];
-#pragma unroll
-                for (int e = 0; e < 8; ++e) v[e] = nsteps > 0 ? __uint_as_float(ov[c * 8 + e]) * inv : 0.f;
-                dst[c] = make_uint4(pack2<T>(v[0], v[1]), pack2<T>(v[2], v[3]), pack2<T>(v[4], v[5]),
-                                    pack2<T>(v[6], v[7]));
-            }
+            tc::fence_before_sync();  // O reads ordered before the next item's first P.V (p_full)
         }
     }
     tc::fence_before_sync();
@@ -446,7 +562,7 @@ unsigned long long* g_attn_trace = nullptr;
 
 sf_status attn_tc(const sf_attn_args& a, const sf_bsr_dev& b, cudaStream_t st, bool probe_only) {
     const bool shape_ok = b.block_m == kBM && (b.block_n == 16 || b.block_n == 32 || b.block_n == 64) &&
-                          a.head_size == kD && b.n_cols <= kMaxLoads;
+                          a.head_size == kD && b.n_rows <= kMaxRowBlocks;
     const bool layout_ok = a.q_sn % 8 == 0 && a.q_sh % 8 == 0 && a.q_sb % 8 == 0 && a.o_sn % 8 == 0 &&
                            a.o_sh % 8 == 0 && a.o_sb % 8 == 0 &&
                            ((reinterpret_cast<uintptr_t>(a.q) | reinterpret_cast<uintptr_t>(a.k) |
@@ -462,13 +578,13 @@ sf_status attn_tc(const sf_attn_args& a, const sf_bsr_dev& b, cudaStream_t st, b
     SF_TRY(make_tmap_4d(&p.tv, a.v, a.seq_len, a.h, a.bs, a.q_sn, a.q_sh, a.q_sb, b.block_n, bf));
     p.n = a.seq_len;
     p.h = a.h;
-    p.bn = b.block_n;
-    p.G = kNS / b.block_n;
+    p.bh = a.bs * a.h;
+    p.n_rows = b.n_rows;
+    p.n_items = b.n_rows * p.bh;
     p.load_row_ptr = b.load_row_ptr;
     p.load_col_idx = b.load_col_idx;
     p.load_tile = b.load_tile;
     p.pool = b.pool;
-    p.tile_bytes = b.tile_bytes;
     p.o = a.o;
     p.o_sb = a.o_sb;
     p.o_sh = a.o_sh;
@@ -481,7 +597,14 @@ sf_status attn_tc(const sf_attn_args& a, const sf_bsr_dev& b, cudaStream_t st, b
     else kern = bf ? attn_tc_kernel<__nv_bfloat16, 64> : attn_tc_kernel<__half, 64>;
     if (b.tile_bytes != kBM * b.block_n / 8) return fail(SF_PLAN_ERROR, "BSR tile_bytes does not match block shape");
     SF_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
-    dim3 grid(b.n_rows, static_cast<unsigned>(a.bs) * a.h);
+    static int n_sm = 0;
+    if (!n_sm) {
+        int dev = 0;
+        SF_CUDA_TRY(cudaGetDevice(&dev));
+        SF_CUDA_TRY(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
+    }
+    // persistent: two CTAs per SM (smem and TMEM are sized for it), items round-robin
+    dim3 grid(static_cast<unsigned>(std::min<int64_t>(p.n_items, 2 * n_sm)));
     kern<<<grid, kThreads, kSmem, st>>>(p);
     SF_LAUNCH_CHECK();
     return SF_OK;

@@ -339,7 +339,9 @@ __global__ void __launch_bounds__(Cfg2<LN>::THREADS, 1) gemm2_kernel(const __gri
                         if (yy != my_y) tc::mbar_arrive_cluster(&lnb[par], px + 2 * yy);
                     tc::mbar_arrive(&lnb[par]);
                 }
+                if (warp == 4 && lane == 0) GTRACE(i, 7);  // partials out (passes 1-2 done)
                 tc::mbar_wait_cluster(&lnb[par], (i >> 1) & 1);
+                if (warp == 4 && lane == 0) GTRACE(i, 6);  // exchange complete
                 const int parts = static_cast<int>(2 * nct);
                 float msum = 0.f;
                 for (int j = 0; j < parts; ++j) msum += slot[j * BM + r_local].x;

@@ -91,55 +91,87 @@ class EncoderLayer:
         self.f = e(M, F)
         self.out = e(M, H)
         self.graph = None
+        self.graph_timed = None
+        self.marks = []
 
     # (bs, heads, seq, d) views of a (bs*seq, width) activation at column offset c0
     def _heads(self, t: torch.Tensor, c0: int) -> torch.Tensor:
         s = self.s
         return t[:, c0:c0 + s.hidden].view(s.bs, s.seq_len, s.heads, s.head_size).permute(0, 2, 1, 3)
 
-    def _mha(self, src: torch.Tensor, stream=None):
+    def _mha(self, src: torch.Tensor, stream=None, mark=None):
         H = self.s.hidden
         if self.compat:
             q = k = v = self._heads(src, 0)
         else:
             fused.gemm_fused(src, self.W["wqkv"], self.qkv, bias=self.W["bqkv"], stream=stream)
+            mark("qkv_gemm")
             q, k, v = self._heads(self.qkv, 0), self._heads(self.qkv, H), self._heads(self.qkv, 2 * H)
         sf.mha(q, k, v, self.ctx, out=self._heads(self.attn, 0), stream=stream)
+        mark("masked_mha")
 
-    def forward(self, x: torch.Tensor, stream=None) -> torch.Tensor:
+    def forward(self, x: torch.Tensor, stream=None, mark=None) -> torch.Tensor:
+        """One layer step. `mark(name)`, if given, is called after each launch (the bench records a
+        timing event there)."""
         W, A = self.W, self.aux
+        mark = mark or (lambda name: None)
         if self.model == "bert-layer":
-            self._mha(x, stream)
+            self._mha(x, stream, mark)
             fused.gemm_fused(self.attn, W["wo"], self.x1, bias=W["bo"], aux=A.get("add1", x),
                              ln_gamma=W["ln1_g"], ln_beta=W["ln1_b"], stream=stream)
+            mark("out_proj_gemm_ln")
             fused.gemm_fused(self.x1, W["w1"], self.f, bias=W["b1"], act="gelu", stream=stream)
+            mark("ffn1_gemm_gelu")
             fused.gemm_fused(self.f, W["w2"], self.out, bias=W["b2"], aux=A.get("add2", self.x1),
                              ln_gamma=W["ln2_g"], ln_beta=W["ln2_b"], stream=stream)
+            mark("ffn2_gemm_ln")
         else:
             fused.mi_chain(x, self.h, ln_gamma=W["ln1_g"], ln_beta=W["ln1_b"], stream=stream)
-            self._mha(self.h, stream)
+            mark("ln1_mi_chain")
+            self._mha(self.h, stream, mark)
             fused.gemm_fused(self.attn, W["wo"], self.h2, bias=W["bo"], aux=A.get("add1", x),
                              ln_gamma=W["ln2_g"], ln_beta=W["ln2_b"], out_pre_ln=self.x1, stream=stream)
+            mark("out_proj_gemm_ln")
             fused.gemm_fused(self.h2, W["w1"], self.f, bias=W["b1"], act=self.act, stream=stream)
+            mark("ffn1_gemm_act")
             fused.gemm_fused(self.f, W["w2"], self.out, bias=W["b2"], aux=A.get("add2", self.x1), stream=stream)
+            mark("ffn2_gemm")
         return self.out
 
     def kernels_per_step(self) -> int:
         n = 4 if self.model == "bert-layer" else 5
         return n + (0 if self.compat else 1)
 
-    # CUDA graph of one step (launch-bound small configs)
-    def capture(self, x: torch.Tensor) -> None:
+    # CUDA graph of one step (launch-bound small configs). timed=True adds an event-record node
+    # before the first launch and after every launch (self.marks: [(name, event)], "start" first),
+    # so per-kernel device time is read from the real step without host overhead.
+    def capture(self, x: torch.Tensor, timed: bool = False) -> None:
         s = torch.cuda.Stream()
         s.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(s):
             self.forward(x, stream=s)  # warm (tensor maps, attributes)
         torch.cuda.current_stream().wait_stream(s)
         g = torch.cuda.CUDAGraph()
+        self.marks = []
+        mark = None
+        if timed:
+            def mark(name):
+                e = torch.cuda.Event(enable_timing=True, external=True)
+                e.record(s)
+                self.marks.append((name, e))
         with torch.cuda.graph(g, stream=s):
-            self.forward(x, stream=s)
-        self.graph = g
+            if timed:
+                mark("start")
+            self.forward(x, stream=s, mark=mark)
+        if timed:
+            self.graph_timed = g
+        else:
+            self.graph = g
 
-    def replay(self):
-        self.graph.replay()
+    def kernel_ms(self) -> Dict[str, float]:
+        """Per-launch device time of the last replay of a timed capture."""
+        return {n: a.elapsed_time(b) for (_, a), (n, b) in zip(self.marks, self.marks[1:])}
+
+    def replay(self, timed: bool = False):
+        (self.graph_timed if timed else self.graph).replay()
         return self.out

@@ -1,7 +1,8 @@
 """clock64 timeline of CTA pair 0 of the CTA-pair GEMM (needs the trace build:
 make -C paper_2506_06095_b200/csrc OUT=$PWD/paper_2506_06095_b200/_lib_trace EXTRA_NVFLAGS=-DSF_GEMM_TRACE).
 Events per tile: 0 producer first k-block, 1 MMA got accumulator, 2 MMA first stage full,
-3 MMA committed tile, 4 epilogue saw tfull, 5 epilogue released TMEM, 6 epilogue stores issued."""
+3 MMA committed tile, 4 epilogue saw tfull, 5 epilogue released TMEM, 6 epilogue stores issued
+(LN: 6 = row-statistics exchange complete, 7 = own partials sent)."""
 import ctypes as C
 import os
 import sys
@@ -15,8 +16,9 @@ from paper_2506_06095_b200 import _lib, fused
 L = _lib.lib()
 L.sf_debug_gemm_trace.argtypes = [C.c_void_p]
 M = 16384
+ln = lambda N: {"ln_gamma": torch.rand(N, device="cuda") + 0.5, "ln_beta": torch.rand(N, device="cuda") - 0.5}
 for name, N, K, kw in (("qkv", 2304, 768, {}), ("ffn1_gelu", 3072, 768, {"act": "gelu"}),
-                       ("ffn2", 768, 3072, {})):
+                       ("ffn2", 768, 3072, {}), ("out_ln", 768, 768, ln(768)), ("ffn2_ln", 768, 3072, ln(768))):
     x = torch.randn(M, K, device="cuda").half()
     w = (torch.randn(N, K, device="cuda") * 0.02).half()
     b = torch.randn(N, device="cuda")
@@ -39,6 +41,6 @@ for name, N, K, kw in (("qkv", 2304, 768, {}), ("ffn1_gelu", 3072, 768, {"act": 
         mma = r[3] - r[2]
         epi = r[6] - r[4]
         print(f"tile {i:2d}: prod {r[0]:7d} mma_acc {r[1]:7d} first_full {r[2]:7d} commit {r[3]:7d} | "
-              f"epi_in {r[4]:7d} rel {r[5]:7d} done {r[6]:7d} | mma {mma:6d} epi {epi:6d}"
+              f"epi_in {r[4]:7d} rel {r[5]:7d} done {r[6]:7d} ln_part {r[7]:7d} | mma {mma:6d} epi {epi:6d}"
               + (f" gap {r[2] - prev:6d}" if prev is not None else ""))
         prev = r[3]
