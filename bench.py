@@ -202,6 +202,138 @@ def work_model(cfg, nnz):
     return w, mha_flops
 
 
+# ----------------------------------------------------------------------------------------------
+# cfg5: masking-pattern x sequence-length sweep of the masked MHA (BASELINE configs[4])
+SWEEP_PATTERNS = ("sliding", "dilated", "longformer", "bigbird", "causal", "strided")
+SWEEP_SEQ = (128, 256, 512, 1024, 2048, 4096, 8192)
+MUFU_PER_CLK_SM = 16  # ex2 throughput per SM per clock on sm_100 (B300's doubled SFU is sm_103 only)
+
+
+def sweep_terms(pattern, n):
+    w = int(np.floor(np.sqrt(n)))  # band and global width = sqrt(seq_len)
+    return {"sliding": [dict(pattern="sliding", seq_len=n, band_width=w)],
+            "dilated": [dict(pattern="dilated", seq_len=n, band_width=w, dilation_rate=1)],
+            "longformer": [dict(pattern="longformer", seq_len=n, global_width=w, band_width=w)],
+            "bigbird": [dict(pattern="bigbird", seq_len=n, global_width=w, band_width=w, filling_rate=0.10, seed=0,
+                             block=16)],
+            "causal": [dict(pattern="causal", seq_len=n)],
+            "strided": [dict(pattern="strided", seq_len=n, band_width=w)]}[pattern]
+
+
+def run_sweep(args):
+    """Masked-MHA latency and % of roofline for every (pattern, n), bs 16 x 12 heads x 64 on one
+    GPU (the sweep shards (b, h) units over ranks with no exchange, so per-GPU work is this at any
+    N). Roofline per SURVEY §8(d): bound = max(useful flops / tensor peak, exps / MUFU rate,
+    compulsory bytes / HBM peak). One JSON line per point; the reference's own block_sparse_sdpa
+    (16x16 BSR, oracle/_ref) is timed on one (b, h) slice where that takes < ~2 s and scaled."""
+    import torch
+    from paper_2506_06095_b200 import sparsefuse as sf
+    torch.cuda.set_device(0)
+    pk = peaks()
+    clk_hz = 1.965e9
+    bs, h, d = 16, 12, 64
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    ref = None
+    if not args.no_cpu_baseline:
+        from oracle.oracle import Reference
+        ref = Reference()
+        if not ref.available:
+            ref = None
+    pats = args.patterns.split(",") if args.patterns else SWEEP_PATTERNS
+    seqs = [int(x) for x in args.seqs.split(",")] if args.seqs else SWEEP_SEQ
+    for n in seqs:
+        g = torch.Generator(device="cuda").manual_seed(1)
+        q, k, v = ((torch.rand(bs, h, n, d, device="cuda", generator=g) * 2 - 1).half() for _ in range(3))
+        o = torch.empty_like(q)
+        for pat in pats:
+            dm = sf.generate_mask(sweep_terms(pat, n))
+            nnz = dm.true_count()
+            plan = sf.select_plan(dm, sf.hw_preset("b200"), n, h, bs, d, mode="b200")
+            ctx = sf.MhaContext(dm, plan)
+            run = lambda: sf.mha(q, k, v, ctx, out=o)
+            for _ in range(3):
+                run()
+            st = torch.cuda.Stream()
+            st.wait_stream(torch.cuda.current_stream())
+            gr = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gr, stream=st):
+                sf.mha(q, k, v, ctx, out=o, stream=st)
+            ts = []
+            for _ in range(args.steps):
+                flush.zero_()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(); gr.replay(); b.record()
+                torch.cuda.synchronize()
+                ts.append(a.elapsed_time(b) * 1e3)
+            us = statistics.median(ts)
+            flops = 4.0 * d * bs * h * nnz
+            exps = float(bs * h * nnz)
+            comp = 4.0 * bs * h * n * d * 2
+            t_tc = flops / (pk["tflops"] * 1e12) * 1e6
+            t_exp = exps / (MUFU_PER_CLK_SM * 148 * clk_hz) * 1e6
+            t_hbm = comp / (pk["hbm_gbs"] * 1e9) * 1e6
+            bound_us = max(t_tc, t_exp, t_hbm)
+            binds = ("tensor", "mufu", "hbm")[[t_tc, t_exp, t_hbm].index(bound_us)]
+            line = {"sweep": "masked_mha", "pattern": pat, "seq_len": n, "bs": bs, "heads": h, "head_size": d,
+                    "nnz_per_slice": nnz, "density": nnz / float(n * n),
+                    "plan": [plan.kind, plan.block_m, plan.block_n], "latency_us": us,
+                    "useful_tflops": flops / us / 1e6, "compulsory_gbs": comp / us / 1e3,
+                    "roofline": {"bound": binds, "bound_us": bound_us, "t_tensor_us": t_tc, "t_mufu_us": t_exp,
+                                 "t_hbm_us": t_hbm, "frac": bound_us / us},
+                    "l2": "flushed before each timed launch", "timing": f"median of {args.steps} single launches"}
+            if plan.kind == "block_wise":
+                line["executed_cells_per_slice"] = int(ctx.bsr.n_load) * plan.block_m * plan.block_n
+
+            def time_launch(fn):
+                st2 = torch.cuda.Stream()
+                st2.wait_stream(torch.cuda.current_stream())
+                for _ in range(2):
+                    fn(None)
+                g2 = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g2, stream=st2):
+                    fn(st2)
+                tt = []
+                for _ in range(max(5, args.steps // 2)):
+                    flush.zero_()
+                    a2, b2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    a2.record(); g2.replay(); b2.record()
+                    torch.cuda.synchronize()
+                    tt.append(a2.elapsed_time(b2) * 1e3)
+                return statistics.median(tt)
+
+            # both executors where the other one is affordable: the data behind the selector
+            if args.both and bs * h * nnz <= 4e8:
+                if plan.kind == "block_wise":
+                    rw = sf.build_rowwise(dm)
+                    line["rowwise_us"] = time_launch(lambda s_: sf.rowwise_sdpa(q, k, v, rw, out=o, stream=s_))
+                    del rw
+                else:
+                    line["rowwise_us"] = us
+            if args.both and plan.kind != "block_wise":
+                bsr = sf.build_bsr(dm, 128, 16)
+                line["blockwise_us"] = time_launch(lambda s_: sf.block_sparse_sdpa(q, k, v, bsr, out=o, stream=s_))
+                line["executed_cells_per_slice"] = int(bsr.n_load) * 128 * 16
+                del bsr
+            elif args.both:
+                line["blockwise_us"] = us
+            if ref is not None and nnz <= 6_000_000:
+                from oracle.oracle import Oracle
+                o_ = Oracle()
+                m = o_.mask(sweep_terms(pat, n))
+                q1, k1, v1 = (x[:1, :1].float().cpu().numpy() for x in (q, k, v))
+                t0 = time.perf_counter()
+                ref.block_sparse_sdpa(q1, k1, v1, m, 16, 16, threads=1)
+                sl = time.perf_counter() - t0
+                line["cpu_baseline"] = {"kind": "reference", "cores": 1, "slice_ms": sl * 1e3,
+                                        "latency_us_scaled": sl * 1e6 * bs * h,
+                                        "sample": "one (b,h) slice of the reference block_sparse_sdpa (16x16 BSR), "
+                                                  "scaled by bs*h (the per-slice work is identical, attention.hpp:58-59)"}
+            print(json.dumps(line), flush=True)
+            del ctx
+        del q, k, v, o
+        torch.cuda.empty_cache()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -210,7 +342,13 @@ def main():
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sweep", action="store_true", help="cfg5: masked-MHA pattern x seq_len sweep (JSON lines)")
+    ap.add_argument("--patterns", default="", help="--sweep: comma list (default: all six)")
+    ap.add_argument("--seqs", default="", help="--sweep: comma list (default: 128..8192)")
+    ap.add_argument("--both", action="store_true", help="--sweep: also time the executor the plan did not pick")
     args = ap.parse_args()
+    if args.sweep:
+        return run_sweep(args)
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         return run_reference_arm(args, cfg)

@@ -4,12 +4,15 @@
 //   split into 4 groups of 8 lanes; each group handles one gathered key at a time, so a K/V row
 //   of d fp16 is read by 8 lanes with 16-byte vector loads (coalesced 128-byte row for d=64).
 //   Per-group online softmax in fp32, merged across the 4 groups with shuffles at the end.
+//   attn_rowwise64: the head-size-64 specialisation (two keys in flight per group, FFMA2, lazy
+//   max update).
 //
 // attn_bsr_generic: the block-skipping executor (attention.hpp:71-172) for ANY tile shape the
 //   reference accepts (the tcgen05 kernel in attn_tc.cu covers block_m = 128). One CTA per
 //   (row block, b*h); one thread per query row; K/V tiles staged through shared memory; the
 //   per-load-entry tile id (-1 = full) replaces the merge walk.
 #include <algorithm>
+#include <type_traits>
 
 #include "common.cuh"
 
@@ -106,6 +109,133 @@ __global__ void __launch_bounds__(256) attn_rowwise_kernel(sf_attn_args a, const
 #pragma unroll
         for (int e = 0; e < DPL; ++e)
             if (d0 + e < d) O[d0 + e] = DT<T>::from_f(acc[e] * inv);
+    }
+}
+
+// Head size 64, 16-byte aligned rows (the common case): same warp/group geometry, but each
+// group keeps TWO gathered keys in flight (4 x 16-byte loads issued before any use), the dot and
+// P.V updates run as packed fp32 pairs (FFMA2), and the running max is updated lazily (rescale
+// only when a score exceeds the max by > 2^8, so p <= 256): one exp2 per key instead of two.
+__device__ __forceinline__ void h8_to_f(const uint4& raw, float2 (&f)[4]) {
+    const __half2* h = reinterpret_cast<const __half2*>(&raw);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) f[e] = __half22float2(h[e]);
+}
+__device__ __forceinline__ void h8_to_f(const uint4& raw, float2 (&f)[4], __nv_bfloat16) {
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) f[e] = __bfloat1622float2(h[e]);
+}
+template <typename T>
+__device__ __forceinline__ void cvt8(const uint4& raw, float2 (&f)[4]) {
+    if constexpr (std::is_same<T, __half>::value) h8_to_f(raw, f);
+    else h8_to_f(raw, f, __nv_bfloat16{});
+}
+__device__ __forceinline__ float2 f2fma(float2 a, float2 b, float2 c) {
+    float2 d;
+    asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+        "mov.b64 rc, {%6, %7};\n\tfma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+        : "=f"(d.x), "=f"(d.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+    return d;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) attn_rowwise64_kernel(sf_attn_args a, const int32_t* __restrict__ row_ptr,
+                                                             const int32_t* __restrict__ col_idx) {
+    constexpr float kLazy = 8.0f;
+    const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t rows = static_cast<int64_t>(a.bs) * a.h * a.seq_len;
+    if (gw >= rows) return;
+    const int lane = threadIdx.x & 31, grp = lane >> 3, gl = lane & 7;
+    const int64_t i = gw % a.seq_len;
+    const int64_t bh = gw / a.seq_len;
+    const int64_t b = bh / a.h, hh = bh % a.h;
+    const int64_t base = b * a.q_sb + hh * a.q_sh + gl * 8;
+    const T* Q = static_cast<const T*>(a.q) + base;
+    const T* K = static_cast<const T*>(a.k) + base;
+    const T* V = static_cast<const T*>(a.v) + base;
+    const float sl2 = a.scale * 1.4426950408889634f;
+    float2 q[4], acc[4];
+    {
+        cvt8<T>(*reinterpret_cast<const uint4*>(Q + i * a.q_sn), q);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            q[e] = make_float2(q[e].x * sl2, q[e].y * sl2);  // scores come out in the log2 domain
+            acc[e] = make_float2(0.f, 0.f);
+        }
+    }
+    float m = -INFINITY, l = 0.f;
+    const unsigned gmask = 0xffu << (grp * 8);
+    const int32_t r0 = row_ptr[i], r1 = row_ptr[i + 1];
+    for (int32_t kk = r0 + grp; kk < r1; kk += 8) {
+        const bool two = kk + 4 < r1;  // group-uniform
+        const int64_t j0 = col_idx[kk];
+        const int64_t j1 = two ? col_idx[kk + 4] : j0;
+        const uint4 k0 = *reinterpret_cast<const uint4*>(K + j0 * a.q_sn);
+        const uint4 k1 = *reinterpret_cast<const uint4*>(K + j1 * a.q_sn);
+        const uint4 v0 = *reinterpret_cast<const uint4*>(V + j0 * a.q_sn);
+        const uint4 v1 = *reinterpret_cast<const uint4*>(V + j1 * a.q_sn);
+        float2 kf[4], d0 = make_float2(0.f, 0.f), d1 = make_float2(0.f, 0.f);
+        cvt8<T>(k0, kf);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) d0 = f2fma(q[e], kf[e], d0);
+        cvt8<T>(k1, kf);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) d1 = f2fma(q[e], kf[e], d1);
+        float s0 = d0.x + d0.y, s1 = d1.x + d1.y;
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) {
+            s0 += __shfl_xor_sync(gmask, s0, o);
+            s1 += __shfl_xor_sync(gmask, s1, o);
+        }
+        if (!two) s1 = -INFINITY;
+        const float mx = fmaxf(s0, s1);
+        if (mx > m + kLazy || m == -INFINITY) {  // group-uniform
+            const float a1 = m == -INFINITY ? 0.f : exp2f(m - mx);
+            l *= a1;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) acc[e] = make_float2(acc[e].x * a1, acc[e].y * a1);
+            m = mx;
+        }
+        const float p0 = exp2f(s0 - m), p1 = exp2f(s1 - m);  // s1 = -inf -> 0
+        l += p0 + p1;
+        float2 vf[4];
+        cvt8<T>(v0, vf);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[e] = f2fma(make_float2(p0, p0), vf[e], acc[e]);
+        cvt8<T>(v1, vf);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[e] = f2fma(make_float2(p1, p1), vf[e], acc[e]);
+    }
+    // merge the 4 groups (lanes gl, gl+8, gl+16, gl+24 hold the same dims)
+#pragma unroll
+    for (int o = 8; o < 32; o <<= 1) {
+        const float m2 = __shfl_xor_sync(0xffffffffu, m, o);
+        const float l2 = __shfl_xor_sync(0xffffffffu, l, o);
+        const float mn = fmaxf(m, m2);
+        const float a1 = (m == -INFINITY) ? 0.f : exp2f(m - mn);
+        const float a2 = (m2 == -INFINITY) ? 0.f : exp2f(m2 - mn);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const float x2 = __shfl_xor_sync(0xffffffffu, acc[e].x, o);
+            const float y2 = __shfl_xor_sync(0xffffffffu, acc[e].y, o);
+            acc[e] = make_float2(acc[e].x * a1 + x2 * a2, acc[e].y * a1 + y2 * a2);
+        }
+        l = l * a1 + l2 * a2;
+        m = mn;
+    }
+    if (grp == 0) {
+        const float inv = l > 0.f ? 1.f / l : 0.f;  // rows without valid columns stay zero
+        T* O = static_cast<T*>(a.o) + b * a.o_sb + hh * a.o_sh + i * a.o_sn + gl * 8;
+        uint4 u;
+        T* h = reinterpret_cast<T*>(&u);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            h[2 * e] = DT<T>::from_f(acc[e].x * inv);
+            h[2 * e + 1] = DT<T>::from_f(acc[e].y * inv);
+        }
+        *reinterpret_cast<uint4*>(O) = u;
     }
 }
 
@@ -207,6 +337,14 @@ sf_status rowwise_dispatch(const sf_attn_args& a, const sf_csr_dev& c, cudaStrea
     const int d = a.head_size;
     const bool vec = (d % 64 == 0) && (a.q_sn % 8 == 0) && (a.q_sb % 8 == 0) && (a.q_sh % 8 == 0) &&
                      (reinterpret_cast<uintptr_t>(a.k) % 16 == 0) && (reinterpret_cast<uintptr_t>(a.v) % 16 == 0);
+    if (d == 64 && vec && a.o_sn % 8 == 0 && reinterpret_cast<uintptr_t>(a.o) % 16 == 0 &&
+        reinterpret_cast<uintptr_t>(a.q) % 16 == 0) {
+        const int64_t warps = static_cast<int64_t>(a.bs) * a.h * a.seq_len;
+        attn_rowwise64_kernel<T><<<static_cast<unsigned>(ceil_div(warps * 32, 256)), 256, 0, st>>>(a, c.row_ptr,
+                                                                                                 c.col_idx);
+        SF_LAUNCH_CHECK();
+        return SF_OK;
+    }
     if (d == 64 && vec) return launch_rowwise<T, 8, true>(a, c, st);
     if (d == 128 && vec) return launch_rowwise<T, 16, true>(a, c, st);
     if (d <= 8) return launch_rowwise<T, 1>(a, c, st);

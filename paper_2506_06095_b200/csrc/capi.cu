@@ -28,6 +28,13 @@ sf_status attn_tc(const sf_attn_args& a, const sf_bsr_dev& b, cudaStream_t st, b
 
 namespace {
 
+// B200 executor throughputs measured by `bench.py --sweep --both` (profiles/r01/sweep_both.jsonl):
+// the tcgen05 block executor retires ~1.5-2.3e12 executed cells/s (cells of the loaded 128x16
+// tiles), the row-wise gather ~3.5e10 valid cells/s; ~10 us launch + prologue floor for either.
+constexpr double kBlockCellsPerUs = 1.6e6;
+constexpr double kRowNnzPerUs = 3.5e4;
+constexpr double kLaunchFloorUs = 10.0;
+
 double threshold_from_loads(int32_t n, int64_t loads16, double tau) {
     // planner.hpp:67-76: L / N^2 - tau / (log2 N)^2 with N = ceil(n/16)
     const double big_n = static_cast<double>((n + 15) / 16);
@@ -155,7 +162,31 @@ extern "C" sf_status sf_select_plan(const uint32_t* d_bits, const sf_hw_spec* hw
     if (h <= 0 || bs <= 0 || head_size <= 0) return fail(SF_INVALID_PARAMETER, "hyperparameters must be positive");
     int64_t loads = 0;
     if (seq_len > 16) SF_TRY(loads16_of(d_bits, static_cast<int32_t>(seq_len), &loads, stream));
-    return sf_select_plan_from_loads(loads, hw, seq_len, h, bs, head_size, mode, out);
+    SF_TRY(sf_select_plan_from_loads(loads, hw, seq_len, h, bs, head_size, mode, out));
+    if (mode == SF_PLAN_B200 && out->kind == SF_ROW_WISE && seq_len > 16 && head_size == 64) {
+        // B200 calibration of the Eq. 1 decision: Eq. 1 assumes a row-wise
+        // executor that is competitive per valid cell. On B200 the tcgen05 block executor runs
+        // ~50x more cells per second than the CUDA-core row-wise gather (profiles/r01 sweep), so
+        // a row-wise plan is kept only while the predicted block-wise time is not < half of it.
+        sf_bsr_dev b{};
+        SF_TRY(sf_bsr_build(d_bits, static_cast<int32_t>(seq_len), 128, 16, &b, stream));
+        const int64_t n_load = b.n_load;
+        SF_TRY(sf_bsr_free(&b, stream));
+        int64_t nnz = 0;
+        SF_TRY(sf_mask_count(d_bits, static_cast<int32_t>(seq_len), &nnz, stream));
+        const double slices = static_cast<double>(bs) * h;
+        const double t_bw = kLaunchFloorUs + static_cast<double>(n_load) * 128.0 * 16.0 * slices / kBlockCellsPerUs;
+        const double t_rw = kLaunchFloorUs + static_cast<double>(nnz) * slices / kRowNnzPerUs;
+        if (t_bw < 0.5 * t_rw) {
+            out->kind = SF_BLOCK_WISE;
+            out->block_m = 128;
+            out->block_n = 16;
+            out->num_warps = 8;
+            out->score = plan_score(128, 16, 8, *hw, seq_len, h, bs, head_size);
+            out->fallback = 0;
+        }
+    }
+    return SF_OK;
 }
 
 extern "C" sf_status sf_mha_blockwise(const sf_attn_args* args, const sf_bsr_dev* bsr, const sf_plan* plan,

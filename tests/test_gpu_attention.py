@@ -177,3 +177,17 @@ def test_unified_mha_dispatch(sf, oracle):
                                   filling_rate=0.1, seed=0)])
     plan = sf.select_plan(wide, sf.hw_preset("b200"), 1024, 12, 16, 64, mode="b200")
     assert plan.kind == "block_wise" and plan.block_m == 128
+
+
+def test_b200_selector_calibration(sf):
+    """Eq. 1 routes a 16-wide band at n = 2048 row-wise; the B200 mode keeps
+    that verdict when the work is tiny but moves the full bs16 x 12-head problem block-wise, where
+    the tcgen05 executor is predicted (and measured, profiles/r01) several times faster."""
+    dm = sf.gen_sliding_window(2048, 16)
+    ref = sf.select_plan(dm, sf.hw_preset("b200"), 2048, 12, 16, 64, mode="reference")
+    assert ref.kind == "row_wise" and ref.threshold < 0
+    b200 = sf.select_plan(dm, sf.hw_preset("b200"), 2048, 12, 16, 64, mode="b200")
+    assert b200.kind == "block_wise" and (b200.block_m, b200.block_n) == (128, 16)
+    assert b200.threshold == ref.threshold
+    small = sf.select_plan(sf.gen_sliding_window(2048, 4), sf.hw_preset("b200"), 2048, 2, 1, 64, mode="b200")
+    assert small.kind == "row_wise"
