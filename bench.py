@@ -197,6 +197,7 @@ def work_model(cfg, nnz):
          "ffn1_gemm_gelu": ("tensor", 2.0 * M * F * H), "ffn1_gemm_act": ("tensor", 2.0 * M * F * H),
          "ffn2_gemm_ln": ("tensor", 2.0 * M * H * F), "ffn2_gemm": ("tensor", 2.0 * M * H * F),
          "ln1_mi_chain": ("hbm", 2.0 * M * H * 2),
+         "out_proj_gemm": ("tensor", 2.0 * M * H * H),          "out_proj_ln": ("hbm", 2.0 * M * H * 2), "ffn2_ln": ("hbm", 2.0 * M * H * 2),
          "masked_mha": ("hbm", 4.0 * cfg["bs"] * cfg["heads"] * cfg["seq"] * d * 2)}
     mha_flops = 4.0 * d * cfg["bs"] * cfg["heads"] * nnz
     return w, mha_flops
@@ -342,6 +343,7 @@ def main():
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ln-split", action="store_true", help="residual+LN as a MiChain pass after the GEMM")
     ap.add_argument("--sweep", action="store_true", help="cfg5: masked-MHA pattern x seq_len sweep (JSON lines)")
     ap.add_argument("--patterns", default="", help="--sweep: comma list (default: all six)")
     ap.add_argument("--seqs", default="", help="--sweep: comma list (default: 128..8192)")
@@ -367,7 +369,7 @@ def main():
     plan = sf.select_plan(dm, sf.hw_preset("b200"), s.seq_len, s.heads, s.bs, s.head_size, mode="b200")
     ctx = sf.MhaContext(dm, plan)
     W = layer.init_weights(cfg["model"], s, seed=1 + rank)
-    L = layer.EncoderLayer(cfg["model"], s, W, ctx)
+    L = layer.EncoderLayer(cfg["model"], s, W, ctx, ln_split=args.ln_split)
     g = torch.Generator(device="cuda").manual_seed(7 + rank)
     x = (torch.rand(s.rows, s.hidden, device="cuda", generator=g) * 2 - 1).half()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
@@ -426,7 +428,7 @@ def main():
     hx = torch.empty(s.rows, s.hidden, dtype=torch.float16, pin_memory=True)
     hx.copy_(x.cpu())
     hy = [torch.empty_like(hx, pin_memory=True) for _ in range(2)]
-    Ls = [L, layer.EncoderLayer(cfg["model"], s, W, ctx)]
+    Ls = [L, layer.EncoderLayer(cfg["model"], s, W, ctx, ln_split=args.ln_split)]
     xs = [x, torch.empty_like(x)]
     Ls[1].capture(xs[1])
     s_in, s_comp, s_out = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()

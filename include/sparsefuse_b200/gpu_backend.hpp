@@ -246,11 +246,12 @@ private:
         a.x = x; a.ldx = n.inner;
         a.w = nodes_[static_cast<std::size_t>(node)].w_nk.data(); a.ldw = n.inner;
         a.out = y; a.ldout = n.cols;
-        a.tile_n = (s.tile_n == 128 || s.tile_n == 256) ? s.tile_n : 0;
+        a.tile_n = (s.tile_n == 128 || s.tile_n == 256 || s.tile_n == SF_TILE_PAIR) ? s.tile_n : SF_TILE_AUTO;
         std::size_t used = 0;
         if (!post.empty()) {
             const bool ln = post[0].e.ln_gamma != nullptr;
-            const bool ln_fits = n.cols % 128 == 0 && n.cols <= 2048 && (a.tile_n != 256 || n.cols % 256 == 0);
+            const bool ln_fits = n.cols % 128 == 0 && n.cols <= 2048 && (a.tile_n != 256 || n.cols % 256 == 0) &&
+                                 (a.tile_n != SF_TILE_PAIR || (n.cols % 256 == 0 && n.cols <= 1024 && rows_ > 128));
             if (!ln || ln_fits) {
                 a.epi = post[0].e;
                 used = 1;

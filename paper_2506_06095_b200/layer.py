@@ -70,7 +70,8 @@ class EncoderLayer:
     """One layer of `model` on a fixed (bs, seq_len) with activations resident in HBM."""
 
     def __init__(self, model: str, shape: LayerShape, weights: Dict[str, torch.Tensor], ctx: sf.MhaContext,
-                 compat: bool = False, aux: Optional[Dict[str, torch.Tensor]] = None, dtype=torch.float16):
+                 compat: bool = False, aux: Optional[Dict[str, torch.Tensor]] = None, dtype=torch.float16,
+                 ln_split: bool = False):
         if model not in ("bert-layer", "gpt-layer", "t5-layer"):
             raise sf._lib.InvalidParameter(f"unknown preset model: {model}")  # fusion.hpp:394
         if shape.heads * shape.head_size != shape.hidden:
@@ -78,6 +79,9 @@ class EncoderLayer:
         if ctx.mask.seq_len != shape.seq_len:
             raise sf._lib.ShapeError("MHA mask seq_len mismatch")  # backend.hpp:333
         self.model, self.s, self.W, self.ctx, self.compat = model, shape, weights, ctx, compat
+        # ln_split: residual+LayerNorm as a separate MiChain pass after the GEMM (+bias+residual)
+        # instead of inside the GEMM epilogue (the fusion search's choice at the BASELINE shapes)
+        self.ln_split = ln_split
         self.aux = aux or {}
         self.act = "relu" if model == "t5-layer" else "gelu"
         M, H, F = shape.rows, shape.hidden, shape.ff
@@ -90,6 +94,7 @@ class EncoderLayer:
         self.h2 = e(M, H)
         self.f = e(M, F)
         self.out = e(M, H)
+        self.tmp = e(M, H) if ln_split else None
         self.graph = None
         self.graph_timed = None
         self.marks = []
@@ -117,29 +122,39 @@ class EncoderLayer:
         mark = mark or (lambda name: None)
         if self.model == "bert-layer":
             self._mha(x, stream, mark)
-            fused.gemm_fused(self.attn, W["wo"], self.x1, bias=W["bo"], aux=A.get("add1", x),
-                             ln_gamma=W["ln1_g"], ln_beta=W["ln1_b"], stream=stream)
-            mark("out_proj_gemm_ln")
+            self._gemm_ln(self.attn, "wo", "bo", A.get("add1", x), "ln1", self.x1, None, "out_proj", stream, mark)
             fused.gemm_fused(self.x1, W["w1"], self.f, bias=W["b1"], act="gelu", stream=stream)
             mark("ffn1_gemm_gelu")
-            fused.gemm_fused(self.f, W["w2"], self.out, bias=W["b2"], aux=A.get("add2", self.x1),
-                             ln_gamma=W["ln2_g"], ln_beta=W["ln2_b"], stream=stream)
-            mark("ffn2_gemm_ln")
+            self._gemm_ln(self.f, "w2", "b2", A.get("add2", self.x1), "ln2", self.out, None, "ffn2", stream, mark)
         else:
             fused.mi_chain(x, self.h, ln_gamma=W["ln1_g"], ln_beta=W["ln1_b"], stream=stream)
             mark("ln1_mi_chain")
             self._mha(self.h, stream, mark)
-            fused.gemm_fused(self.attn, W["wo"], self.h2, bias=W["bo"], aux=A.get("add1", x),
-                             ln_gamma=W["ln2_g"], ln_beta=W["ln2_b"], out_pre_ln=self.x1, stream=stream)
-            mark("out_proj_gemm_ln")
+            self._gemm_ln(self.attn, "wo", "bo", A.get("add1", x), "ln2", self.h2, self.x1, "out_proj", stream, mark)
             fused.gemm_fused(self.h2, W["w1"], self.f, bias=W["b1"], act=self.act, stream=stream)
             mark("ffn1_gemm_act")
             fused.gemm_fused(self.f, W["w2"], self.out, bias=W["b2"], aux=A.get("add2", self.x1), stream=stream)
             mark("ffn2_gemm")
         return self.out
 
+    def _gemm_ln(self, x, w, b, aux, ln, out, pre, name, stream, mark):
+        """out = LN(x @ W^T + bias + aux) (pre, if given, receives the pre-LN sum): fused into the
+        GEMM epilogue (cluster LayerNorm), or GEMM(+bias+aux) followed by a MiChain LN pass."""
+        W = self.W
+        if not self.ln_split:
+            fused.gemm_fused(x, W[w], out, bias=W[b], aux=aux, ln_gamma=W[ln + "_g"], ln_beta=W[ln + "_b"],
+                             out_pre_ln=pre, stream=stream)
+            mark(name + "_gemm_ln")
+            return
+        mid = pre if pre is not None else self.tmp
+        fused.gemm_fused(x, W[w], mid, bias=W[b], aux=aux, stream=stream)
+        mark(name + "_gemm")
+        fused.mi_chain(mid, out, ln_gamma=W[ln + "_g"], ln_beta=W[ln + "_b"], stream=stream)
+        mark(name + "_ln")
+
     def kernels_per_step(self) -> int:
         n = 4 if self.model == "bert-layer" else 5
+        n += (2 if self.model == "bert-layer" else 1) if self.ln_split else 0
         return n + (0 if self.compat else 1)
 
     # CUDA graph of one step (launch-bound small configs). timed=True adds an event-record node

@@ -21,7 +21,7 @@ def parity(out, ref, max_abs=2e-2, mean_rel=1e-3):
     return ma, mr
 
 
-def build(sf, layer, o, model, bs, seq, hid, heads, terms, compat):
+def build(sf, layer, o, model, bs, seq, hid, heads, terms, compat, ln_split=False):
     import torch
     hs = hid // heads
     gd = graph_data(o, model, bs, seq, hid, 4 * hid, 1)
@@ -60,18 +60,19 @@ def build(sf, layer, o, model, bs, seq, hid, heads, terms, compat):
     plan = sf.select_plan(dm, sf.hw_preset("b200"), seq, heads, bs, hs, mode="b200")
     ctx = sf.MhaContext(dm, plan)
     shape = layer.LayerShape(bs, seq, hid, heads, hs)
-    L = layer.EncoderLayer(model, shape, W, ctx, compat=compat, aux=aux)
+    L = layer.EncoderLayer(model, shape, W, ctx, compat=compat, aux=aux, ln_split=ln_split)
     ref = run_chain(o, model, gd, x, o.mask(terms), bs, seq, heads, hs, 16, 16, threads=8, qkv=qkv)
     return L, dev(x), ref
 
 
 @pytest.mark.parametrize("model", ["bert-layer", "gpt-layer", "t5-layer"])
 @pytest.mark.parametrize("compat", [True, False])
-def test_layer_matches_chain_oracle(sf, oracle, model, compat):
+@pytest.mark.parametrize("ln_split", [False, True])
+def test_layer_matches_chain_oracle(sf, oracle, model, compat, ln_split):
     from paper_2506_06095_b200 import layer
     bs, seq, hid, heads = 2, 256, 256, 4
     terms = [dict(pattern="bigbird", seq_len=seq, global_width=16, band_width=16, filling_rate=0.1, seed=0)]
-    L, x, ref = build(sf, layer, oracle, model, bs, seq, hid, heads, terms, compat)
+    L, x, ref = build(sf, layer, oracle, model, bs, seq, hid, heads, terms, compat, ln_split)
     parity(L.forward(x), ref)
 
 
