@@ -266,6 +266,11 @@ typedef struct sf_gemm_args {
                                 256 x 256 tiles, tcgen05 cta_group::2) */
 } sf_gemm_args;
 
+/* Programmatic dependent launch for the hot-path kernels (default on; env SF_PDL=0 disables):
+ * each kernel is scheduled while its stream predecessor drains and waits for it on device
+ * (griddepcontrol) before touching global data. Not part of the reference API. */
+sf_status sf_set_pdl(int32_t on);
+
 /* CiMi template (backend.hpp:240-264): tcgen05 GEMM + fused epilogue. */
 sf_status sf_gemm_fused(const sf_gemm_args* args, void* stream);
 

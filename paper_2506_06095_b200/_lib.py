@@ -119,6 +119,7 @@ SIGNATURES = {
     "sf_mha_blockwise": (C.c_int, [C.POINTER(AttnArgs), C.POINTER(BsrDev), C.POINTER(Plan), C.POINTER(AttnStats), _P]),
     "sf_mha_rowwise": (C.c_int, [C.POINTER(AttnArgs), C.POINTER(CsrDev), _P]),
     "sf_set_attn_impl": (C.c_int, [_I32]),
+    "sf_set_pdl": (C.c_int, [_I32]),
     "sf_get_attn_impl": (_I32, []),
     "sf_gemm_fused": (C.c_int, [C.POINTER(GemmArgs), _P]),
     "sf_mi_chain": (C.c_int, [_I32, _I32, _I32, _P, _I64, C.POINTER(GemmEpilogue), _P, _I64, _P]),

@@ -217,6 +217,7 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
                                               // unambiguous only within one phase of lag)
     uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(o_full + 2);
 
+    pdl_enter();
     const uint32_t warp = tc::warp_id();
     const uint32_t lane = threadIdx.x & 31;
 
@@ -605,7 +606,7 @@ sf_status attn_tc(const sf_attn_args& a, const sf_bsr_dev& b, cudaStream_t st, b
     }
     // persistent: two CTAs per SM (smem and TMEM are sized for it), items round-robin
     dim3 grid(static_cast<unsigned>(std::min<int64_t>(p.n_items, 2 * n_sm)));
-    kern<<<grid, kThreads, kSmem, st>>>(p);
+    SF_CUDA_TRY(launch_pdl(kern, grid, dim3(kThreads), kSmem, st, nullptr, p));
     SF_LAUNCH_CHECK();
     return SF_OK;
 }

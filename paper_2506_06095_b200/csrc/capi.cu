@@ -1,6 +1,7 @@
 // capi.cu — host side of the C ABI: error state, launch accounting, the analytical selector
 // (planner.hpp:20-161, exact doubles, host C++), attention dispatch and the CUDA-event timing
 // hook behind the MeasurementBackend contract (backend.hpp:391-402, 488-500).
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -69,6 +70,24 @@ double plan_score(int bm, int bn, int w, const sf_hw_spec& hw, int64_t seq, int 
 using namespace sf;
 
 extern "C" const char* sf_last_error(void) { return g_last_error.c_str(); }
+namespace sf {
+static std::atomic<int> g_pdl{-1};
+bool pdl_enabled() {
+    int v = g_pdl.load();
+    if (v < 0) {
+        const char* e = std::getenv("SF_PDL");
+        v = (e && e[0] == '0') ? 0 : 1;
+        g_pdl.store(v);
+    }
+    return v != 0;
+}
+}  // namespace sf
+
+extern "C" sf_status sf_set_pdl(int32_t on) {
+    sf::g_pdl.store(on ? 1 : 0);
+    return SF_OK;
+}
+
 extern "C" const char* sf_version(void) { return "sparsefuse-b200 0.1 sm_100a"; }
 extern "C" int64_t sf_launch_count(void) { return g_launches.load(); }
 

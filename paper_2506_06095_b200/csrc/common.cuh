@@ -9,6 +9,7 @@
 #include <stdint.h>
 
 #include <atomic>
+#include <utility>
 #include <string>
 
 #include "../../include/sf_capi.h"
@@ -20,6 +21,35 @@ void set_error(const std::string& msg);
 sf_status fail(sf_status st, const std::string& msg);
 // Host-side launch counter (sf_launch_count): every kernel launch goes through note_launch().
 void note_launch(int64_t n = 1);
+
+// Programmatic dependent launch (PDL). The hot-path kernels are launched with programmatic stream
+// serialization, so a kernel's grid is scheduled while its predecessor drains; each of them
+// starts with pdl_enter(): wait for the predecessor grid (complete, memory visible) before
+// touching any global data, then allow its own dependents to be scheduled. A kernel launched
+// without the attribute passes both instantly. sf_set_pdl(0) turns the attribute off.
+bool pdl_enabled();
+__device__ __forceinline__ void pdl_enter() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+// cudaLaunchKernelEx with the PDL attribute (plus up to one extra attribute, e.g. a cluster shape)
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       const cudaLaunchAttribute* extra, Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    int n = 1;
+    if (extra) attr[n++] = *extra;
+    cfg.attrs = attr;
+    cfg.numAttrs = n;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 

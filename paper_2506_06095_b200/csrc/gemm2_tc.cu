@@ -76,6 +76,7 @@ __global__ void __launch_bounds__(Cfg2<LN>::THREADS, 1) gemm2_kernel(const __gri
     uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(abar + C::EPI_WARPS);
     float* red = reinterpret_cast<float*>(smem + C::STAGES * (C::A_BYTES + C::B_BYTES) + C::STG_BYTES + C::BAR_BYTES);
 
+    pdl_enter();
     const uint32_t warp = tc::warp_id();
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t rank = tc::cluster_rank();
@@ -442,19 +443,12 @@ sf_status launch_pair(const sf_gemm_args& a, cudaStream_t st) {
     SF_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     const int units = LN ? mp_tiles : mp_tiles * n_tiles;  // work items of one cluster
     const int clusters = std::max(1, std::min(units, max_clusters<T, LN>(nct)));
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(2, nct * clusters);
-    cfg.blockDim = dim3(Cf::THREADS);
-    cfg.dynamicSmemBytes = Cf::SMEM;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
-    attr[0].val.clusterDim.y = static_cast<unsigned>(nct);
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    SF_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, p));
+    cudaLaunchAttribute cl;
+    cl.id = cudaLaunchAttributeClusterDimension;
+    cl.val.clusterDim.x = 2;
+    cl.val.clusterDim.y = static_cast<unsigned>(nct);
+    cl.val.clusterDim.z = 1;
+    SF_CUDA_TRY(launch_pdl(kern, dim3(2, nct * clusters), dim3(Cf::THREADS), Cf::SMEM, st, &cl, p));
     SF_LAUNCH_CHECK();
     return SF_OK;
 }

@@ -40,6 +40,7 @@ struct Cfg {
 template <typename T, int BN, bool LN>
 __global__ void __launch_bounds__(Cfg<BN, LN>::THREADS, 1) gemm_fused_kernel(const __grid_constant__ GemmParams p) {
     using C = Cfg<BN, LN>;
+    pdl_enter();
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     unsigned char* sA = smem;
@@ -308,7 +309,7 @@ sf_status launch_gemm(const sf_gemm_args& a, cudaStream_t st) {
     cfg.blockDim = dim3(Cf::THREADS);
     cfg.dynamicSmemBytes = Cf::SMEM;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     if (LN) {
         const int nct = n_tiles;  // whole row per cluster
         const int clusters = std::max(1, std::min(m_tiles, num_sms() / nct));
@@ -331,6 +332,12 @@ sf_status launch_gemm(const sf_gemm_args& a, cudaStream_t st) {
             cfg.numAttrs = 1;
         }
     }
+    cudaLaunchAttribute pdl;
+    pdl.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    pdl.val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    attr[cfg.numAttrs] = pdl;
+    cfg.numAttrs += 1;
+    cfg.attrs = attr;
     SF_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, p));
     SF_LAUNCH_CHECK();
     return SF_OK;

@@ -51,6 +51,7 @@ template <typename T, int V, int W>
 __global__ void __launch_bounds__(kWarpsPerCta * 32) mi_chain_kernel(int32_t M, int32_t N, const T* __restrict__ x,
                                                                      int64_t ldx, sf_gemm_epilogue e,
                                                                      T* __restrict__ out, int64_t ldout) {
+    pdl_enter();
     const int64_t row = static_cast<int64_t>(blockIdx.x) * kWarpsPerCta + (threadIdx.x >> 5);
     if (row >= M) return;
     const int lane = threadIdx.x & 31;
@@ -128,6 +129,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, V >= 4 ? 2 : 3) mi_chain_ro
                                                                           const T* __restrict__ x, int64_t ldx,
                                                                           sf_gemm_epilogue e, T* __restrict__ out,
                                                                           int64_t ldout) {
+    pdl_enter();
     __shared__ float4 sprm[3][2 * V * 32];  // bias, gamma, beta
     const int lane = threadIdx.x & 31;
     const T* aux = static_cast<const T*>(e.aux);
@@ -231,7 +233,8 @@ void launch_rows_act(int32_t M, int32_t N, const T* x, int64_t ldx, const sf_gem
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int64_t need = ceil_div(M, kWarpsPerCta);
     const unsigned grid = static_cast<unsigned>(std::min<int64_t>(need, static_cast<int64_t>(sms) * per_sm));
-    mi_chain_rows_kernel<T, V, ACT><<<grid, kWarpsPerCta * 32, 0, st>>>(M, N, x, ldx, e, out, ldout);
+    (void)launch_pdl(mi_chain_rows_kernel<T, V, ACT>, grid, dim3(kWarpsPerCta * 32), 0, st, nullptr, M, N, x, ldx, e, out,
+                     ldout);  // errors surface in the caller's SF_LAUNCH_CHECK
 }
 
 template <typename T, int V>
@@ -247,6 +250,7 @@ void launch_rows(int32_t M, int32_t N, const T* x, int64_t ldx, const sf_gemm_ep
 template <typename T, int ACT>
 __global__ void __launch_bounds__(256) mi_chain_ew_kernel(int32_t M, int32_t N, const T* __restrict__ x, int64_t ldx,
                                                           sf_gemm_epilogue e, T* __restrict__ out, int64_t ldout) {
+    pdl_enter();
     const int64_t vpr = N / 8;  // vectors per row
     const int64_t total = static_cast<int64_t>(M) * vpr;
     const float* bias = static_cast<const float*>(e.bias);
@@ -286,9 +290,9 @@ void launch_ew(int32_t M, int32_t N, const T* x, int64_t ldx, const sf_gemm_epil
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int64_t total = static_cast<int64_t>(M) * (N / 8);
     const unsigned grid = static_cast<unsigned>(std::min<int64_t>(ceil_div(total, 256), static_cast<int64_t>(sms) * 8));
-    if (e.act == SF_ACT_GELU) mi_chain_ew_kernel<T, SF_ACT_GELU><<<grid, 256, 0, st>>>(M, N, x, ldx, e, out, ldout);
-    else if (e.act == SF_ACT_RELU) mi_chain_ew_kernel<T, SF_ACT_RELU><<<grid, 256, 0, st>>>(M, N, x, ldx, e, out, ldout);
-    else mi_chain_ew_kernel<T, SF_ACT_NONE><<<grid, 256, 0, st>>>(M, N, x, ldx, e, out, ldout);
+    if (e.act == SF_ACT_GELU) (void)launch_pdl(mi_chain_ew_kernel<T, SF_ACT_GELU>, grid, dim3(256), 0, st, nullptr, M, N, x, ldx, e, out, ldout);
+    else if (e.act == SF_ACT_RELU) (void)launch_pdl(mi_chain_ew_kernel<T, SF_ACT_RELU>, grid, dim3(256), 0, st, nullptr, M, N, x, ldx, e, out, ldout);
+    else (void)launch_pdl(mi_chain_ew_kernel<T, SF_ACT_NONE>, grid, dim3(256), 0, st, nullptr, M, N, x, ldx, e, out, ldout);
 }
 
 template <typename T, int W>
@@ -314,15 +318,15 @@ sf_status launch(int32_t M, int32_t N, const void* x, int64_t ldx, const sf_gemm
             return SF_OK;
         }
     }
-    if (chunks <= 1) mi_chain_kernel<T, 1, W><<<grid, kWarpsPerCta * 32, 0, st>>>(M, N, xp, ldx, e, op, ldout);
-    else if (chunks <= 2) mi_chain_kernel<T, 2, W><<<grid, kWarpsPerCta * 32, 0, st>>>(M, N, xp, ldx, e, op, ldout);
-    else if (chunks <= 4) mi_chain_kernel<T, 4, W><<<grid, kWarpsPerCta * 32, 0, st>>>(M, N, xp, ldx, e, op, ldout);
-    else if (chunks <= 8) mi_chain_kernel<T, 8, W><<<grid, kWarpsPerCta * 32, 0, st>>>(M, N, xp, ldx, e, op, ldout);
-    else if (chunks <= 16) mi_chain_kernel<T, 16, W><<<grid, kWarpsPerCta * 32, 0, st>>>(M, N, xp, ldx, e, op, ldout);
+    if (chunks <= 1) SF_CUDA_TRY(launch_pdl(mi_chain_kernel<T, 1, W>, grid, dim3(kWarpsPerCta * 32), 0, st, nullptr, M, N, xp, ldx, e, op, ldout));
+    else if (chunks <= 2) SF_CUDA_TRY(launch_pdl(mi_chain_kernel<T, 2, W>, grid, dim3(kWarpsPerCta * 32), 0, st, nullptr, M, N, xp, ldx, e, op, ldout));
+    else if (chunks <= 4) SF_CUDA_TRY(launch_pdl(mi_chain_kernel<T, 4, W>, grid, dim3(kWarpsPerCta * 32), 0, st, nullptr, M, N, xp, ldx, e, op, ldout));
+    else if (chunks <= 8) SF_CUDA_TRY(launch_pdl(mi_chain_kernel<T, 8, W>, grid, dim3(kWarpsPerCta * 32), 0, st, nullptr, M, N, xp, ldx, e, op, ldout));
+    else if (chunks <= 16) SF_CUDA_TRY(launch_pdl(mi_chain_kernel<T, 16, W>, grid, dim3(kWarpsPerCta * 32), 0, st, nullptr, M, N, xp, ldx, e, op, ldout));
     else if constexpr (kMax > 16) {
-        if (chunks <= 32) mi_chain_kernel<T, 32, W><<<grid, kWarpsPerCta * 32, 0, st>>>(M, N, xp, ldx, e, op, ldout);
-        else if (chunks <= 64) mi_chain_kernel<T, 64, W><<<grid, kWarpsPerCta * 32, 0, st>>>(M, N, xp, ldx, e, op, ldout);
-        else mi_chain_kernel<T, 128, W><<<grid, kWarpsPerCta * 32, 0, st>>>(M, N, xp, ldx, e, op, ldout);
+        if (chunks <= 32) SF_CUDA_TRY(launch_pdl(mi_chain_kernel<T, 32, W>, grid, dim3(kWarpsPerCta * 32), 0, st, nullptr, M, N, xp, ldx, e, op, ldout));
+        else if (chunks <= 64) SF_CUDA_TRY(launch_pdl(mi_chain_kernel<T, 64, W>, grid, dim3(kWarpsPerCta * 32), 0, st, nullptr, M, N, xp, ldx, e, op, ldout));
+        else SF_CUDA_TRY(launch_pdl(mi_chain_kernel<T, 128, W>, grid, dim3(kWarpsPerCta * 32), 0, st, nullptr, M, N, xp, ldx, e, op, ldout));
     }
     SF_LAUNCH_CHECK();
     return SF_OK;
