@@ -154,18 +154,25 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* m, uin
         : "memory");
 }
 
-// The CTA's work items, in the order every role walks them. Item idx = blockIdx.x + k*gridDim.x
-// over (row-block rank, b*h) with row blocks ranked by descending load count, so the static
-// round robin hands the longest items out first (a cheap LPT schedule).
+// The CTA's work items, in the order every role walks them. Items (row-block rank, b*h) are
+// numbered with row blocks ranked by descending load count and dealt to the CTAs in snake order
+// (round k goes c = 0..G-1 when k is even, G-1..0 when odd), so the longest items go out first
+// and each CTA's total is balanced (an LPT-style static schedule; no atomics, graph-replayable).
 struct Items {
     const int32_t* lrp;
     const int32_t* order;  // smem: row block of each rank
     int bh_count, n_items, G;
+    __device__ __forceinline__ int pos(int k) const {
+        const int c = static_cast<int>(blockIdx.x), g = static_cast<int>(gridDim.x);
+        return (k & 1) ? g - 1 - c : c;
+    }
     __device__ __forceinline__ int count() const {
-        return blockIdx.x < n_items ? (n_items - 1 - static_cast<int>(blockIdx.x)) / static_cast<int>(gridDim.x) + 1 : 0;
+        const int g = static_cast<int>(gridDim.x);
+        const int full = n_items / g, rem = n_items % g;
+        return full + (rem > 0 && pos(full) < rem ? 1 : 0);
     }
     __device__ __forceinline__ void get(int k, int& rb, int& bh, int& l0, int& L, int& nsteps) const {
-        const int idx = static_cast<int>(blockIdx.x) + k * static_cast<int>(gridDim.x);
+        const int idx = k * static_cast<int>(gridDim.x) + pos(k);
         rb = order[idx / bh_count];
         bh = idx % bh_count;
         l0 = lrp[rb];
