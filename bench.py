@@ -335,6 +335,68 @@ def run_sweep(args):
         torch.cuda.empty_cache()
 
 
+# ----------------------------------------------------------------------------------------------
+# format builders (A1-A4, A9): device latency vs the reference's own builders on the host
+def run_formats(args):
+    """Device latency (CUDA events around the C-ABI call, warm, median of --steps) of mask
+    generation, build_bsr at the reference's 16x16 and the B200 plan's (128,16), build_rowwise
+    and select_plan, for every BASELINE mask and n = 8192 masks; the reference's generate_mask /
+    build_bsr / build_rowwise (oracle/_ref) timed on one host core beside them. These builders
+    are latency-bound: the metric is microseconds, the roofline is not the point."""
+    import torch
+    from paper_2506_06095_b200 import sparsefuse as sf
+    torch.cuda.set_device(0)
+    ref = None
+    if not args.no_cpu_baseline:
+        from oracle.oracle import Reference
+        ref = Reference()
+        if not ref.available:
+            ref = None
+    masks = [(name, cfg["mask"]) for name, cfg in sorted(CONFIGS.items())]
+    masks += [(f"{pat}-8192", sweep_terms(pat, 8192)) for pat in ("sliding", "bigbird", "causal")]
+
+    def dev_us(fn):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(args.steps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(); fn(); b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b) * 1e3)
+        return statistics.median(ts)
+
+    def host_ms(fn, reps=3):
+        best = 1e30
+        for _ in range(reps):
+            t0 = time.perf_counter(); fn(); best = min(best, time.perf_counter() - t0)
+        return best * 1e3
+
+    for name, terms in masks:
+        dm = sf.generate_mask(terms)
+        n = dm.seq_len
+        line = {"formats": name, "seq_len": n, "nnz": dm.true_count(),
+                "device_us": {"generate_mask": dev_us(lambda: sf.generate_mask(terms)),
+                              "build_bsr_16x16": dev_us(lambda: sf.build_bsr(dm, 16, 16)),
+                              "build_bsr_128x16": dev_us(lambda: sf.build_bsr(dm, 128, 16)),
+                              "build_rowwise": dev_us(lambda: sf.build_rowwise(dm)),
+                              "select_plan_b200": dev_us(lambda: sf.select_plan(dm, sf.hw_preset("b200"), n, 12, 16,
+                                                                                 64, mode="b200"))},
+                "timing": f"CUDA events around the call incl. its host sync (sizes), warm, median of {args.steps}"}
+        if ref is not None:
+            m = dm.to_numpy()  # the same mask bytes (strided/causal are generators the reference lacks)
+            r = {"build_bsr_16x16": host_ms(lambda: ref.sfbr(m, 16, 16)),
+                 "build_rowwise": host_ms(lambda: ref.rowwise(m))}
+            try:
+                r["generate_mask"] = host_ms(lambda: ref.mask(terms))
+            except ValueError:
+                pass
+            line["reference_ms_1core"] = r
+            line["reference_note"] = "build_bsr timed through write_bsr serialisation (SFBR bytes), one host core"
+        print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -348,9 +410,12 @@ def main():
     ap.add_argument("--patterns", default="", help="--sweep: comma list (default: all six)")
     ap.add_argument("--seqs", default="", help="--sweep: comma list (default: 128..8192)")
     ap.add_argument("--both", action="store_true", help="--sweep: also time the executor the plan did not pick")
+    ap.add_argument("--formats", action="store_true", help="format-builder latency (A1-A4, A9) vs the reference")
     args = ap.parse_args()
     if args.sweep:
         return run_sweep(args)
+    if args.formats:
+        return run_formats(args)
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         return run_reference_arm(args, cfg)

@@ -83,6 +83,22 @@ bool pdl_enabled() {
 }
 }  // namespace sf
 
+namespace sf {
+cudaError_t pool_malloc(void** p, size_t bytes, cudaStream_t st) {
+    static std::atomic<int> ready{0};
+    if (!ready.load()) {
+        int dev = 0;
+        cudaMemPool_t pool;
+        if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t keep = ~0ull;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+        ready.store(1);
+    }
+    return cudaMallocAsync(p, bytes, st);
+}
+}  // namespace sf
+
 extern "C" sf_status sf_set_pdl(int32_t on) {
     sf::g_pdl.store(on ? 1 : 0);
     return SF_OK;

@@ -28,6 +28,12 @@ void note_launch(int64_t n = 1);
 // touching any global data, then allow its own dependents to be scheduled. A kernel launched
 // without the attribute passes both instantly. sf_set_pdl(0) turns the attribute off.
 bool pdl_enabled();
+
+// Stream-ordered allocation for the format builders' scratch and outputs. The device's default
+// memory pool is set (once) to keep freed blocks instead of returning them to the driver at every
+// synchronisation (release threshold 0 by default), so repeated builds reuse memory and a build's
+// latency is its kernels and its one size read-back, not driver allocations.
+cudaError_t pool_malloc(void** p, size_t bytes, cudaStream_t st);
 __device__ __forceinline__ void pdl_enter() {
     asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");

@@ -157,39 +157,51 @@ __global__ void compact_kernel(const uint8_t* __restrict__ cls, Geo g,
     }
 }
 
-__device__ bool tiles_equal(const uint32_t* __restrict__ bits, const Geo& g, int64_t ta, int64_t tb) {
+// Tile equality, one full warp: lanes take rows di = lane, lane+32, ... (independent loads, one
+// ballot) instead of one thread walking all block_m rows serially.
+__device__ __forceinline__ bool tiles_equal_warp(const uint32_t* __restrict__ bits, const Geo& g, int64_t ta,
+                                                 int64_t tb) {
+    const int lane = threadIdx.x & 31;
     const int64_t ar = ta / g.n_cols, ac = ta - ar * g.n_cols;
     const int64_t br_ = tb / g.n_cols, bc_ = tb - br_ * g.n_cols;
-    for (int di = 0; di < g.bm; ++di) {
+    bool diff = false;
+    for (int di = lane; di < g.bm; di += 32) {
         const int64_t ia = ar * g.bm + di, ib = br_ * g.bm + di;
         for (int64_t c = 0; c * 64 < g.bn; ++c) {
             const int64_t ja = ac * g.bn + 64 * c, jb = bc_ * g.bn + 64 * c;
             const uint64_t va = ia < g.n ? row_bits64(bits + ia * g.words, ja, imin64(g.n, ac * g.bn + g.bn)) : 0ull;
             const uint64_t vb = ib < g.n ? row_bits64(bits + ib * g.words, jb, imin64(g.n, bc_ * g.bn + g.bn)) : 0ull;
-            if (va != vb) return false;
+            diff |= va != vb;
         }
     }
-    return true;
+    return __ballot_sync(0xffffffffu, diff) == 0u;
 }
 
+// Intern part tiles by content: one warp per part tile; lane 0 probes the open-addressing table,
+// the warp compares contents on a hash match. Each slot ends holding the smallest row-major tile
+// id of its content class (atomicMin), which fixes the pool order to first occurrence
+// (bsr.hpp:83-91).
 __global__ void dedup_insert_kernel(const uint32_t* __restrict__ bits, Geo g, int32_t n_part,
                                     const int32_t* __restrict__ part_lin, const uint64_t* __restrict__ hash,
                                     int32_t* table, uint32_t cap_mask, int32_t* part_slot) {
-    const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t k = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     if (k >= n_part) return;
+    const int lane = threadIdx.x & 31;
     const int32_t lin = part_lin[k];
     const uint64_t h = hash[lin];
     uint32_t s = static_cast<uint32_t>(h ^ (h >> 32)) & cap_mask;
     for (;;) {
-        int32_t cur = atomicCAS(&table[s], -1, lin);
+        int32_t cur = 0;
+        if (lane == 0) cur = atomicCAS(&table[s], -1, lin);
+        cur = __shfl_sync(0xffffffffu, cur, 0);
         if (cur == -1) break;  // claimed an empty slot
-        if (hash[cur] == h && tiles_equal(bits, g, cur, lin)) {
-            atomicMin(&table[s], lin);
+        if (hash[cur] == h && tiles_equal_warp(bits, g, cur, lin)) {
+            if (lane == 0) atomicMin(&table[s], lin);
             break;
         }
         s = (s + 1) & cap_mask;
     }
-    part_slot[k] = static_cast<int32_t>(s);
+    if (lane == 0) part_slot[k] = static_cast<int32_t>(s);
 }
 
 __global__ void first_flag_kernel(int32_t n_part, const int32_t* __restrict__ part_lin,
@@ -319,7 +331,7 @@ extern "C" sf_status sf_bsr_build(const uint32_t* d_bits, int32_t seq_len, int32
     char* s1 = nullptr;
     const int64_t s1_bytes = ceil_div(tiles, 256) * 256 + ceil_div(tiles * 8, 256) * 256 +
                              6 * (ceil_div((g.n_rows + 1) * 4, 256) * 256) + 256;
-    SF_CUDA_TRY(cudaMallocAsync(&s1, s1_bytes, st));
+    SF_CUDA_TRY(pool_malloc(reinterpret_cast<void**>(&s1), s1_bytes, st));
     char* p = s1;
     uint8_t* cls = carve<uint8_t>(p, tiles);
     uint64_t* hash = carve<uint64_t>(p, tiles);
@@ -351,7 +363,7 @@ extern "C" sf_status sf_bsr_build(const uint32_t* d_bits, int32_t seq_len, int32
                               2 * ceil_div(std::max(1, n_load) * 4ll, 256) * 256 +
                               ceil_div(imax64(1, static_cast<int64_t>(n_part) * tile_bytes), 256) * 256;
     char* ob = nullptr;
-    SF_CUDA_TRY(cudaMallocAsync(&ob, out_bytes, st));
+    SF_CUDA_TRY(pool_malloc(reinterpret_cast<void**>(&ob), out_bytes, st));
     p = ob;
     out->full_row_ptr = carve<int32_t>(p, rp);
     out->part_row_ptr = carve<int32_t>(p, rp);
@@ -374,7 +386,7 @@ extern "C" sf_status sf_bsr_build(const uint32_t* d_bits, int32_t seq_len, int32
     const int64_t np1 = std::max(1, n_part);
     const int64_t s2_bytes = 5 * ceil_div((np1 + 1) * 4, 256) * 256 + 2 * ceil_div(cap * 4ll, 256) * 256 +
                              ceil_div(std::max(1, n_load) * 4ll, 256) * 256;
-    SF_CUDA_TRY(cudaMallocAsync(&s2, s2_bytes, st));
+    SF_CUDA_TRY(pool_malloc(reinterpret_cast<void**>(&s2), s2_bytes, st));
     p = s2;
     int32_t* part_lin = carve<int32_t>(p, np1);
     int32_t* part_slot = carve<int32_t>(p, np1);
@@ -393,8 +405,8 @@ extern "C" sf_status sf_bsr_build(const uint32_t* d_bits, int32_t seq_len, int32
     }
     int32_t n_pool = 0;
     if (n_part > 0) {
-        dedup_insert_kernel<<<blocks_for(n_part), 256, 0, st>>>(d_bits, g, n_part, part_lin, hash, table,
-                                                                cap - 1, part_slot);
+        dedup_insert_kernel<<<blocks_for(static_cast<int64_t>(n_part) * 32), 256, 0, st>>>(
+            d_bits, g, n_part, part_lin, hash, table, cap - 1, part_slot);
         SF_LAUNCH_CHECK();
         first_flag_kernel<<<blocks_for(n_part), 256, 0, st>>>(n_part, part_lin, table, part_slot, first);
         SF_LAUNCH_CHECK();
@@ -493,19 +505,19 @@ extern "C" sf_status sf_rowwise_build(const uint32_t* d_bits, int32_t seq_len, s
     cudaStream_t st = as_stream(stream);
     const int32_t words = sf_mask_words(seq_len);
     int32_t* cnt = nullptr;
-    SF_CUDA_TRY(cudaMallocAsync(&cnt, (seq_len + 1) * 4ll + 256, st));
+    SF_CUDA_TRY(pool_malloc(reinterpret_cast<void**>(&cnt), (seq_len + 1) * 4ll + 256, st));
     int32_t* total = cnt + seq_len;
     char* blk = nullptr;
     row_popc_kernel<<<blocks_for(static_cast<int64_t>(seq_len) * 32), 256, 0, st>>>(d_bits, seq_len, words, cnt);
     SF_LAUNCH_CHECK();
     int32_t* rp_tmp = nullptr;
-    SF_CUDA_TRY(cudaMallocAsync(&rp_tmp, (seq_len + 1) * 4ll, st));
+    SF_CUDA_TRY(pool_malloc(reinterpret_cast<void**>(&rp_tmp), (seq_len + 1) * 4ll, st));
     SF_TRY(scan_exclusive(cnt, rp_tmp, seq_len, total, st));
     int32_t nnz = 0;
     SF_CUDA_TRY(cudaMemcpyAsync(&nnz, total, 4, cudaMemcpyDeviceToHost, st));
     SF_CUDA_TRY(cudaStreamSynchronize(st));
     const int64_t rp_bytes = ceil_div((seq_len + 1) * 4ll, 256) * 256;
-    SF_CUDA_TRY(cudaMallocAsync(&blk, rp_bytes + imax64(4, nnz * 4ll), st));
+    SF_CUDA_TRY(pool_malloc(reinterpret_cast<void**>(&blk), rp_bytes + imax64(4, nnz * 4ll), st));
     out->row_ptr = reinterpret_cast<int32_t*>(blk);
     out->col_idx = reinterpret_cast<int32_t*>(blk + rp_bytes);
     SF_CUDA_TRY(cudaMemcpyAsync(out->row_ptr, rp_tmp, (seq_len + 1) * 4ll, cudaMemcpyDeviceToDevice, st));

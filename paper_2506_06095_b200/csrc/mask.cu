@@ -220,7 +220,7 @@ extern "C" sf_status sf_mask_generate(const sf_mask_desc* terms, int32_t n_terms
         if (d.pattern == SF_PATTERN_RANDOM || d.pattern == SF_PATTERN_BIGBIRD) {
             const int64_t draws = static_cast<int64_t>(e.rgrid) * e.rgrid;
             uint32_t* rt = nullptr;
-            SF_CUDA_TRY(cudaMallocAsync(&rt, ceil_div(draws, 32) * 4, st));
+            SF_CUDA_TRY(pool_malloc(reinterpret_cast<void**>(&rt), ceil_div(draws, 32) * 4, st));
             SF_CUDA_TRY(cudaMemsetAsync(rt, 0, ceil_div(draws, 32) * 4, st));
             random_tiles_kernel<<<1, kMtN, 0, st>>>(d.seed, draws, d.filling_rate, rt);
             SF_LAUNCH_CHECK();
@@ -267,7 +267,7 @@ extern "C" sf_status sf_mask_count(const uint32_t* d_bits, int32_t seq_len, int6
                                    void* stream) {
     cudaStream_t st = as_stream(stream);
     unsigned long long* d = nullptr;
-    SF_CUDA_TRY(cudaMallocAsync(&d, 8, st));
+    SF_CUDA_TRY(pool_malloc(reinterpret_cast<void**>(&d), 8, st));
     SF_CUDA_TRY(cudaMemsetAsync(d, 0, 8, st));
     const int64_t total = static_cast<int64_t>(seq_len) * sf_mask_words(seq_len);
     popcount_kernel<<<296, 256, 0, st>>>(d_bits, total, d);
