@@ -53,7 +53,19 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t cta)
         "r"(cta)
         : "memory");
 }
+#ifndef SF_MBAR_SUSPEND_NS
+#define SF_MBAR_SUSPEND_NS 0  // > 0: try_wait suspend-time hint (ns) instead of the system default
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#if SF_MBAR_SUSPEND_NS > 0
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+        "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity), "n"(SF_MBAR_SUSPEND_NS)
+        : "memory");
+#else
     asm volatile(
         "{\n\t.reg .pred P1;\n\t"
         "WAIT_%=:\n\t"
@@ -61,6 +73,25 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
         "r"(parity)
         : "memory");
+#endif
+}
+// Wait with back-off for the single-thread roles (TMA producer, MMA issuer) whose waits are long
+// and off the critical path: a failed probe sleeps the warp instead of re-issuing the probe, so the
+// spin loop does not take issue slots from the math warps sharing its SM sub-partition.
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.b32 %0, 1, 0, P1;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+template <int kSleepNs = 64>
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+    while (!mbar_try(bar, parity)) __nanosleep(kSleepNs);
 }
 // cluster-scope acquire variant (for barriers remote CTAs arrive on)
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
