@@ -96,6 +96,14 @@ sf_status sf_mask_generate(const sf_mask_desc* terms, int32_t n_terms, uint32_t*
 sf_status sf_mask_pack_u8(const uint8_t* d_mask_u8, int32_t seq_len, uint32_t* d_bits,
                           void* stream);
 
+/* SFMK dense-mask dump (write_dense_mask / read_dense_mask, io.hpp:61-95): header "SFMK", version 1,
+ * seq_len, reserved, then the n*n bits row-major LSB-first. serialize: buf == NULL -> *nbytes only;
+ * synchronizes. deserialize: d_bits == NULL -> *seq_len only; d_bits holds n * sf_mask_words(n)
+ * words. SF_IO_ERROR on bad magic / version / truncation (the reference's io_error). */
+sf_status sf_mask_serialize(const uint32_t* d_bits, int32_t seq_len, uint8_t* buf, int64_t cap, int64_t* nbytes,
+                            void* stream);
+sf_status sf_mask_deserialize(const uint8_t* buf, int64_t nbytes, int32_t* seq_len, uint32_t* d_bits, void* stream);
+
 /* d_acc |= d_src over n rows of sf_mask_words(n) words: compose of arbitrary masks
  * (mask.hpp:146-166) when they are not all descriptor-generated. */
 sf_status sf_mask_or(const uint32_t* d_src, uint32_t* d_acc, int32_t seq_len, void* stream);

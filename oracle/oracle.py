@@ -308,6 +308,19 @@ class Reference:
         self.lib.ref_build_bsr_sfbr(_ptr(mask, C.c_uint8), n, bm, bn, _ptr(buf, C.c_uint8), nb.value, C.byref(nb), None)
         return buf.tobytes(), counts
 
+    def sfmk(self, mask) -> bytes:
+        """the reference's write_dense_mask bytes (io.hpp:66-76)."""
+        mask = np.ascontiguousarray(mask, np.uint8)
+        n = mask.shape[0]
+        nb = C.c_int64()
+        self.lib.ref_mask_sfmk.argtypes = [C.POINTER(C.c_uint8), C.c_int, C.POINTER(C.c_uint8), C.c_int64,
+                                           C.POINTER(C.c_int64)]
+        self.lib.ref_mask_sfmk(_ptr(mask, C.c_uint8), n, None, 0, C.byref(nb))
+        buf = np.zeros(nb.value, np.uint8)
+        if self.lib.ref_mask_sfmk(_ptr(mask, C.c_uint8), n, _ptr(buf, C.c_uint8), nb.value, C.byref(nb)):
+            raise ValueError("ref_mask_sfmk failed")
+        return buf.tobytes()
+
     def rowwise(self, mask):
         mask = np.ascontiguousarray(mask, np.uint8)
         n = mask.shape[0]

@@ -105,6 +105,17 @@ int ref_build_bsr_sfbr(const uint8_t* mask, int n, int bm, int bn, uint8_t* buf,
     });
 }
 
+// write_dense_mask (io.hpp:66-76) of a uint8 mask: the reference's SFMK bytes.
+int ref_mask_sfmk(const uint8_t* mask, int n, uint8_t* buf, int64_t cap, int64_t* nbytes) {
+    return guard([&] {
+        std::ostringstream os;
+        write_dense_mask(os, from_u8(mask, n));
+        const std::string s = os.str();
+        *nbytes = static_cast<int64_t>(s.size());
+        if (buf) std::memcpy(buf, s.data(), std::min<size_t>(s.size(), static_cast<size_t>(cap)));
+    });
+}
+
 // build_rowwise (bsr.hpp:198).
 int ref_build_rowwise(const uint8_t* mask, int n, int32_t* row_ptr, int32_t* col_idx, int64_t cap,
                       int64_t* nnz) {

@@ -108,6 +108,8 @@ SIGNATURES = {
     "sf_bsr_free": (C.c_int, [C.POINTER(BsrDev), _P]),
     "sf_bsr_to_host": (C.c_int, [C.POINTER(BsrDev)] + [_P] * 8 + [_P]),
     "sf_bsr_serialize": (C.c_int, [C.POINTER(BsrDev), _P, _I64, C.POINTER(_I64), _P]),
+    "sf_mask_serialize": (C.c_int, [_P, _I32, _P, _I64, C.POINTER(_I64), _P]),
+    "sf_mask_deserialize": (C.c_int, [_P, _I64, C.POINTER(_I32), _P, _P]),
     "sf_rowwise_build": (C.c_int, [_P, _I32, C.POINTER(CsrDev), _P]),
     "sf_csr_free": (C.c_int, [C.POINTER(CsrDev), _P]),
     "sf_csr_to_host": (C.c_int, [C.POINTER(CsrDev), _P, _P, _P]),

@@ -10,6 +10,7 @@
 // dependency phases, then temper in parallel, and set tile bits in a ceil(n/block)^2 bitmap
 // that the word kernel reads. Bit-exact with the reference: the comparison
 // (x >> 11) * 2^-53 < filling_rate is exact in double precision.
+#include <cstring>
 #include <vector>
 
 #include "common.cuh"
@@ -277,5 +278,87 @@ extern "C" sf_status sf_mask_count(const uint32_t* d_bits, int32_t seq_len, int6
     SF_CUDA_TRY(cudaFreeAsync(d, st));
     SF_CUDA_TRY(cudaStreamSynchronize(st));
     *count = static_cast<int64_t>(h);
+    return SF_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// SFMK dense-mask dump (io.hpp:61-95 write_dense_mask / read_dense_mask): 16-byte header
+// ("SFMK", version 1, seq_len, reserved 0) then the n*n bits row-major, packed LSB-first with no
+// per-row padding. The device rows are word-padded, so the flat stream is re-packed on device:
+// one thread per output byte gathers its 8 bits.
+namespace sf {
+namespace {
+__global__ void sfmk_pack_kernel(const uint32_t* __restrict__ bits, int32_t n, int32_t words, int64_t nbytes,
+                                 uint8_t* __restrict__ out) {
+    const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k >= nbytes) return;
+    const int64_t total = static_cast<int64_t>(n) * n;
+    uint32_t v = 0;
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+        const int64_t f = 8 * k + b;
+        if (f >= total) break;
+        const int64_t i = f / n, j = f - i * n;
+        v |= ((bits[i * words + (j >> 5)] >> (j & 31)) & 1u) << b;
+    }
+    out[k] = static_cast<uint8_t>(v);
+}
+__global__ void sfmk_unpack_kernel(const uint8_t* __restrict__ in, int32_t n, int32_t words, uint32_t* __restrict__ bits) {
+    const int64_t w = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (w >= static_cast<int64_t>(n) * words) return;
+    const int64_t i = w / words, j0 = (w - i * words) * 32;
+    uint32_t v = 0;
+    for (int b = 0; b < 32 && j0 + b < n; ++b) {
+        const int64_t f = i * n + j0 + b;
+        v |= ((in[f >> 3] >> (f & 7)) & 1u) << b;
+    }
+    bits[w] = v;
+}
+}  // namespace
+}  // namespace sf
+
+extern "C" sf_status sf_mask_serialize(const uint32_t* d_bits, int32_t seq_len, uint8_t* buf, int64_t cap,
+                                       int64_t* nbytes, void* stream) {
+    if (seq_len <= 0) return fail(SF_INVALID_PARAMETER, "seq_len must be positive");
+    const int64_t payload = (static_cast<int64_t>(seq_len) * seq_len + 7) / 8;
+    if (nbytes) *nbytes = 16 + payload;
+    if (!buf) return SF_OK;
+    if (cap < 16 + payload) return fail(SF_INVALID_PARAMETER, "buffer too small for the SFMK dump");
+    cudaStream_t st = as_stream(stream);
+    uint8_t* d = nullptr;
+    SF_CUDA_TRY(pool_malloc(reinterpret_cast<void**>(&d), static_cast<size_t>(payload), st));
+    sfmk_pack_kernel<<<static_cast<unsigned>(ceil_div(payload, 256)), 256, 0, st>>>(d_bits, seq_len,
+                                                                                   sf_mask_words(seq_len), payload, d);
+    SF_LAUNCH_CHECK();
+    const uint32_t hdr[4] = {0x4B4D4653u /* "SFMK" */, 1u, static_cast<uint32_t>(seq_len), 0u};
+    std::memcpy(buf, hdr, 16);
+    SF_CUDA_TRY(cudaMemcpyAsync(buf + 16, d, static_cast<size_t>(payload), cudaMemcpyDeviceToHost, st));
+    SF_CUDA_TRY(cudaFreeAsync(d, st));
+    SF_CUDA_TRY(cudaStreamSynchronize(st));
+    return SF_OK;
+}
+
+extern "C" sf_status sf_mask_deserialize(const uint8_t* buf, int64_t nbytes, int32_t* seq_len, uint32_t* d_bits,
+                                         void* stream) {
+    if (!buf || nbytes < 16) return fail(SF_IO_ERROR, "truncated mask dump");
+    uint32_t hdr[4];
+    std::memcpy(hdr, buf, 16);
+    if (hdr[0] != 0x4B4D4653u) return fail(SF_IO_ERROR, "bad mask dump magic");           // io.hpp:80
+    if (hdr[1] != 1u) return fail(SF_IO_ERROR, "unsupported mask dump version");          // io.hpp:82
+    const int32_t n = static_cast<int32_t>(hdr[2]);
+    const int64_t payload = (static_cast<int64_t>(n) * n + 7) / 8;
+    if (n <= 0 || nbytes < 16 + payload) return fail(SF_IO_ERROR, "truncated mask dump");  // io.hpp:88
+    if (seq_len) *seq_len = n;
+    if (!d_bits) return SF_OK;
+    cudaStream_t st = as_stream(stream);
+    uint8_t* d = nullptr;
+    SF_CUDA_TRY(pool_malloc(reinterpret_cast<void**>(&d), static_cast<size_t>(payload), st));
+    SF_CUDA_TRY(cudaMemcpyAsync(d, buf + 16, static_cast<size_t>(payload), cudaMemcpyHostToDevice, st));
+    const int32_t words = sf_mask_words(n);
+    sfmk_unpack_kernel<<<static_cast<unsigned>(ceil_div(static_cast<int64_t>(n) * words, 256)), 256, 0, st>>>(
+        d, n, words, d_bits);
+    SF_LAUNCH_CHECK();
+    SF_CUDA_TRY(cudaFreeAsync(d, st));
+    SF_CUDA_TRY(cudaStreamSynchronize(st));
     return SF_OK;
 }

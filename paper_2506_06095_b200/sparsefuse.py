@@ -108,6 +108,24 @@ class DenseMask:
         bits = np.unpackbits(w.view(np.uint8), axis=1, bitorder="little")
         return bits[:, : self.seq_len].astype(np.uint8)
 
+    def sfmk(self, stream=None) -> bytes:
+        """write_dense_mask bytes (io.hpp:61-76), packed on device."""
+        nb = C.c_int64()
+        check(lib().sf_mask_serialize(self.bits.data_ptr(), self.seq_len, None, 0, C.byref(nb), _stream(stream)))
+        buf = (C.c_uint8 * nb.value)()
+        check(lib().sf_mask_serialize(self.bits.data_ptr(), self.seq_len, buf, nb.value, C.byref(nb), _stream(stream)))
+        return bytes(buf)
+
+    @staticmethod
+    def from_sfmk(data: bytes, device="cuda", stream=None) -> "DenseMask":
+        """read_dense_mask (io.hpp:78-95): IoError on bad magic / version / truncation."""
+        buf = (C.c_uint8 * len(data)).from_buffer_copy(data)
+        n = C.c_int32()
+        check(lib().sf_mask_deserialize(buf, len(data), C.byref(n), None, _stream(stream)))
+        dm = DenseMask.empty(n.value, device)
+        check(lib().sf_mask_deserialize(buf, len(data), C.byref(n), dm.bits.data_ptr(), _stream(stream)))
+        return dm
+
     def true_count(self, stream=None) -> int:
         c = C.c_int64()
         check(lib().sf_mask_count(self.bits.data_ptr(), self.seq_len, C.byref(c), _stream(stream)))

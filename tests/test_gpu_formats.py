@@ -123,3 +123,42 @@ def test_planner_matches_golden(sf):
         assert p.score == e["score"] and p.threshold == e["threshold"]
     with pytest.raises(sf._lib.DegenerateInput):
         sf.threshold(sf.generate_mask(dict(pattern="sliding", seq_len=16, band_width=2)))
+
+
+def _sfmk_restated(m):
+    """write_dense_mask (io.hpp:66-76) restated: header + the n*n bits, row-major, LSB-first."""
+    n = m.shape[0]
+    return b"SFMK" + np.array([1, n, 0], np.uint32).tobytes() + np.packbits(m.flatten(), bitorder="little").tobytes()
+
+
+@pytest.mark.parametrize("cfg", list(CONFIG_MASKS))
+def test_sfmk_dump_matches_reference_bytes(sf, oracle, cfg):
+    terms = CONFIG_MASKS[cfg]
+    dm = sf.generate_mask(terms)
+    got = dm.sfmk()
+    assert got == _sfmk_restated(oracle.mask(terms))
+    from oracle.oracle import Reference
+    r = Reference()
+    if r.available:  # the reference's own writer on the same mask bytes
+        assert got == r.sfmk(dm.to_numpy())
+    back = sf.DenseMask.from_sfmk(got)  # read_dense_mask round trip
+    assert back.seq_len == dm.seq_len and np.array_equal(back.to_numpy(), dm.to_numpy())
+
+
+@pytest.mark.parametrize("n", [1, 7, 33, 300, 1000, 2049])
+def test_sfmk_round_trip_ragged(sf, n):
+    m = (np.random.default_rng(n).random((n, n)) < 0.3).astype(np.uint8)
+    dm = sf.DenseMask.from_numpy(m)
+    data = dm.sfmk()
+    assert data == _sfmk_restated(m)
+    assert np.array_equal(sf.DenseMask.from_sfmk(data).to_numpy(), m)
+
+
+def test_sfmk_errors(sf):
+    data = sf.gen_sliding_window(64, 4).sfmk()
+    with pytest.raises(sf._lib.IoError):
+        sf.DenseMask.from_sfmk(b"SFBR" + data[4:])  # io.hpp:80 bad magic
+    with pytest.raises(sf._lib.IoError):
+        sf.DenseMask.from_sfmk(data[:4] + np.array([2], np.uint32).tobytes() + data[8:])  # :82 version
+    with pytest.raises(sf._lib.IoError):
+        sf.DenseMask.from_sfmk(data[:-1])  # :88 truncated

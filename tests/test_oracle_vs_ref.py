@@ -171,3 +171,13 @@ def test_chain_oracle_equals_reference_run_chain(oracle, reference, model):
     ours = run_chain(oracle, model, gd, gd["input"], m, bs, seq, heads, hs, 16, 16, threads=1)
     ref = reference.run_chain(model, bs, seq, hid, heads, hs, 1, m, 16, 16)
     assert np.max(np.abs(ours - ref)) <= 1e-5, np.max(np.abs(ours - ref))
+
+
+def test_sfmk_format_restatement_matches_reference(reference):
+    """The SFMK dump the GPU tests check against (header + LSB-first n*n bits, io.hpp:61-76) is
+    byte-identical to the reference's write_dense_mask, ragged sizes included."""
+    import numpy as np
+    for n in (1, 7, 33, 300, 1024):
+        m = (np.random.default_rng(n).random((n, n)) < 0.3).astype(np.uint8)
+        restated = b"SFMK" + np.array([1, n, 0], np.uint32).tobytes() + np.packbits(m.flatten(), bitorder="little").tobytes()
+        assert reference.sfmk(m) == restated
