@@ -4,7 +4,7 @@
 //   split into 4 groups of 8 lanes; each group handles one gathered key at a time, so a K/V row
 //   of d fp16 is read by 8 lanes with 16-byte vector loads (coalesced 128-byte row for d=64).
 //   Per-group online softmax in fp32, merged across the 4 groups with shuffles at the end.
-//   attn_rowwise64: the head-size-64 specialisation (two keys in flight per group, FFMA2, lazy
+//   attn_rowwise64: the head-size-64 specialisation (four keys in flight per group, FFMA2, lazy
 //   max update).
 //
 // attn_bsr_generic: the block-skipping executor (attention.hpp:71-172) for ANY tile shape the
@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(256) attn_rowwise_kernel(sf_attn_args a, const
 }
 
 // Head size 64, 16-byte aligned rows (the common case): same warp/group geometry, but each
-// group keeps TWO gathered keys in flight (4 x 16-byte loads issued before any use), the dot and
+// group keeps FOUR gathered keys in flight (8 x 16-byte loads issued before any use), the dot and
 // P.V updates run as packed fp32 pairs (FFMA2), and the running max is updated lazily (rescale
 // only when a score exceeds the max by > 2^8, so p <= 256): one exp2 per key instead of two.
 __device__ __forceinline__ void h8_to_f(const uint4& raw, float2 (&f)[4]) {
@@ -168,29 +168,41 @@ __global__ void __launch_bounds__(256) attn_rowwise64_kernel(sf_attn_args a, con
     float m = -INFINITY, l = 0.f;
     const unsigned gmask = 0xffu << (grp * 8);
     const int32_t r0 = row_ptr[i], r1 = row_ptr[i + 1];
-    for (int32_t kk = r0 + grp; kk < r1; kk += 8) {
-        const bool two = kk + 4 < r1;  // group-uniform
-        const int64_t j0 = col_idx[kk];
-        const int64_t j1 = two ? col_idx[kk + 4] : j0;
-        const uint4 k0 = *reinterpret_cast<const uint4*>(K + j0 * a.q_sn);
-        const uint4 k1 = *reinterpret_cast<const uint4*>(K + j1 * a.q_sn);
-        const uint4 v0 = *reinterpret_cast<const uint4*>(V + j0 * a.q_sn);
-        const uint4 v1 = *reinterpret_cast<const uint4*>(V + j1 * a.q_sn);
-        float2 kf[4], d0 = make_float2(0.f, 0.f), d1 = make_float2(0.f, 0.f);
-        cvt8<T>(k0, kf);
+    // kNK keys per group in flight: all column indices, then all K and V rows are requested before
+    // any is used (the loop is bound by dependent gather latency, not by arithmetic)
+    constexpr int kNK = 4;
+    for (int32_t kk = r0 + grp; kk < r1; kk += 4 * kNK) {
+        int64_t jj[kNK];
+        bool live[kNK];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) d0 = f2fma(q[e], kf[e], d0);
-        cvt8<T>(k1, kf);
-#pragma unroll
-        for (int e = 0; e < 4; ++e) d1 = f2fma(q[e], kf[e], d1);
-        float s0 = d0.x + d0.y, s1 = d1.x + d1.y;
-#pragma unroll
-        for (int o = 1; o < 8; o <<= 1) {
-            s0 += __shfl_xor_sync(gmask, s0, o);
-            s1 += __shfl_xor_sync(gmask, s1, o);
+        for (int t = 0; t < kNK; ++t) {
+            live[t] = kk + 4 * t < r1;  // group-uniform
+            jj[t] = live[t] ? col_idx[kk + 4 * t] : 0;
         }
-        if (!two) s1 = -INFINITY;
-        const float mx = fmaxf(s0, s1);
+        uint4 kr[kNK], vr[kNK];
+#pragma unroll
+        for (int t = 0; t < kNK; ++t) kr[t] = *reinterpret_cast<const uint4*>(K + jj[t] * a.q_sn);
+#pragma unroll
+        for (int t = 0; t < kNK; ++t) vr[t] = *reinterpret_cast<const uint4*>(V + jj[t] * a.q_sn);
+        float sc[kNK];
+#pragma unroll
+        for (int t = 0; t < kNK; ++t) {
+            float2 kf[4], dd = make_float2(0.f, 0.f);
+            cvt8<T>(kr[t], kf);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) dd = f2fma(q[e], kf[e], dd);
+            sc[t] = dd.x + dd.y;
+        }
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1)
+#pragma unroll
+            for (int t = 0; t < kNK; ++t) sc[t] += __shfl_xor_sync(gmask, sc[t], o);
+        float mx = -INFINITY;
+#pragma unroll
+        for (int t = 0; t < kNK; ++t) {
+            if (!live[t]) sc[t] = -INFINITY;
+            mx = fmaxf(mx, sc[t]);
+        }
         if (mx > m + kLazy || m == -INFINITY) {  // group-uniform
             const float a1 = m == -INFINITY ? 0.f : exp2f(m - mx);
             l *= a1;
@@ -198,15 +210,15 @@ __global__ void __launch_bounds__(256) attn_rowwise64_kernel(sf_attn_args a, con
             for (int e = 0; e < 4; ++e) acc[e] = make_float2(acc[e].x * a1, acc[e].y * a1);
             m = mx;
         }
-        const float p0 = exp2f(s0 - m), p1 = exp2f(s1 - m);  // s1 = -inf -> 0
-        l += p0 + p1;
-        float2 vf[4];
-        cvt8<T>(v0, vf);
 #pragma unroll
-        for (int e = 0; e < 4; ++e) acc[e] = f2fma(make_float2(p0, p0), vf[e], acc[e]);
-        cvt8<T>(v1, vf);
+        for (int t = 0; t < kNK; ++t) {
+            const float pt = exp2f(sc[t] - m);  // dead slots: -inf -> 0
+            l += pt;
+            float2 vf[4];
+            cvt8<T>(vr[t], vf);
 #pragma unroll
-        for (int e = 0; e < 4; ++e) acc[e] = f2fma(make_float2(p1, p1), vf[e], acc[e]);
+            for (int e = 0; e < 4; ++e) acc[e] = f2fma(make_float2(pt, pt), vf[e], acc[e]);
+        }
     }
     // merge the 4 groups (lanes gl, gl+8, gl+16, gl+24 hold the same dims)
 #pragma unroll
