@@ -487,30 +487,33 @@ def main():
     value = tokens / (ms_per_step / 1e3)
 
     # ---- e2e through the public API with host buffers: every step copies its input from pinned
-    # host memory and reads its output back. Copies run on their own streams (copy engines) and
-    # overlap the previous/next step's compute; two layer instances (shared weights and formats)
-    # double-buffer the activations so no buffer is overwritten while a copy still reads it.
+    # host memory and reads its output back. Copies run on their own streams (copy engines, both
+    # PCIe directions at once) and overlap neighbouring steps' compute; NB layer instances (shared
+    # weights and formats) rotate the activations so no buffer is overwritten while a copy still
+    # reads it, and the copy streams never wait on the compute of the step just before.
+    NB = 3
     hx = torch.empty(s.rows, s.hidden, dtype=torch.float16, pin_memory=True)
     hx.copy_(x.cpu())
-    hy = [torch.empty_like(hx, pin_memory=True) for _ in range(2)]
-    Ls = [L, layer.EncoderLayer(cfg["model"], s, W, ctx, ln_split=args.ln_split)]
-    xs = [x, torch.empty_like(x)]
-    Ls[1].capture(xs[1])
+    hy = [torch.empty_like(hx, pin_memory=True) for _ in range(NB)]
+    Ls = [L] + [layer.EncoderLayer(cfg["model"], s, W, ctx, ln_split=args.ln_split) for _ in range(NB - 1)]
+    xs = [x] + [torch.empty_like(x) for _ in range(NB - 1)]
+    for b in range(1, NB):
+        Ls[b].capture(xs[b])
     s_in, s_comp, s_out = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
     ev = lambda: torch.cuda.Event(enable_timing=False)
-    in_ready, comp_done, out_done = [ev(), ev()], [ev(), ev()], [ev(), ev()]
+    in_ready, comp_done, out_done = [ev() for _ in range(NB)], [ev() for _ in range(NB)], [ev() for _ in range(NB)]
 
     def e2e_run(n):
         for i in range(n):
-            b = i & 1
-            if i >= 2:
-                s_in.wait_event(comp_done[b])       # x[b] no longer read by step i-2
+            b = i % NB
+            if i >= NB:
+                s_in.wait_event(comp_done[b])       # x[b] no longer read by step i-NB
             with torch.cuda.stream(s_in):
                 xs[b].copy_(hx, non_blocking=True)
                 in_ready[b].record(s_in)
             s_comp.wait_event(in_ready[b])
-            if i >= 2:
-                s_comp.wait_event(out_done[b])      # out of layer b read back by step i-2
+            if i >= NB:
+                s_comp.wait_event(out_done[b])      # out of layer b read back by step i-NB
             with torch.cuda.stream(s_comp):
                 Ls[b].replay()                      # the layer's launches as one CUDA graph
             comp_done[b].record(s_comp)
@@ -527,7 +530,7 @@ def main():
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(s_in)
     e2e_run(e2e_steps)
-    s_out.wait_event(out_done[(e2e_steps - 1) & 1])
+    s_out.wait_event(out_done[(e2e_steps - 1) % NB])
     e1.record(s_out)
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1) / e2e_steps
@@ -571,7 +574,8 @@ def main():
                        "kernel_timing": "event-record nodes between the launches of an instrumented copy of the step's CUDA graph, K extra steps, mean"},
             "e2e": {"value": tokens / (e2e_ms / 1e3), "unit": "tokens/s",
                     "h2d_bytes_per_step": int(hx.numel() * 2), "d2h_bytes_per_step": int(hy[0].numel() * 2),
-                    "copies": "pinned host buffers, H2D/D2H on copy streams overlapping adjacent steps' compute"},
+                    "copies": "pinned host buffers, H2D/D2H on copy streams overlapping adjacent steps' compute",
+                    "pcie_bound": "25.2 MB each way per step at ~49 GB/s per direction concurrently (tools/pcie_bw.py)"},
             "gpu_launches": int(launches), "roofline": roof, "kernels_ms": parts, "mha": mha,
             "clocks": clk.summary()}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
