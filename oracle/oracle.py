@@ -373,6 +373,16 @@ class Reference:
             raise ValueError(f"ref_run_pipeline_synthetic status {st}")
         return buf.value.decode()
 
+    def cache_session(self, model, bs, seq, model_seed, cfg_seed, path_in="", path_out="") -> str:
+        f = self.lib.ref_cache_session
+        f.argtypes = [C.c_char_p, C.c_int64, C.c_int64, C.c_uint64, C.c_uint64, C.c_char_p, C.c_char_p,
+                      C.c_char_p, C.c_int64]
+        buf = C.create_string_buffer(1 << 16)
+        st = f(model.encode(), bs, seq, model_seed, cfg_seed, path_in.encode(), path_out.encode(), buf, len(buf))
+        if st:
+            raise ValueError(f"ref_cache_session status {st}")
+        return buf.value.decode()
+
     def run_chain(self, model, bs, seq, hidden, heads, head_size, seed, mask, bm, bn, code="", threads=1):
         mask = np.ascontiguousarray(mask, np.uint8)
         out = np.zeros((bs * seq, hidden), np.float32)

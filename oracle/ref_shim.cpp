@@ -348,4 +348,34 @@ int ref_run_pipeline_synthetic(const char* model, int64_t bs, int64_t seq, uint6
     });
 }
 
+// Two-stage search on the SyntheticBackend with tuning-cache persistence (io.hpp:407-458): load the
+// context's entries from path_in (if given), run, append the session's entries to path_out.
+// Returns the report line (same format as above) — cross-implementation cache files must yield
+// identical warm sessions.
+int ref_cache_session(const char* model, int64_t bs, int64_t seq, uint64_t model_seed, uint64_t cfg_seed,
+                      const char* path_in, const char* path_out, char* out, int64_t cap) {
+    return guard([&] {
+        GraphHyper hy{bs, seq, 768, 12, 64, 0};
+        const OpGraph g = build_preset_graph(model, hy);
+        SyntheticCostModel m = SyntheticCostModel::random_model(model_seed);
+        SyntheticBackend be(m);
+        SearchConfig cfg;
+        cfg.seed = cfg_seed;
+        const std::string ctx = cache_context(g, be.id(), "a100");
+        TuningCache cache = (path_in && path_in[0]) ? load_cache_file(path_in, ctx) : TuningCache{};
+        const TuningReport r = run_pipeline(g, hw_preset("a100"), DenseMask(static_cast<int>(seq), true), be, cfg, cache);
+        if (path_out && path_out[0]) append_cache_file(path_out, ctx, cache);
+        std::ostringstream o;
+        o.precision(17);
+        o << "ctx=" << ctx << ";code=" << r.code << ";e2e=" << r.end_to_end_s;
+        for (const auto& sg : r.segments) o << ";seg=" << sg.seg.begin << "-" << sg.seg.end << ":" << sg.setting.key() << ":" << sg.duration;
+        const auto& t = r.stats;
+        o << ";stats=" << t.measure_calls << "," << t.sample_evals << "," << t.cache_hits << "," << t.e2e_calls << ","
+          << t.e2e_hits;
+        const std::string str = o.str();
+        std::strncpy(out, str.c_str(), static_cast<size_t>(cap - 1));
+        out[cap - 1] = '\0';
+    });
+}
+
 }  // extern "C"

@@ -3,9 +3,12 @@
 // CUDA-event timed with the reference's 3-warm-up best-of-N protocol, backend.hpp:488-500), with a
 // JSON tuning report on stdout (the fields of the reference's report, io.hpp:360-458).
 //
-//   sf_tune <bert-layer|gpt-layer|t5-layer> <bs> <seq_len> <mask> [seed]
+//   sf_tune <bert-layer|gpt-layer|t5-layer> <bs> <seq_len> <mask> [seed] [--cache file.jsonl]
 //   mask := term("+"term)*, term := pattern[:band[:global[:dilation[:fill[:seed]]]]]
 //   e.g.   sf_tune t5-layer 8 4096 dilated:64:0:1+global:0:64
+// --cache: the tuning cache persisted across sessions (io.hpp:407-458 schema and context hash,
+// interchangeable with the reference's files): the context's entries are loaded before the
+// search and the session's new measurements appended after it.
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -13,6 +16,7 @@
 #include <sstream>
 
 #include "sparsefuse_b200/gpu_backend.hpp"
+#include "sparsefuse_b200/io.hpp"
 
 using namespace sparsefuse;
 
@@ -53,10 +57,19 @@ static DenseMask parse_mask(const std::string& spec, int n) {
 static std::string jstr(const std::string& s) { return "\"" + s + "\""; }
 
 int main(int argc, char** argv) {
-    if (argc < 5) {
-        std::fprintf(stderr, "usage: sf_tune <model> <bs> <seq_len> <mask> [seed]\n");
+    std::string cache_path;
+    std::vector<char*> pos;
+    for (int i = 1; i < argc; ++i) {
+        if (std::string(argv[i]) == "--cache" && i + 1 < argc) cache_path = argv[++i];
+        else pos.push_back(argv[i]);
+    }
+    if (pos.size() < 4) {
+        std::fprintf(stderr, "usage: sf_tune <model> <bs> <seq_len> <mask> [seed] [--cache file.jsonl]\n");
         return 2;
     }
+    argc = static_cast<int>(pos.size()) + 1;
+    pos.insert(pos.begin(), argv[0]);
+    argv = pos.data();
     try {
         const std::string model = argv[1];
         GraphHyper hy{std::atoll(argv[2]), std::atoll(argv[3]), 768, 12, 64, 0};
@@ -70,8 +83,11 @@ int main(int argc, char** argv) {
         SearchConfig cfg;
         cfg.space = ParamSpace::b200();
         cfg.seed = seed;
-        TuningCache cache;
+        const std::string ctx = cache_context(g, be.id(), "b200");
+        TuningCache cache = cache_path.empty() ? TuningCache{} : load_cache_file(cache_path, ctx);
+        const std::int64_t preloaded = cache.size();
         const TuningReport r = run_pipeline(g, hw_preset("b200"), plan, be, cfg, cache);
+        if (!cache_path.empty()) append_cache_file(cache_path, ctx, cache);
         const auto unfused = unfused_scheme(g.size());
         const double e2e_unfused = be.end_to_end(g, unfused, {});
         std::ostringstream o;
@@ -96,7 +112,8 @@ int main(int argc, char** argv) {
           << ", \"sample_evals\": " << t.sample_evals << ", \"cache_hits\": " << t.cache_hits << ", \"e2e_calls\": "
           << t.e2e_calls << ", \"schemes_evaluated\": " << t.schemes_evaluated << ", \"stage1_accepted\": "
           << t.stage1_accepted << ", \"stage2_iterations\": " << t.stage2_iterations
-          << "}, \"tuning_wall_s\": " << r.wall_time_s << "}";
+          << "}, \"cache\": {\"ctx\": " << jstr(ctx) << ", \"file\": " << jstr(cache_path)
+          << ", \"preloaded_entries\": " << preloaded << "}, \"tuning_wall_s\": " << r.wall_time_s << "}";
         std::cout << o.str() << std::endl;
     } catch (const std::exception& e) {
         std::fprintf(stderr, "sf_tune: %s\n", e.what());

@@ -12,6 +12,7 @@
 #include <sstream>
 
 #include "sparsefuse_b200/gpu_backend.hpp"
+#include "sparsefuse_b200/io.hpp"
 
 using namespace sparsefuse;
 
@@ -64,6 +65,31 @@ static int cmd_search(int argc, char** argv) {
     // a warm re-run on the same cache re-finds the same scheme (stage 1 is fully cache-served)
     const TuningReport r2 = run_pipeline(g, HardwareSpec{"a100", 108, 192 * 1024, 64, 2}, plan, be, cfg, cache);
     REQUIRE(r2.code == r.code);
+    return 0;
+}
+
+// host_api_test cache <model> <bs> <seq> <model_seed> <cfg_seed> <path_in|-> <path_out|->
+// the reference's ref_cache_session, through this API (tests/test_cpp_host_api.py)
+static int cmd_cache(int argc, char** argv) {
+    if (argc < 9) return 2;
+    GraphHyper hy{std::atoll(argv[3]), std::atoll(argv[4]), 768, 12, 64, 0};
+    const OpGraph g = build_preset_graph(argv[2], hy);
+    SyntheticBackend be(SyntheticCostModel::random_model(std::strtoull(argv[5], nullptr, 10)));
+    SearchConfig cfg;
+    cfg.seed = std::strtoull(argv[6], nullptr, 10);
+    const std::string in = argv[7], out = argv[8];
+    const std::string ctx = cache_context(g, be.id(), "a100");
+    TuningCache cache = in != "-" ? load_cache_file(in, ctx) : TuningCache{};
+    KernelPlan plan;
+    const TuningReport r = run_pipeline(g, HardwareSpec{"a100", 108, 192 * 1024, 64, 2}, plan, be, cfg, cache);
+    if (out != "-") append_cache_file(out, ctx, cache);
+    std::ostringstream o;
+    o.precision(17);
+    o << "ctx=" << ctx << ";code=" << r.code << ";e2e=" << r.end_to_end_s;
+    for (const auto& s : r.segments) o << ";seg=" << s.seg.begin << "-" << s.seg.end << ":" << s.setting.key() << ":" << s.duration;
+    const auto& t = r.stats;
+    o << ";stats=" << t.measure_calls << "," << t.sample_evals << "," << t.cache_hits << "," << t.e2e_calls << "," << t.e2e_hits;
+    std::cout << o.str() << "\n";
     return 0;
 }
 
@@ -209,6 +235,7 @@ int main(int argc, char** argv) {
     const std::string cmd = argv[1];
     try {
         if (cmd == "search") return cmd_search(argc, argv);
+        if (cmd == "cache") return cmd_cache(argc, argv);
         if (cmd == "gpu-basics") return cmd_gpu_basics();
         if (cmd == "gpu-backend") return cmd_gpu_backend();
     } catch (const std::exception& e) {

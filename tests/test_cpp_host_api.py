@@ -35,6 +35,26 @@ def test_search_decisions_match_reference(reference, case):
     assert ours == ref
 
 
+@pytest.mark.parametrize("case", [("bert-layer", 16, 1024, 3, 7), ("t5-layer", 8, 4096, 9, 2)])
+def test_tuning_cache_files_are_interchangeable(reference, tmp_path, case):
+    """io.hpp:407-458: a cache file written by either implementation warms the other exactly like
+    its own (same decisions, durations and cache-hit counters), and a cold session's report is the
+    same in both."""
+    model, bs, seq, ms, cs = case
+    ours_f, ref_f = str(tmp_path / "ours.jsonl"), str(tmp_path / "ref.jsonl")
+
+    def ours(pin, pout):
+        return subprocess.run([_bin(), "cache", model, str(bs), str(seq), str(ms), str(cs), pin or "-", pout or "-"],
+                              capture_output=True, text=True, check=True).stdout.strip()
+
+    cold_ours, cold_ref = ours("", ours_f), reference.cache_session(model, bs, seq, ms, cs, "", ref_f)
+    assert cold_ours == cold_ref
+    warm_ref_own = reference.cache_session(model, bs, seq, ms, cs, ref_f, "")
+    assert reference.cache_session(model, bs, seq, ms, cs, ours_f, "") == warm_ref_own
+    assert ours(ref_f, "") == ours(ours_f, "") == warm_ref_own
+    assert warm_ref_own != cold_ref  # the warm session really was served from the file
+
+
 @pytest.mark.gpu
 def test_cpp_api_reference_cases_on_gpu():
     r = subprocess.run([_bin(), "gpu-basics"], capture_output=True, text=True, timeout=600)
