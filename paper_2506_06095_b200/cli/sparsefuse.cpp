@@ -1,0 +1,212 @@
+// sparsefuse — command-line surface over the B200 host API (SPEC.md "cli" module; the
+// reference's tools/sparsefuse.cpp is a stub). JSON on stdout; exit 0 success, 1 verification
+// failure, 2 usage.
+//
+//   sparsefuse mask gen    <mask flags> [--dump file.sfmk]
+//   sparsefuse mask stats  <mask flags> --block BMxBN
+//   sparsefuse plan select <mask flags> --hw NAME --heads H --bs B [--head-size D] [--mode reference|b200]
+//   sparsefuse fuse encode 0-1,1-3,3-4
+//   sparsefuse fuse decode 0110
+//   sparsefuse attn verify <mask flags> [--bs B] [--heads H] [--head-size D] [--seed S]
+//   mask flags: --pattern P --seq-len N [--band W] [--global G] [--dilation R] [--fill F]
+//               [--block-rand B] [--seed S]   (or --sfmk file.sfmk)
+// `tune run` is sf_tune (same directory).
+#include <cstdio>
+#include <cstdlib>
+#include <fstream>
+#include <iostream>
+#include <map>
+#include <random>
+#include <sstream>
+
+#include "sparsefuse_b200/ops.hpp"
+#include "sparsefuse_b200/fusion.hpp"
+
+using namespace sparsefuse;
+
+namespace {
+
+struct Args {
+    std::vector<std::string> pos;
+    std::map<std::string, std::string> kv;
+    std::string get(const std::string& k, const std::string& d = "") const {
+        const auto it = kv.find(k);
+        return it == kv.end() ? d : it->second;
+    }
+    bool has(const std::string& k) const { return kv.count(k) != 0; }
+};
+
+Args parse(int argc, char** argv, int from) {
+    Args a;
+    for (int i = from; i < argc; ++i) {
+        const std::string s = argv[i];
+        if (s.rfind("--", 0) == 0 && i + 1 < argc) a.kv[s.substr(2)] = argv[++i];
+        else a.pos.push_back(s);
+    }
+    return a;
+}
+
+[[noreturn]] void usage(const std::string& why) {
+    std::cout << "{\"error\": \"usage\", \"message\": \"" << why << "\"}" << std::endl;
+    std::exit(2);
+}
+
+std::string num(double v) {
+    std::ostringstream o;
+    o.precision(17);
+    o << v;
+    return o.str();
+}
+
+MaskDescriptor descriptor(const Args& a) {
+    if (!a.has("pattern") || !a.has("seq-len")) usage("mask flags need --pattern and --seq-len");
+    MaskDescriptor d;
+    d.pattern = a.get("pattern");
+    d.seq_len = std::atoi(a.get("seq-len").c_str());
+    d.params.band_width = std::atoi(a.get("band", "0").c_str());
+    d.params.global_width = std::atoi(a.get("global", "0").c_str());
+    d.params.dilation_rate = std::atoi(a.get("dilation", "0").c_str());
+    d.params.filling_rate = std::atof(a.get("fill", "0").c_str());
+    d.params.block = std::atoi(a.get("block-rand", "16").c_str());
+    d.params.seed = std::strtoull(a.get("seed", "0").c_str(), nullptr, 10);
+    return d;
+}
+
+DenseMask mask_of(const Args& a) {
+    if (a.has("sfmk")) {
+        std::ifstream f(a.get("sfmk"), std::ios::binary);
+        if (!f) usage("cannot open " + a.get("sfmk"));
+        const std::string data((std::istreambuf_iterator<char>(f)), std::istreambuf_iterator<char>());
+        int32_t n = 0;
+        check(sf_mask_deserialize(reinterpret_cast<const uint8_t*>(data.data()), static_cast<int64_t>(data.size()), &n,
+                                  nullptr, nullptr));
+        DenseMask m(n);
+        check(sf_mask_deserialize(reinterpret_cast<const uint8_t*>(data.data()), static_cast<int64_t>(data.size()), &n,
+                                  m.mutable_device_bits(), nullptr));
+        return m;
+    }
+    return generate_mask(descriptor(a));
+}
+
+int64_t count(const DenseMask& m) {
+    int64_t c = 0;
+    check(sf_mask_count(m.device_bits(), m.seq_len(), &c, nullptr));
+    return c;
+}
+
+int mask_gen(const Args& a) {
+    const MaskDescriptor d = descriptor(a);
+    const DenseMask m = generate_mask(d);
+    const int64_t nnz = count(m);
+    const double n2 = static_cast<double>(m.seq_len()) * m.seq_len();
+    if (a.has("dump")) {
+        int64_t nb = 0;
+        check(sf_mask_serialize(m.device_bits(), m.seq_len(), nullptr, 0, &nb, nullptr));
+        std::vector<uint8_t> buf(static_cast<size_t>(nb));
+        check(sf_mask_serialize(m.device_bits(), m.seq_len(), buf.data(), nb, &nb, nullptr));
+        std::ofstream(a.get("dump"), std::ios::binary).write(reinterpret_cast<const char*>(buf.data()), nb);
+    }
+    std::cout << "{\"pattern\": \"" << d.pattern << "\", \"seq_len\": " << d.seq_len << ", \"band_width\": "
+              << d.params.band_width << ", \"global_width\": " << d.params.global_width << ", \"dilation_rate\": "
+              << d.params.dilation_rate << ", \"filling_rate\": " << num(d.params.filling_rate) << ", \"block\": "
+              << d.params.block << ", \"seed\": " << d.params.seed << ", \"nnz\": " << nnz
+              << ", \"sparsity\": " << num(1.0 - nnz / n2) << "}" << std::endl;
+    return 0;
+}
+
+int mask_stats(const Args& a) {
+    const DenseMask m = mask_of(a);
+    int bm = 16, bn = 16;
+    const std::string b = a.get("block", "16x16");
+    if (std::sscanf(b.c_str(), "%dx%d", &bm, &bn) < 2) bn = bm;
+    const BsrMask bsr = build_bsr(m, bm, bn);
+    const BlockStats s = block_stats(bsr);
+    const double n2 = static_cast<double>(m.seq_len()) * m.seq_len();
+    std::cout << "{\"seq_len\": " << m.seq_len() << ", \"block_m\": " << bm << ", \"block_n\": " << bn
+              << ", \"full_count\": " << s.full_count << ", \"part_count\": " << s.part_count << ", \"empty_count\": "
+              << s.empty_count << ", \"valid_block_ratio\": " << num(s.valid_block_ratio) << ", \"sparsity\": "
+              << num(1.0 - count(m) / n2) << ", \"pool\": " << bsr.part_mask_pool.size() << "}" << std::endl;
+    return 0;
+}
+
+int plan_select(const Args& a) {
+    const DenseMask m = mask_of(a);
+    const HardwareSpec hw = hw_preset(a.get("hw", "b200"));
+    const PlanMode mode = a.get("mode", "reference") == "b200" ? PlanMode::B200 : PlanMode::Reference;
+    const KernelPlan p = select_plan(m, hw, m.seq_len(), std::atoi(a.get("heads", "12").c_str()),
+                                     std::atoll(a.get("bs", "1").c_str()), std::atoi(a.get("head-size", "64").c_str()), mode);
+    std::cout << "{\"kind\": \"" << to_string(p.kind) << "\", \"block_m\": " << p.block_m << ", \"block_n\": "
+              << p.block_n << ", \"num_warps\": " << p.num_warps << ", \"score\": " << num(p.score)
+              << ", \"threshold\": " << (std::isnan(p.threshold) ? std::string("null") : num(p.threshold))
+              << ", \"fallback\": " << (p.fallback ? "true" : "false") << ", \"hw\": \"" << hw.name << "\"}" << std::endl;
+    return 0;
+}
+
+int fuse(const Args& a, const std::string& op) {
+    if (a.pos.empty()) usage("fuse " + op + " needs an argument");
+    if (op == "decode") {
+        const auto segs = decode(a.pos[0]);
+        std::cout << "{\"code\": \"" << a.pos[0] << "\", \"segments\": [";
+        for (size_t i = 0; i < segs.size(); ++i) std::cout << (i ? ", " : "") << "[" << segs[i].begin << ", " << segs[i].end << "]";
+        std::cout << "]}" << std::endl;
+        return 0;
+    }
+    std::vector<Segment> segs;
+    std::stringstream ss(a.pos[0]);
+    std::string item;
+    while (std::getline(ss, item, ',')) {
+        int b = 0, e = 0;
+        if (std::sscanf(item.c_str(), "%d-%d", &b, &e) != 2) usage("segments look like 0-1,1-3");
+        segs.push_back({b, e});
+    }
+    std::cout << "{\"code\": \"" << encode(segs) << "\"}" << std::endl;
+    return 0;
+}
+
+// block-wise (tcgen05 at the B200 plan's tile) vs row-wise on the same seeded inputs; the loaded
+// tile count against block_stats (the executor visits exactly the valid tiles)
+int attn_verify(const Args& a) {
+    const DenseMask m = mask_of(a);
+    const int bs = std::atoi(a.get("bs", "1").c_str()), h = std::atoi(a.get("heads", "2").c_str());
+    const int d = std::atoi(a.get("head-size", "64").c_str());
+    const auto in = random_attention_input<float>(bs, h, m.seq_len(), d, std::strtoull(a.get("seed", "1").c_str(), nullptr, 10));
+    const KernelPlan p = select_plan(m, hw_preset("b200"), m.seq_len(), h, bs, d, PlanMode::B200);
+    const int bm = p.kind == KernelKind::BlockWise ? p.block_m : 128, bn = p.kind == KernelKind::BlockWise ? p.block_n : 16;
+    const BsrMask bsr = build_bsr(m, bm, bn);
+    BlockExecStats st;
+    const Tensor4<float> bw = block_sparse_sdpa(in, bsr, &st);
+    const AttentionInput<double> ind{in.q.cast<double>(), in.k.cast<double>(), in.v.cast<double>()};
+    const Tensor4<double> rw = rowwise_sdpa(ind, build_rowwise(m));
+    double mx = 0.0;
+    for (size_t i = 0; i < bw.v.size(); ++i) mx = std::max(mx, std::abs(static_cast<double>(bw.v[i]) - rw.v[i]));
+    const BlockStats bs_ = block_stats(bsr);
+    const bool tiles_ok = st.tiles_loaded == bs_.full_count + bs_.part_count;
+    const double tol = std::atof(a.get("tol", "2e-2").c_str());
+    const bool pass = mx <= tol && tiles_ok;
+    std::cout << "{\"pass\": " << (pass ? "true" : "false") << ", \"max_abs_blockwise_vs_rowwise\": " << num(mx)
+              << ", \"tolerance\": " << num(tol) << ", \"block\": [" << bm << ", " << bn << "], \"tiles_loaded\": "
+              << st.tiles_loaded << ", \"valid_tiles\": " << bs_.full_count + bs_.part_count << "}" << std::endl;
+    return pass ? 0 : 1;
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+    if (argc < 3) usage("sparsefuse <mask|plan|fuse|attn> <command> [flags]");
+    const std::string grp = argv[1], cmd = argv[2];
+    const Args a = parse(argc, argv, 3);
+    try {
+        if (grp == "mask" && cmd == "gen") return mask_gen(a);
+        if (grp == "mask" && cmd == "stats") return mask_stats(a);
+        if (grp == "plan" && cmd == "select") return plan_select(a);
+        if (grp == "fuse" && (cmd == "encode" || cmd == "decode")) return fuse(a, cmd);
+        if (grp == "attn" && cmd == "verify") return attn_verify(a);
+    } catch (const std::invalid_argument& e) {
+        std::cout << "{\"error\": \"invalid_parameter\", \"message\": \"" << e.what() << "\"}" << std::endl;
+        return 2;
+    } catch (const std::exception& e) {
+        std::cout << "{\"error\": \"failure\", \"message\": \"" << e.what() << "\"}" << std::endl;
+        return 1;
+    }
+    usage("unknown command " + grp + " " + cmd);
+}

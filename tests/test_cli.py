@@ -1,0 +1,49 @@
+"""The `sparsefuse` CLI (SPEC.md cli module): JSON on stdout, exit codes 0 / 1 / 2. The codec
+commands run anywhere; mask / plan / attention commands need the GPU."""
+import json
+import subprocess
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+CLI = ROOT / "paper_2506_06095_b200" / "_lib" / "sparsefuse"
+
+
+def run(*args):
+    if not CLI.exists():
+        pytest.fail("sparsefuse CLI not built — run __graft_entry__.build()")
+    r = subprocess.run([str(CLI), *map(str, args)], capture_output=True, text=True, timeout=300)
+    return r.returncode, json.loads(r.stdout)
+
+
+def test_fuse_codec_commands():
+    rc, j = run("fuse", "decode", "0110")  # SPEC.md: segments [0],[1,2],[3]
+    assert rc == 0 and j["segments"] == [[0, 1], [1, 3], [3, 4]]
+    rc, j = run("fuse", "encode", "0-1,1-3,3-4")
+    assert rc == 0 and j["code"] == "0110"
+
+
+def test_usage_errors_exit_2():
+    rc, j = run("mask", "nope")
+    assert rc == 2 and j["error"] == "usage"
+
+
+@pytest.mark.gpu
+def test_mask_and_plan_commands(oracle, tmp_path):
+    rc, j = run("mask", "gen", "--pattern", "sliding", "--seq-len", 1024, "--band", 32, "--dump", tmp_path / "m.sfmk")
+    assert rc == 0 and abs(j["sparsity"] - 0.938) <= 0.005  # Table 2
+    m = oracle.mask([dict(pattern="sliding", seq_len=1024, band_width=32)])
+    rc, s = run("mask", "stats", "--sfmk", tmp_path / "m.sfmk", "--block", "16x16")
+    b = oracle.bsr(m, 16, 16)
+    assert rc == 0 and (s["full_count"], s["part_count"]) == (len(b["full_col_idx"]), len(b["part_col_idx"]))
+    rc, p = run("plan", "select", "--sfmk", tmp_path / "m.sfmk", "--hw", "a100", "--heads", 12, "--bs", 8)
+    assert rc == 0 and p["kind"] == "block_wise"
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("pattern", [["--pattern", "sliding", "--band", 24], ["--pattern", "bigbird", "--band", 16,
+                                                                               "--global", 16, "--fill", 0.1]])
+def test_attn_verify_passes(pattern):
+    rc, j = run("attn", "verify", *pattern, "--seq-len", 512, "--bs", 1, "--heads", 2)
+    assert rc == 0 and j["pass"] and j["tiles_loaded"] == j["valid_tiles"]
