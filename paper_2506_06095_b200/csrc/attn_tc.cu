@@ -40,7 +40,7 @@ constexpr int kStages = 4;                   // K/V ring depth (two CTAs per SM 
 // must not alias S. S_{j+2}'s commit covers P_j V_j, so P[j%2] is free again at step j+2.
 constexpr int kSBuf = 2;
 constexpr uint32_t kPCol = 128, kOCol = 192;
-constexpr int kMaxRowBlocks = 64;            // n <= 8192 at block_m 128
+constexpr int kMaxRowBlocks = 128;           // n <= 8192 at block_m 64
 constexpr int kQBytes = kBM * kD * 2;
 constexpr int kKVBytes = kNS * kD * 2;       // one 64-key stage of K (or V)
 constexpr int kMaskBytes = kBM * 8;          // 64 bits per query row per stage
@@ -48,9 +48,29 @@ constexpr float kRescaleLog2 = 8.0f;         // lazy-rescale threshold (P <= 2^8
 constexpr int kSmem = 1024 + 2 * kQBytes + 2 * kStages * kKVBytes + kStages * kMaskBytes + kStages * 16 +
                       kMaxRowBlocks * 4 + 256;
 
+// Geometry per query-block height. BM = 128: one (b, h) slice per work item, M = 128 MMAs.
+// BM = 64 ("head pair"): a work item is one 64-row block of TWO heads that share the block's load
+// list (the mask is per (row, column), the same for every head). Each head's tiles are M = 64
+// MMAs whose accumulators sit in TMEM lanes {32q + 0..15} (head A) and {32q + 16..31} (head B)
+// (the cta_group::1 M = 64 layout, lane offset 0 / 16; tools/micro/umma64.cu), so the same 128
+// softmax threads serve both heads and every column group is skipped at 16-row granularity.
+// 64-row blocks execute a third fewer cells than 128-row blocks on BigBird-like masks.
+template <int BM>
+struct AttnGeo {
+    static constexpr bool kPair = BM == 64;
+    static constexpr int kHeads = kPair ? 2 : 1;
+    static constexpr int kStagesG = kPair ? 2 : kStages;
+    static constexpr int kQB = BM * kD * 2 * kHeads;          // 16 KB either way
+    static constexpr int kKVB = kHeads * kNS * kD * 2;         // one stage of K (or V), all heads
+    static constexpr int kMaskB = BM * 8;                      // 64 bits per query row per stage
+    static constexpr int kSmemG = 1024 + 2 * kQB + 2 * kStagesG * kKVB + kStagesG * kMaskB + kStagesG * 16 +
+                                  kMaxRowBlocks * 4 + 256;
+};
+
 struct AttnParams {
     CUtensorMap tq, tk, tv;  // 4-D (d, n, h, b) maps; boxes {64,128,1,1} / {64,bn,1,1}
-    int32_t n, h, bh, n_rows, n_items;
+    int32_t n, h, bh, n_rows, n_items;  // bh: work units per row block (slices, or head pairs at BM 64)
+    int32_t bh_total;                   // b * h slices
     const int32_t* load_row_ptr;
     const int32_t* load_col_idx;
     const int32_t* load_tile;
@@ -201,16 +221,22 @@ struct Cursor {
     }
 };
 
-template <typename T, int BN>
+template <typename T, int BN, int BM>
 __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_constant__ AttnParams p) {
+    using Geo = AttnGeo<BM>;
+    constexpr bool kPair = Geo::kPair;
+    constexpr int kStages = Geo::kStagesG;   // shadows the file-scope BM = 128 values
+    constexpr int kQBytes = Geo::kQB;
+    constexpr int kKVBytes = Geo::kKVB;
+    constexpr int kMaskBytes = Geo::kMaskB;
     constexpr int G = kNS / BN;          // column tiles gathered per 64-key step
-    constexpr int TB = kBM * BN / 8;     // packed bytes of one part tile (pool stride)
+    constexpr int TB = BM * BN / 8;      // packed bytes of one part tile (pool stride)
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     unsigned char* sQ = sm;                               // [2] Q tiles (double-buffered across items)
     unsigned char* sK = sQ + 2 * kQBytes;
     unsigned char* sV = sK + kStages * kKVBytes;
-    unsigned char* sMask = sV + kStages * kKVBytes;        // [kStages][1 KB]: packed part-tile bits
+    unsigned char* sMask = sV + kStages * kKVBytes;        // [kStages][BM * 8 B]: packed part-tile bits
     int32_t* s_kind = reinterpret_cast<int32_t*>(sMask + kStages * kMaskBytes);  // [kStages][4]
     int32_t* s_order = s_kind + 4 * kStages;                                      // [kMaxRowBlocks]
     uint64_t* bars = reinterpret_cast<uint64_t*>(s_order + kMaxRowBlocks);
@@ -275,11 +301,22 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
             int rb, bh, l0, L, nsteps;
             items.get(k, rb, bh, l0, L, nsteps);
             if (nsteps == 0) continue;
-            const int b = bh / p.h, hh = bh % p.h;
+            // the unit's heads: one slice, or the pair (2u, 2u+1) (an odd last pair repeats head A)
+            int hb[2], hh2[2];
+#pragma unroll
+            for (int t = 0; t < Geo::kHeads; ++t) {
+                int s_ = kPair ? 2 * bh + t : bh;
+                if (s_ >= p.bh_total) s_ = 2 * bh;
+                hb[t] = s_ / p.h;
+                hh2[t] = s_ % p.h;
+            }
             if (lane == 0) {
                 tc::mbar_wait(&q_empty[qi & 1], ((qi >> 1) & 1) ^ 1);
                 tc::mbar_expect_tx(&q_full[qi & 1], kQBytes);
-                tma_load_4d(sQ + (qi & 1) * kQBytes, &p.tq, &q_full[qi & 1], 0, rb * kBM, hh, b);
+#pragma unroll
+                for (int t = 0; t < Geo::kHeads; ++t)
+                    tma_load_4d(sQ + (qi & 1) * kQBytes + t * (BM * kD * 2), &p.tq, &q_full[qi & 1], 0, rb * BM, hh2[t],
+                                hb[t]);
             }
             ++qi;
             for (int c = 0; c < L; c += 32) {
@@ -305,8 +342,12 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
 #pragma unroll
                         for (int gg = 0; gg < G; ++gg) {
                             const int col = cols[gg] * BN;
-                            tma_load_4d(sK + st * kKVBytes + gg * BN * kD * 2, &p.tk, &kv_full[st], 0, col, hh, b);
-                            tma_load_4d(sV + st * kKVBytes + gg * BN * kD * 2, &p.tv, &kv_full[st], 0, col, hh, b);
+#pragma unroll
+                            for (int t = 0; t < Geo::kHeads; ++t) {  // head t's 64 keys at t * 8 KB
+                                const int off = st * kKVBytes + t * (kNS * kD * 2) + gg * BN * kD * 2;
+                                tma_load_4d(sK + off, &p.tk, &kv_full[st], 0, col, hh2[t], hb[t]);
+                                tma_load_4d(sV + off, &p.tv, &kv_full[st], 0, col, hh2[t], hb[t]);
+                            }
                             if (tiles[gg] >= 0)
                                 tc::bulk_load(sMask + st * kMaskBytes + gg * TB,
                                               p.pool + static_cast<int64_t>(tiles[gg]) * TB, TB, &kv_full[st]);
@@ -318,8 +359,8 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
     } else if (warp == 1) {
         // ------------------------------------------------------------------ MMA issuer
         constexpr bool bf = std::is_same<T, __nv_bfloat16>::value;
-        constexpr uint32_t idesc_s = tc::idesc_f16(kBM, kNS, bf, 0, 0);  // Q (K-major) x K (K-major)
-        constexpr uint32_t idesc_o = tc::idesc_f16(kBM, kD, bf, 0, 1);   // P (TMEM) x V (MN-major)
+        constexpr uint32_t idesc_s = tc::idesc_f16(BM, kNS, bf, 0, 0);  // Q (K-major) x K (K-major)
+        constexpr uint32_t idesc_o = tc::idesc_f16(BM, kD, bf, 0, 1);   // P (TMEM) x V (MN-major)
         if (tc::elect_one()) {
             Cursor cs, cp;
             cs.next_item(items, nitems);
@@ -335,12 +376,15 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
                 tc::mbar_wait(&kv_full[s], (gS / kStages) & 1);
                 SF_TRACE(gS, 14);
                 tc::fence_after_sync();
-                const uint32_t q0 = tc::smem_u32(sQ + (cs.qi & 1) * kQBytes);
-                const uint32_t k0 = tc::smem_u32(sK + s * kKVBytes);
 #pragma unroll
-                for (int k = 0; k < kD / 16; ++k)
-                    tc::mma_f16_ss(tmem + 64 * (gS % kSBuf), tc::sdesc_sw128(q0 + 32 * k), tc::sdesc_sw128(k0 + 32 * k),
-                                   idesc_s, k != 0);
+                for (int t = 0; t < Geo::kHeads; ++t) {  // head t: M = BM rows at TMEM lane offset 16t
+                    const uint32_t q0 = tc::smem_u32(sQ + (cs.qi & 1) * kQBytes + t * (BM * kD * 2));
+                    const uint32_t k0 = tc::smem_u32(sK + s * kKVBytes + t * (kNS * kD * 2));
+#pragma unroll
+                    for (int k = 0; k < kD / 16; ++k)
+                        tc::mma_f16_ss(tmem + ((16u * t) << 16) + 64 * (gS % kSBuf), tc::sdesc_sw128(q0 + 32 * k),
+                                       tc::sdesc_sw128(k0 + 32 * k), idesc_s, k != 0);
+                }
                 tc::mma_commit(&s_full[gS % kSBuf]);
                 if (cs.j == cs.ns - 1) tc::mma_commit(&q_empty[cs.qi & 1]);  // last S of the item: Q free
                 ++gS;
@@ -353,11 +397,15 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
                 tc::mbar_wait(&p_full[sb], (g / kSBuf) & 1);  // P_g in TMEM (S_g consumed), O rescaled
                 SF_TRACE(g, 8);
                 tc::fence_after_sync();
-                const uint32_t v0 = tc::smem_u32(sV + s * kKVBytes);
 #pragma unroll
-                for (int k = 0; k < kNS / 16; ++k)  // P_g: 64 keys = 32 packed columns, 8 per K=16
-                    tc::mma_f16_ts(tO, tmem + kPCol + 32 * sb + 8 * k, tc::sdesc_sw128_mn(v0 + 2048 * k), idesc_o,
-                                   (cp.j | k) != 0);
+                for (int t = 0; t < Geo::kHeads; ++t) {
+                    const uint32_t v0 = tc::smem_u32(sV + s * kKVBytes + t * (kNS * kD * 2));
+                    const uint32_t lo = (16u * t) << 16;
+#pragma unroll
+                    for (int k = 0; k < kNS / 16; ++k)  // P_g: 64 keys = 32 packed columns, 8 per K=16
+                        tc::mma_f16_ts(tO + lo, tmem + lo + kPCol + 32 * sb + 8 * k, tc::sdesc_sw128_mn(v0 + 2048 * k),
+                                       idesc_o, (cp.j | k) != 0);
+                }
                 tc::mma_commit(&o_full[g & 1]);
                 tc::mma_commit(&kv_empty[s]);
                 SF_TRACE(g, 9);
@@ -370,7 +418,10 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
         // ------------------------------------------------------------------ softmax / epilogue
         // One thread per query row (TMEM lane), all 64 columns of the step.
         const uint32_t q = warp & 3;  // TMEM lane quarter this warp may access
-        const int r = static_cast<int>(q * 32 + lane);
+        // the query row this thread (TMEM lane) holds: BM 128 -> 32q + lane; head pairs (BM 64)
+        // -> row 16q + lane%16 of head lane/16 (the M = 64 accumulator layout)
+        const int r = kPair ? static_cast<int>(q * 16 + (lane & 15)) : static_cast<int>(q * 32 + lane);
+        const int my_head = kPair ? static_cast<int>(lane >> 4) : 0;
         const uint32_t trow = tmem + ((q * 32) << 16);
         const float sl2 = p.scale_log2;
         const uint32_t kind_a = tc::smem_u32(s_kind);
@@ -503,8 +554,10 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
                 if (tr) SF_TRACE(j, 6);
             }
             // ---- epilogue: out = O / l; rows without a valid column stay zero
-            const int b = bh / p.h, hh = bh % p.h;
-            const int64_t i = static_cast<int64_t>(rb) * kBM + r;
+            const int slice = kPair ? 2 * bh + my_head : bh;
+            const bool slice_ok = slice < p.bh_total;  // an odd last head pair has no head B
+            const int b = slice_ok ? slice / p.h : 0, hh = slice_ok ? slice % p.h : 0;
+            const int64_t i = static_cast<int64_t>(rb) * BM + r;
             if (nsteps > 0) {
                 tc::mbar_wait(&o_full[(g - 1) & 1], ((g - 1) >> 1) & 1);
                 tc::fence_after_sync();
@@ -521,7 +574,7 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
 #pragma unroll
                     for (int e = 0; e < 32; ++e) ov[e] = 0u;
                 }
-                if (i < p.n) {
+                if (i < p.n && slice_ok) {
 #pragma unroll
                     for (int c = 0; c < 4; ++c) {
                         float v[8];
@@ -569,24 +622,25 @@ sf_status make_tmap_4d(CUtensorMap* map, const void* base, int n, int h, int bs,
 unsigned long long* g_attn_trace = nullptr;
 
 sf_status attn_tc(const sf_attn_args& a, const sf_bsr_dev& b, cudaStream_t st, bool probe_only) {
-    const bool shape_ok = b.block_m == kBM && (b.block_n == 16 || b.block_n == 32 || b.block_n == 64) &&
+    const bool shape_ok = (b.block_m == 128 || b.block_m == 64) && (b.block_n == 16 || b.block_n == 32 || b.block_n == 64) &&
                           a.head_size == kD && b.n_rows <= kMaxRowBlocks;
     const bool layout_ok = a.q_sn % 8 == 0 && a.q_sh % 8 == 0 && a.q_sb % 8 == 0 && a.o_sn % 8 == 0 &&
                            a.o_sh % 8 == 0 && a.o_sb % 8 == 0 &&
                            ((reinterpret_cast<uintptr_t>(a.q) | reinterpret_cast<uintptr_t>(a.k) |
                              reinterpret_cast<uintptr_t>(a.v) | reinterpret_cast<uintptr_t>(a.o)) & 15) == 0;
     if (!shape_ok || !layout_ok)
-        return fail(SF_PLAN_ERROR, "tcgen05 attention needs block_m 128, block_n 16/32/64, head_size 64, "
+        return fail(SF_PLAN_ERROR, "tcgen05 attention needs block_m 64/128, block_n 16/32/64, head_size 64, "
                                    "16-byte aligned strides");
     if (probe_only) return SF_OK;
     AttnParams p{};
     const bool bf = a.dtype == SF_BF16;
-    SF_TRY(make_tmap_4d(&p.tq, a.q, a.seq_len, a.h, a.bs, a.q_sn, a.q_sh, a.q_sb, kBM, bf));
+    SF_TRY(make_tmap_4d(&p.tq, a.q, a.seq_len, a.h, a.bs, a.q_sn, a.q_sh, a.q_sb, b.block_m, bf));
     SF_TRY(make_tmap_4d(&p.tk, a.k, a.seq_len, a.h, a.bs, a.q_sn, a.q_sh, a.q_sb, b.block_n, bf));
     SF_TRY(make_tmap_4d(&p.tv, a.v, a.seq_len, a.h, a.bs, a.q_sn, a.q_sh, a.q_sb, b.block_n, bf));
     p.n = a.seq_len;
     p.h = a.h;
-    p.bh = a.bs * a.h;
+    p.bh_total = a.bs * a.h;
+    p.bh = b.block_m == 64 ? (p.bh_total + 1) / 2 : p.bh_total;  // head pairs at block_m 64
     p.n_rows = b.n_rows;
     p.n_items = b.n_rows * p.bh;
     p.load_row_ptr = b.load_row_ptr;
@@ -600,11 +654,19 @@ sf_status attn_tc(const sf_attn_args& a, const sf_bsr_dev& b, cudaStream_t st, b
     p.scale_log2 = a.scale * 1.4426950408889634f;
     p.trace = g_attn_trace;
     void (*kern)(AttnParams) = nullptr;
-    if (b.block_n == 16) kern = bf ? attn_tc_kernel<__nv_bfloat16, 16> : attn_tc_kernel<__half, 16>;
-    else if (b.block_n == 32) kern = bf ? attn_tc_kernel<__nv_bfloat16, 32> : attn_tc_kernel<__half, 32>;
-    else kern = bf ? attn_tc_kernel<__nv_bfloat16, 64> : attn_tc_kernel<__half, 64>;
-    if (b.tile_bytes != kBM * b.block_n / 8) return fail(SF_PLAN_ERROR, "BSR tile_bytes does not match block shape");
-    SF_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+    int smem = AttnGeo<128>::kSmemG;
+    if (b.block_m == 128) {
+        if (b.block_n == 16) kern = bf ? attn_tc_kernel<__nv_bfloat16, 16, 128> : attn_tc_kernel<__half, 16, 128>;
+        else if (b.block_n == 32) kern = bf ? attn_tc_kernel<__nv_bfloat16, 32, 128> : attn_tc_kernel<__half, 32, 128>;
+        else kern = bf ? attn_tc_kernel<__nv_bfloat16, 64, 128> : attn_tc_kernel<__half, 64, 128>;
+    } else {
+        smem = AttnGeo<64>::kSmemG;
+        if (b.block_n == 16) kern = bf ? attn_tc_kernel<__nv_bfloat16, 16, 64> : attn_tc_kernel<__half, 16, 64>;
+        else if (b.block_n == 32) kern = bf ? attn_tc_kernel<__nv_bfloat16, 32, 64> : attn_tc_kernel<__half, 32, 64>;
+        else kern = bf ? attn_tc_kernel<__nv_bfloat16, 64, 64> : attn_tc_kernel<__half, 64, 64>;
+    }
+    if (b.tile_bytes != b.block_m * b.block_n / 8) return fail(SF_PLAN_ERROR, "BSR tile_bytes does not match block shape");
+    SF_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     static int n_sm = 0;
     if (!n_sm) {
         int dev = 0;
@@ -613,7 +675,7 @@ sf_status attn_tc(const sf_attn_args& a, const sf_bsr_dev& b, cudaStream_t st, b
     }
     // persistent: two CTAs per SM (smem and TMEM are sized for it), items round-robin
     dim3 grid(static_cast<unsigned>(std::min<int64_t>(p.n_items, 2 * n_sm)));
-    SF_CUDA_TRY(launch_pdl(kern, grid, dim3(kThreads), kSmem, st, nullptr, p));
+    SF_CUDA_TRY(launch_pdl(kern, grid, dim3(kThreads), smem, st, nullptr, p));
     SF_LAUNCH_CHECK();
     return SF_OK;
 }

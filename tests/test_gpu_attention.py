@@ -57,7 +57,8 @@ def test_golden_attention_cases(sf, oracle, impl):
 
 @pytest.mark.parametrize("cfg,tile,bs,h", [("cfg1", (128, 16), 1, 12), ("cfg2", (128, 16), 2, 12),
                                            ("cfg3", (128, 16), 1, 4), ("cfg4", (128, 64), 1, 2),
-                                           ("cfg2", (16, 16), 1, 4), ("cfg1", (64, 32), 1, 4)])
+                                           ("cfg2", (16, 16), 1, 4), ("cfg1", (64, 32), 1, 4),
+                                           ("cfg2", (64, 16), 1, 3), ("cfg3", (64, 16), 1, 2), ("cfg4", (64, 64), 1, 1)])
 def test_config_attention_matches_oracle(sf, oracle, cfg, tile, bs, h):
     import torch
     terms = CONFIG_MASKS[cfg]
@@ -67,7 +68,9 @@ def test_config_attention_matches_oracle(sf, oracle, cfg, tile, bs, h):
     ref, _ = oracle.block_sparse_sdpa(q, k, v, m, *tile, threads=8)
     dm = sf.generate_mask(terms)
     b = sf.build_bsr(dm, *tile)
-    impls = ("generic", "tcgen05") if tile[0] == 128 and tile[1] in (16, 32, 64) else ("generic", "auto")
+    # block_m 64 runs the tcgen05 head-pair kernel (two heads per TMEM tile; odd head counts
+    # leave the last pair's second head empty)
+    impls = ("generic", "tcgen05") if tile[0] in (64, 128) and tile[1] in (16, 32, 64) else ("generic", "auto")
     for impl in impls:
         sf.set_attn_impl(impl)
         out = sf.block_sparse_sdpa(to_dev(q, torch.float16), to_dev(k, torch.float16), to_dev(v, torch.float16), b)
