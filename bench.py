@@ -491,7 +491,7 @@ def main():
     # PCIe directions at once) and overlap neighbouring steps' compute; NB layer instances (shared
     # weights and formats) rotate the activations so no buffer is overwritten while a copy still
     # reads it, and the copy streams never wait on the compute of the step just before.
-    NB = 3
+    NB = int(os.environ.get("SF_E2E_BUFFERS", "4"))
     hx = torch.empty(s.rows, s.hidden, dtype=torch.float16, pin_memory=True)
     hx.copy_(x.cpu())
     hy = [torch.empty_like(hx, pin_memory=True) for _ in range(NB)]
