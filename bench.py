@@ -422,10 +422,16 @@ def main():
 
     import torch
     rank, world, local = dist_env()
-    torch.cuda.set_device(local)
+    # SF_BENCH_SHARED_GPU=1 (test aid): every rank on cuda:0 with gloo — exercises the N > 1 code
+    # path on a one-GPU box (NCCL refuses two ranks on one device). Real runs: one GPU per rank, NCCL.
+    shared = os.environ.get("SF_BENCH_SHARED_GPU") == "1"
+    torch.cuda.set_device(0 if shared else local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2506_06095_b200 import _lib, layer, sparsefuse as sf
 
     s = layer.LayerShape(cfg["bs"], cfg["seq"], cfg["hidden"], cfg["heads"], cfg["hidden"] // cfg["heads"])
@@ -457,7 +463,7 @@ def main():
         torch.distributed.barrier()
     torch.cuda.synchronize()
     parts_sum = {}
-    with ClockSampler(local) as clk:
+    with ClockSampler(0 if shared else local) as clk:
         time.sleep(0.3)  # the sampler's first reading lands inside the timed region
         for a, b in evs:
             flush.zero_()
@@ -479,7 +485,7 @@ def main():
     step_ms = [a.elapsed_time(b) for a, b in evs]
     total_ms = float(sum(step_ms))
     if world > 1:
-        t = torch.tensor([total_ms], device="cuda")
+        t = torch.tensor([total_ms], device="cpu" if shared else "cuda")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
@@ -535,7 +541,7 @@ def main():
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1) / e2e_steps
     if world > 1:
-        t = torch.tensor([e2e_ms], device="cuda")
+        t = torch.tensor([e2e_ms], device="cpu" if shared else "cuda")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         e2e_ms = float(t.item())
 
