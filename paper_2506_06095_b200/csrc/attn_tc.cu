@@ -242,9 +242,14 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
     uint64_t* bars = reinterpret_cast<uint64_t*>(s_order + kMaxRowBlocks);
     uint64_t* q_full = bars;                  // [2]
     uint64_t* q_empty = q_full + 2;           // [2]
-    uint64_t* kv_full = q_empty + 2;          // [kStages]
-    uint64_t* kv_empty = kv_full + kStages;   // [kStages]
-    uint64_t* s_full = kv_empty + kStages;    // [kSBuf]
+    // K (with the stage's part-tile bits and kinds) and V have separate barriers: a K slot is
+    // released as soon as the softmax holds S of that step (and read its bits), a V slot when
+    // P.V of that step is done, so K loads run about a step further ahead than V loads
+    uint64_t* k_full = q_empty + 2;           // [kStages]
+    uint64_t* k_empty = k_full + kStages;     // [kStages] (128 softmax arrivals)
+    uint64_t* v_full = k_empty + kStages;     // [kStages]
+    uint64_t* v_empty = v_full + kStages;     // [kStages]
+    uint64_t* s_full = v_empty + kStages;     // [kSBuf]
     uint64_t* p_full = s_full + kSBuf;        // [kSBuf]
     uint64_t* o_full = p_full + kSBuf;        // [2]: P.V step g completes o_full[g&1] (parity waits are
                                               // unambiguous only within one phase of lag)
@@ -275,8 +280,10 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
             tc::mbar_init(&o_full[i], 1);
         }
         for (int s = 0; s < kStages; ++s) {
-            tc::mbar_init(&kv_full[s], 1);
-            tc::mbar_init(&kv_empty[s], 1);
+            tc::mbar_init(&k_full[s], 1);
+            tc::mbar_init(&k_empty[s], 128);
+            tc::mbar_init(&v_full[s], 1);
+            tc::mbar_init(&v_empty[s], 1);
         }
         for (int s = 0; s < kSBuf; ++s) {
             tc::mbar_init(&s_full[s], 1);
@@ -335,23 +342,30 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
                         parts += tiles[gg] >= 0;
                     }
                     if (lane == 0) {
-                        tc::mbar_wait(&kv_empty[st], ((g / kStages) & 1) ^ 1);
+                        const uint32_t ph = ((g / kStages) & 1) ^ 1;
+                        tc::mbar_wait(&k_empty[st], ph);
 #pragma unroll
                         for (int gg = 0; gg < G; ++gg) s_kind[4 * st + gg] = tiles[gg];
-                        tc::mbar_expect_tx(&kv_full[st], 2 * kKVBytes + parts * TB);  // release: s_kind
+                        tc::mbar_expect_tx(&k_full[st], kKVBytes + parts * TB);  // release: s_kind
 #pragma unroll
                         for (int gg = 0; gg < G; ++gg) {
                             const int col = cols[gg] * BN;
 #pragma unroll
-                            for (int t = 0; t < Geo::kHeads; ++t) {  // head t's 64 keys at t * 8 KB
-                                const int off = st * kKVBytes + t * (kNS * kD * 2) + gg * BN * kD * 2;
-                                tma_load_4d(sK + off, &p.tk, &kv_full[st], 0, col, hh2[t], hb[t]);
-                                tma_load_4d(sV + off, &p.tv, &kv_full[st], 0, col, hh2[t], hb[t]);
-                            }
+                            for (int t = 0; t < Geo::kHeads; ++t)  // head t's 64 keys at t * 8 KB
+                                tma_load_4d(sK + st * kKVBytes + t * (kNS * kD * 2) + gg * BN * kD * 2, &p.tk,
+                                            &k_full[st], 0, col, hh2[t], hb[t]);
                             if (tiles[gg] >= 0)
                                 tc::bulk_load(sMask + st * kMaskBytes + gg * TB,
-                                              p.pool + static_cast<int64_t>(tiles[gg]) * TB, TB, &kv_full[st]);
+                                              p.pool + static_cast<int64_t>(tiles[gg]) * TB, TB, &k_full[st]);
                         }
+                        tc::mbar_wait(&v_empty[st], ph);
+                        tc::mbar_expect_tx(&v_full[st], kKVBytes);
+#pragma unroll
+                        for (int gg = 0; gg < G; ++gg)
+#pragma unroll
+                            for (int t = 0; t < Geo::kHeads; ++t)
+                                tma_load_4d(sV + st * kKVBytes + t * (kNS * kD * 2) + gg * BN * kD * 2, &p.tv,
+                                            &v_full[st], 0, cols[gg] * BN, hh2[t], hb[t]);
                     }
                 }
             }
@@ -373,7 +387,7 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
                 }
                 const int s = gS % kStages;
                 SF_TRACE(gS, 13);
-                tc::mbar_wait(&kv_full[s], (gS / kStages) & 1);
+                tc::mbar_wait(&k_full[s], (gS / kStages) & 1);
                 SF_TRACE(gS, 14);
                 tc::fence_after_sync();
 #pragma unroll
@@ -396,6 +410,7 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
                 const int sb = g % kSBuf;
                 tc::mbar_wait(&p_full[sb], (g / kSBuf) & 1);  // P_g in TMEM (S_g consumed), O rescaled
                 SF_TRACE(g, 8);
+                tc::mbar_wait(&v_full[s], (g / kStages) & 1);
                 tc::fence_after_sync();
 #pragma unroll
                 for (int t = 0; t < Geo::kHeads; ++t) {
@@ -407,7 +422,7 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
                                        idesc_o, (cp.j | k) != 0);
                 }
                 tc::mma_commit(&o_full[g & 1]);
-                tc::mma_commit(&kv_empty[s]);
+                tc::mma_commit(&v_empty[s]);
                 SF_TRACE(g, 9);
                 if (cs.valid) issue_s();
                 SF_TRACE(g, 10);
@@ -435,7 +450,7 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
                 const int sb = g % kSBuf;
                 const bool tr = warp == 2 && lane == 0 && k == 0;
                 if (tr) SF_TRACE(j, 0);
-                tc::mbar_wait(&kv_full[st], (g / kStages) & 1);
+                tc::mbar_wait(&k_full[st], (g / kStages) & 1);
                 if (tr) SF_TRACE(j, 1);
                 // this row's 64 mask bits: full tile -> ones, part tile -> its staged pool row,
                 // padding -> 0
@@ -479,6 +494,7 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
 #pragma unroll
                 for (int a = 0; a < 4; ++a) act[a] = __any_sync(0xffffffffu, ((bits[a >> 1] >> (16 * (a & 1))) & 0xffffu) != 0);
                 tc::tmem_ld_wait();
+                tc::mbar_arrive(&k_empty[st]);  // S_g is here (so its MMA read K_g) and the bits were read
                 // masked cells -> -inf once: they drop out of the max and 2^(-inf) = 0 later
                 float sr[64];
 #pragma unroll
@@ -488,7 +504,11 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
 #pragma unroll
                     for (int c = 0; c < 16; ++c) {
                         const int cc = 16 * (a & 1) + c;
+#ifdef SF_EXPERIMENT_NO_MASK  // timing experiment only
+                        sr[16 * a + c] = __uint_as_float(rw[cc]) + 0.f * bw;
+#else
                         sr[16 * a + c] = mask_sel(bw, 1u << cc, __uint_as_float(rw[cc]));
+#endif
                     }
                 }
                 float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
@@ -539,8 +559,12 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
                     for (int c = 16 * a; c < 16 * a + 16; c += 2) {
                         const float2 arg = ffma2(make_float2(sr[c], sr[c + 1]), sl2x2, negm);
                         // the last kEmuPairs pairs of each group on the FMA pipe, the rest on MUFU
-                    const float2 pp = ((c >> 1) & 7) >= 8 - kEmuPairs ? ex2_emu2(arg)
-                                                                      : make_float2(ex2(arg.x), ex2(arg.y));
+#ifdef SF_EXPERIMENT_NO_EXP  // timing experiment only: exponentials replaced by the argument
+                        const float2 pp = arg;
+#else
+                        const float2 pp = ((c >> 1) & 7) >= 8 - kEmuPairs ? ex2_emu2(arg)
+                                                                          : make_float2(ex2(arg.x), ex2(arg.y));
+#endif
                         rs2[(c >> 1) & 1] = fadd2(rs2[(c >> 1) & 1], pp);
                         pk[c >> 1] = pack2<T>(pp.x, pp.y);
                     }
