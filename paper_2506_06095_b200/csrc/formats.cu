@@ -239,12 +239,14 @@ __global__ void load_tile_kernel(int32_t n_load, const int32_t* __restrict__ loa
 }
 
 // One warp per pool tile; lanes produce bytes of pack_bits(tile).
-__global__ void pool_write_kernel(const uint32_t* __restrict__ bits, Geo g, int32_t n_pool,
+// Launched for every part tile (an upper bound of the pool); the pool size is read on device, so
+// the build needs no host round trip between the dedup and the pool write.
+__global__ void pool_write_kernel(const uint32_t* __restrict__ bits, Geo g, const int32_t* __restrict__ n_pool_dev,
                                   const int32_t* __restrict__ pool_src,
                                   const int32_t* __restrict__ part_lin, int32_t tile_bytes,
                                   uint8_t* __restrict__ pool) {
     const int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    if (w >= n_pool) return;
+    if (w >= *n_pool_dev) return;
     const int lane = threadIdx.x & 31;
     const int64_t lin = part_lin[pool_src[w]];
     const int64_t br = lin / g.n_cols, bc = lin - br * g.n_cols;
@@ -347,9 +349,8 @@ extern "C" sf_status sf_bsr_build(const uint32_t* d_bits, int32_t seq_len, int32
     SF_LAUNCH_CHECK();
     row_count_kernel<<<g.n_rows, 256, 0, st>>>(cls, g, fcnt, pcnt, lcnt);
     SF_LAUNCH_CHECK();
-    SF_TRY(scan_exclusive(fcnt, fptr, g.n_rows, totals + 0, st));
-    SF_TRY(scan_exclusive(pcnt, pptr, g.n_rows, totals + 1, st));
-    SF_TRY(scan_exclusive(lcnt, lptr, g.n_rows, totals + 2, st));
+    scan_exclusive3_kernel<<<dim3(1, 3), 1024, 0, st>>>(fcnt, pcnt, lcnt, fptr, pptr, lptr, g.n_rows, totals);
+    SF_LAUNCH_CHECK();
     int32_t h_tot[3] = {0, 0, 0};
     SF_CUDA_TRY(cudaMemcpyAsync(h_tot, totals, 12, cudaMemcpyDeviceToHost, st));
     SF_CUDA_TRY(cudaStreamSynchronize(st));
@@ -375,9 +376,11 @@ extern "C" sf_status sf_bsr_build(const uint32_t* d_bits, int32_t seq_len, int32
     out->load_tile = carve<int32_t>(p, std::max(1, n_load));
     out->pool = carve<uint8_t>(p, imax64(1, static_cast<int64_t>(n_part) * tile_bytes));
     out->_alloc = ob;
-    SF_CUDA_TRY(cudaMemcpyAsync(out->full_row_ptr, fptr, rp * 4, cudaMemcpyDeviceToDevice, st));
-    SF_CUDA_TRY(cudaMemcpyAsync(out->part_row_ptr, pptr, rp * 4, cudaMemcpyDeviceToDevice, st));
-    SF_CUDA_TRY(cudaMemcpyAsync(out->load_row_ptr, lptr, rp * 4, cudaMemcpyDeviceToDevice, st));
+    // the three row-pointer arrays are carved identically (256-byte aligned, back to back) in the
+    // scratch and in the output block: one copy moves all three
+    SF_CUDA_TRY(cudaMemcpyAsync(out->full_row_ptr, fptr,
+                                static_cast<size_t>(reinterpret_cast<char*>(out->load_row_ptr) - reinterpret_cast<char*>(out->full_row_ptr)) + rp * 4,
+                                cudaMemcpyDeviceToDevice, st));
 
     // scratch 2: dedup
     uint32_t cap = 16;
@@ -415,15 +418,17 @@ extern "C" sf_status sf_bsr_build(const uint32_t* d_bits, int32_t seq_len, int32
         SF_LAUNCH_CHECK();
         tile_ids_kernel<<<blocks_for(n_part), 256, 0, st>>>(n_part, part_slot, slot_id, out->part_tile_ids);
         SF_LAUNCH_CHECK();
-        SF_CUDA_TRY(cudaMemcpyAsync(&n_pool, totals + 3, 4, cudaMemcpyDeviceToHost, st));
-        SF_CUDA_TRY(cudaStreamSynchronize(st));
-        pool_write_kernel<<<blocks_for(static_cast<int64_t>(n_pool) * 32), 256, 0, st>>>(
-            d_bits, g, n_pool, pool_src, part_lin, tile_bytes, out->pool);
+        pool_write_kernel<<<blocks_for(static_cast<int64_t>(n_part) * 32), 256, 0, st>>>(
+            d_bits, g, totals + 3, pool_src, part_lin, tile_bytes, out->pool);
         SF_LAUNCH_CHECK();
     }
     if (n_load > 0) {
         load_tile_kernel<<<blocks_for(n_load), 256, 0, st>>>(n_load, load_part, out->part_tile_ids, out->load_tile);
         SF_LAUNCH_CHECK();
+    }
+    if (n_part > 0) {  // the pool size for the host struct: the build's one trailing sync
+        SF_CUDA_TRY(cudaMemcpyAsync(&n_pool, totals + 3, 4, cudaMemcpyDeviceToHost, st));
+        SF_CUDA_TRY(cudaStreamSynchronize(st));
     }
     SF_CUDA_TRY(cudaFreeAsync(s2, st));
     SF_CUDA_TRY(cudaFreeAsync(s1, st));
