@@ -343,7 +343,9 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
                     }
                     if (lane == 0) {
                         const uint32_t ph = ((g / kStages) & 1) ^ 1;
+                        SF_TRACE(g, 4);
                         tc::mbar_wait(&k_empty[st], ph);
+                        SF_TRACE(g, 5);
 #pragma unroll
                         for (int gg = 0; gg < G; ++gg) s_kind[4 * st + gg] = tiles[gg];
                         tc::mbar_expect_tx(&k_full[st], kKVBytes + parts * TB);  // release: s_kind
@@ -358,7 +360,9 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
                                 tc::bulk_load(sMask + st * kMaskBytes + gg * TB,
                                               p.pool + static_cast<int64_t>(tiles[gg]) * TB, TB, &k_full[st]);
                         }
+                        SF_TRACE(g, 7);
                         tc::mbar_wait(&v_empty[st], ph);
+                        SF_TRACE(g, 11);
                         tc::mbar_expect_tx(&v_full[st], kKVBytes);
 #pragma unroll
                         for (int gg = 0; gg < G; ++gg)
