@@ -364,12 +364,17 @@ sf_status gemm_dispatch(const sf_gemm_args& a, cudaStream_t st) {
         const int64_t pair_ctas = 2 * ceil_div(a.M, 2 * BM) * ceil_div(a.N, 256);
         if (pair_ctas >= num_sms()) return gemm_pair_dispatch(a, ln, st);
     }
+    // small problems: 128-wide tiles when 256-wide ones would leave most SMs idle (twice the CTAs
+    // on a latency-bound GEMM, e.g. the M = 512 layers of cfg1)
+    const bool few = ceil_div(a.M, BM) * ceil_div(a.N, 256) < num_sms();
     if (ln) {
-        if (a.N % 256 == 0 && a.N / 256 <= kMaxCluster) return launch_gemm<T, 256, true>(a, st);
-        if (a.N % 128 == 0 && a.N / 128 <= kMaxCluster) return launch_gemm<T, 128, true>(a, st);
+        const bool fit256 = a.N % 256 == 0 && a.N / 256 <= kMaxCluster;
+        const bool fit128 = a.N % 128 == 0 && a.N / 128 <= kMaxCluster;
+        if (fit256 && !(few && fit128)) return launch_gemm<T, 256, true>(a, st);
+        if (fit128) return launch_gemm<T, 128, true>(a, st);
         return fail(SF_SHAPE_ERROR, "fused LayerNorm needs N % 128 == 0 and N <= 2048");
     }
-    if (a.N % 256 == 0) return launch_gemm<T, 256, false>(a, st);
+    if (a.N % 256 == 0 && !few) return launch_gemm<T, 256, false>(a, st);
     return launch_gemm<T, 128, false>(a, st);
 }
 
