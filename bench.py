@@ -531,6 +531,18 @@ def main():
     e2e_steps = max(4, min(args.steps, 100))
     e2e_run(4)
     torch.cuda.synchronize()
+    if os.environ.get("SF_E2E_PROBE"):  # diagnosis: repeated e2e windows in one process
+        for _ in range(6):
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record(s_in)
+            t_host = time.perf_counter()
+            e2e_run(e2e_steps)
+            t_enq = time.perf_counter() - t_host
+            s_out.wait_event(out_done[(e2e_steps - 1) % NB])
+            a1.record(s_out)
+            torch.cuda.synchronize()
+            print(f"e2e probe: {a0.elapsed_time(a1) / e2e_steps:.3f} ms/step (host enqueue {t_enq * 1e3 / e2e_steps:.3f} ms/step)",
+                  file=sys.stderr)
     if world > 1:
         torch.distributed.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
