@@ -336,6 +336,58 @@ def run_sweep(args):
 
 
 # ----------------------------------------------------------------------------------------------
+# cfg3 selector sweep: band width across the Eq. 1 boundary, both executors timed
+def run_band_sweep(args):
+    """BASELINE configs[2] (GPT-2 shapes, bs 8 x 12 heads x 64, n = 2048): sliding and causal-local
+    bands of width {1,2,4,8,16,24,32,48,64} (Eq. 1 turns row-wise at w <= 16 sliding /
+    w <= 48 causal-local). For each: Eq. 1's threshold, the reference-mode and B200-mode plans, and
+    the measured time of BOTH executors, so the selector's choice can be checked against the
+    faster one (regret = chosen / best)."""
+    import torch
+    from paper_2506_06095_b200 import sparsefuse as sf
+    torch.cuda.set_device(0)
+    bs, h, n, d = 8, 12, 2048, 64
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    g = torch.Generator(device="cuda").manual_seed(1)
+    q, k, v = ((torch.rand(bs, h, n, d, device="cuda", generator=g) * 2 - 1).half() for _ in range(3))
+    o = torch.empty_like(q)
+
+    def timed(fn):
+        st = torch.cuda.Stream()
+        st.wait_stream(torch.cuda.current_stream())
+        for _ in range(2):
+            fn(None)
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr, stream=st):
+            fn(st)
+        ts = []
+        for _ in range(max(5, args.steps)):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(); gr.replay(); b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b) * 1e3)
+        return statistics.median(ts)
+
+    for pat in ("sliding", "causal_local"):
+        for w in (1, 2, 4, 8, 16, 24, 32, 48, 64):
+            dm = sf.generate_mask([dict(pattern=pat, seq_len=n, band_width=w)])
+            ref_plan = sf.select_plan(dm, sf.hw_preset("b200"), n, h, bs, d, mode="reference")
+            b200_plan = sf.select_plan(dm, sf.hw_preset("b200"), n, h, bs, d, mode="b200")
+            bsr = sf.build_bsr(dm, 128, 16)
+            rw = sf.build_rowwise(dm)
+            t_bw = timed(lambda s_: sf.block_sparse_sdpa(q, k, v, bsr, out=o, stream=s_))
+            t_rw = timed(lambda s_: sf.rowwise_sdpa(q, k, v, rw, out=o, stream=s_))
+            best = min(t_bw, t_rw)
+            chosen = lambda pl: t_bw if pl.kind == "block_wise" else t_rw
+            print(json.dumps({"band_sweep": pat, "seq_len": n, "band": w, "bs": bs, "heads": h, "nnz": dm.true_count(),
+                              "eq1_threshold": ref_plan.threshold, "reference_plan": ref_plan.kind,
+                              "b200_plan": b200_plan.kind, "blockwise_us": t_bw, "rowwise_us": t_rw,
+                              "regret_reference_mode": chosen(ref_plan) / best,
+                              "regret_b200_mode": chosen(b200_plan) / best}), flush=True)
+
+
+# ----------------------------------------------------------------------------------------------
 # format builders (A1-A4, A9): device latency vs the reference's own builders on the host
 def run_formats(args):
     """Device latency (CUDA events around the C-ABI call, warm, median of --steps) of mask
@@ -411,7 +463,10 @@ def main():
     ap.add_argument("--seqs", default="", help="--sweep: comma list (default: 128..8192)")
     ap.add_argument("--both", action="store_true", help="--sweep: also time the executor the plan did not pick")
     ap.add_argument("--formats", action="store_true", help="format-builder latency (A1-A4, A9) vs the reference")
+    ap.add_argument("--band-sweep", action="store_true", help="cfg3 selector sweep: both executors across Eq. 1")
     args = ap.parse_args()
+    if args.band_sweep:
+        return run_band_sweep(args)
     if args.sweep:
         return run_sweep(args)
     if args.formats:

@@ -140,16 +140,20 @@ __device__ __forceinline__ float2 f2fma(float2 a, float2 b, float2 c) {
     return d;
 }
 
-template <typename T>
+// RPW = rows per warp: 1 -> the four groups split one row's keys and merge at the end; 4 -> each
+// group owns a row (short rows: no idle groups, no merge, a quarter of the warps).
+template <typename T, int RPW>
 __global__ void __launch_bounds__(256) attn_rowwise64_kernel(sf_attn_args a, const int32_t* __restrict__ row_ptr,
                                                              const int32_t* __restrict__ col_idx) {
     constexpr float kLazy = 8.0f;
+    constexpr int kStride = RPW == 1 ? 4 : 1;  // key stride of one group
     const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int64_t rows = static_cast<int64_t>(a.bs) * a.h * a.seq_len;
-    if (gw >= rows) return;
     const int lane = threadIdx.x & 31, grp = lane >> 3, gl = lane & 7;
-    const int64_t i = gw % a.seq_len;
-    const int64_t bh = gw / a.seq_len;
+    const int64_t row_id = RPW == 1 ? gw : gw * 4 + grp;
+    if (row_id >= rows) return;  // RPW 4: a whole group leaves (its shuffles are group-local)
+    const int64_t i = row_id % a.seq_len;
+    const int64_t bh = row_id / a.seq_len;
     const int64_t b = bh / a.h, hh = bh % a.h;
     const int64_t base = b * a.q_sb + hh * a.q_sh + gl * 8;
     const T* Q = static_cast<const T*>(a.q) + base;
@@ -171,13 +175,13 @@ __global__ void __launch_bounds__(256) attn_rowwise64_kernel(sf_attn_args a, con
     // kNK keys per group in flight: all column indices, then all K and V rows are requested before
     // any is used (the loop is bound by dependent gather latency, not by arithmetic)
     constexpr int kNK = 4;
-    for (int32_t kk = r0 + grp; kk < r1; kk += 4 * kNK) {
+    for (int32_t kk = r0 + (RPW == 1 ? grp : 0); kk < r1; kk += kStride * kNK) {
         int64_t jj[kNK];
         bool live[kNK];
 #pragma unroll
         for (int t = 0; t < kNK; ++t) {
-            live[t] = kk + 4 * t < r1;  // group-uniform
-            jj[t] = live[t] ? col_idx[kk + 4 * t] : 0;
+            live[t] = kk + kStride * t < r1;  // group-uniform
+            jj[t] = live[t] ? col_idx[kk + kStride * t] : 0;
         }
         uint4 kr[kNK], vr[kNK];
 #pragma unroll
@@ -222,7 +226,7 @@ __global__ void __launch_bounds__(256) attn_rowwise64_kernel(sf_attn_args a, con
     }
     // merge the 4 groups (lanes gl, gl+8, gl+16, gl+24 hold the same dims)
 #pragma unroll
-    for (int o = 8; o < 32; o <<= 1) {
+    for (int o = 8; o < 32 && RPW == 1; o <<= 1) {
         const float m2 = __shfl_xor_sync(0xffffffffu, m, o);
         const float l2 = __shfl_xor_sync(0xffffffffu, l, o);
         const float mn = fmaxf(m, m2);
@@ -237,7 +241,7 @@ __global__ void __launch_bounds__(256) attn_rowwise64_kernel(sf_attn_args a, con
         l = l * a1 + l2 * a2;
         m = mn;
     }
-    if (grp == 0) {
+    if (RPW == 4 || grp == 0) {
         const float inv = l > 0.f ? 1.f / l : 0.f;  // rows without valid columns stay zero
         T* O = static_cast<T*>(a.o) + b * a.o_sb + hh * a.o_sh + i * a.o_sn + gl * 8;
         uint4 u;
@@ -351,9 +355,16 @@ sf_status rowwise_dispatch(const sf_attn_args& a, const sf_csr_dev& c, cudaStrea
                      (reinterpret_cast<uintptr_t>(a.k) % 16 == 0) && (reinterpret_cast<uintptr_t>(a.v) % 16 == 0);
     if (d == 64 && vec && a.o_sn % 8 == 0 && reinterpret_cast<uintptr_t>(a.o) % 16 == 0 &&
         reinterpret_cast<uintptr_t>(a.q) % 16 == 0) {
-        const int64_t warps = static_cast<int64_t>(a.bs) * a.h * a.seq_len;
-        attn_rowwise64_kernel<T><<<static_cast<unsigned>(ceil_div(warps * 32, 256)), 256, 0, st>>>(a, c.row_ptr,
-                                                                                                 c.col_idx);
+        const int64_t rows = static_cast<int64_t>(a.bs) * a.h * a.seq_len;
+        // short rows (<= 32 keys on average): one 8-lane group per row
+        if (c.nnz <= 32ll * a.seq_len) {
+            const int64_t warps = ceil_div(rows, 4);
+            attn_rowwise64_kernel<T, 4><<<static_cast<unsigned>(ceil_div(warps * 32, 256)), 256, 0, st>>>(a, c.row_ptr,
+                                                                                                      c.col_idx);
+        } else {
+            attn_rowwise64_kernel<T, 1><<<static_cast<unsigned>(ceil_div(rows * 32, 256)), 256, 0, st>>>(a, c.row_ptr,
+                                                                                                     c.col_idx);
+        }
         SF_LAUNCH_CHECK();
         return SF_OK;
     }

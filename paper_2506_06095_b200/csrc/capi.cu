@@ -29,12 +29,15 @@ sf_status attn_tc(const sf_attn_args& a, const sf_bsr_dev& b, cudaStream_t st, b
 
 namespace {
 
-// B200 executor throughputs measured by `bench.py --sweep --both` (profiles/r01/sweep_both.jsonl):
-// the tcgen05 block executor retires ~1.5-2.3e12 executed cells/s (cells of the loaded 128x16
-// tiles), the row-wise gather ~3.5e10 valid cells/s; ~10 us launch + prologue floor for either.
-constexpr double kBlockCellsPerUs = 1.6e6;
-constexpr double kRowNnzPerUs = 3.5e4;
-constexpr double kLaunchFloorUs = 10.0;
+// B200 executor cost model, fitted to `bench.py --sweep --both` and `--band-sweep`
+// (profiles/r01/sweep_mha_both_v2.jsonl, band_sweep_v1.jsonl): the persistent tcgen05 block
+// executor has a ~25 us floor and retires ~1.8e12 executed cells/s (cells of the loaded 128x16
+// tiles); the row-wise gather has a ~10 us floor, a per-row cost (0.2 ns with one 8-lane group
+// per row when rows average <= 32 keys, 0.65 ns with a warp per row) and ~6e10 valid cells/s.
+constexpr double kBlockCellsPerUs = 1.8e6;
+constexpr double kBlockFloorUs = 25.0;
+constexpr double kRowNnzPerUs = 6.0e4;
+constexpr double kRowFloorUs = 10.0;
 
 double threshold_from_loads(int32_t n, int64_t loads16, double tau) {
     // planner.hpp:67-76: L / N^2 - tau / (log2 N)^2 with N = ceil(n/16)
@@ -201,8 +204,8 @@ extern "C" sf_status sf_select_plan(const uint32_t* d_bits, const sf_hw_spec* hw
     if (mode == SF_PLAN_B200 && out->kind == SF_ROW_WISE && seq_len > 16 && head_size == 64) {
         // B200 calibration of the Eq. 1 decision: Eq. 1 assumes a row-wise
         // executor that is competitive per valid cell. On B200 the tcgen05 block executor runs
-        // ~50x more cells per second than the CUDA-core row-wise gather (profiles/r01 sweep), so
-        // a row-wise plan is kept only while the predicted block-wise time is not < half of it.
+        // ~30x more cells per second than the CUDA-core row-wise gather, so a row-wise plan is
+        // kept only while the fitted cost model above predicts it faster.
         sf_bsr_dev b{};
         SF_TRY(sf_bsr_build(d_bits, static_cast<int32_t>(seq_len), 128, 16, &b, stream));
         const int64_t n_load = b.n_load;
@@ -210,9 +213,11 @@ extern "C" sf_status sf_select_plan(const uint32_t* d_bits, const sf_hw_spec* hw
         int64_t nnz = 0;
         SF_TRY(sf_mask_count(d_bits, static_cast<int32_t>(seq_len), &nnz, stream));
         const double slices = static_cast<double>(bs) * h;
-        const double t_bw = kLaunchFloorUs + static_cast<double>(n_load) * 128.0 * 16.0 * slices / kBlockCellsPerUs;
-        const double t_rw = kLaunchFloorUs + static_cast<double>(nnz) * slices / kRowNnzPerUs;
-        if (t_bw < 0.5 * t_rw) {
+        const double rows = slices * static_cast<double>(seq_len);
+        const double per_row_us = nnz <= 32 * seq_len ? 0.0002 : 0.00065;
+        const double t_bw = kBlockFloorUs + static_cast<double>(n_load) * 128.0 * 16.0 * slices / kBlockCellsPerUs;
+        const double t_rw = kRowFloorUs + rows * per_row_us + static_cast<double>(nnz) * slices / kRowNnzPerUs;
+        if (t_bw < t_rw) {
             out->kind = SF_BLOCK_WISE;
             out->block_m = 128;
             out->block_n = 16;
