@@ -10,7 +10,8 @@
 //              rows of G = 64/block_n load-list column blocks, GATHERED into one contiguous 64-key
 //              stage (4-D tensor maps over (d, n, h, b) read Q/K/V in any (b,h,i) stride layout in
 //              place, e.g. the fused-QKV activation), the packed bit tiles of the step's PART tiles
-//              bulk-copied from the BSR pool (full tiles need no bits) and the step's tile kinds.
+//              bulk-copied from the BSR pool; full / padding tiles' bit rows are
+//              filled with ones / zeros by the producer lanes (no per-tile branches in the softmax).
 //              kStages-deep ring, one transaction barrier per stage.
 //   warp 1     TMEM allocator + MMA issuer (one elected thread):
 //                S_j = Q K_j^T   tcgen05.mma (SS) M=128 N=64 K=16 x4 -> TMEM S[j%2] (fp32)
@@ -237,12 +238,11 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
     unsigned char* sK = sQ + 2 * kQBytes;
     unsigned char* sV = sK + kStages * kKVBytes;
     unsigned char* sMask = sV + kStages * kKVBytes;        // [kStages][BM * 8 B]: packed part-tile bits
-    int32_t* s_kind = reinterpret_cast<int32_t*>(sMask + kStages * kMaskBytes);  // [kStages][4]
-    int32_t* s_order = s_kind + 4 * kStages;                                      // [kMaxRowBlocks]
+    int32_t* s_order = reinterpret_cast<int32_t*>(sMask + kStages * kMaskBytes) + 4 * kStages;  // [kMaxRowBlocks]
     uint64_t* bars = reinterpret_cast<uint64_t*>(s_order + kMaxRowBlocks);
     uint64_t* q_full = bars;                  // [2]
     uint64_t* q_empty = q_full + 2;           // [2]
-    // K (with the stage's part-tile bits and kinds) and V have separate barriers: a K slot is
+    // K (with the stage's bit rows) and V have separate barriers: a K slot is
     // released as soon as the softmax holds S of that step (and read its bits), a V slot when
     // P.V of that step is done, so K loads run about a step further ahead than V loads
     uint64_t* k_full = q_empty + 2;           // [kStages]
@@ -341,14 +341,30 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
                         tiles[gg] = __shfl_sync(0xffffffffu, my_tile, j * G + gg - c);
                         parts += tiles[gg] >= 0;
                     }
+                    const uint32_t ph = ((g / kStages) & 1) ^ 1;
                     if (lane == 0) {
-                        const uint32_t ph = ((g / kStages) & 1) ^ 1;
                         SF_TRACE(g, 4);
                         tc::mbar_wait(&k_empty[st], ph);
                         SF_TRACE(g, 5);
+                    }
+                    __syncwarp();
+                    // the stage's bit rows of full (all ones) and padding (zero) tiles are written
+                    // here, so the softmax reads every tile's bits the same way, without branches;
+                    // part tiles' rows arrive by bulk copy from the pool
 #pragma unroll
-                        for (int gg = 0; gg < G; ++gg) s_kind[4 * st + gg] = tiles[gg];
-                        tc::mbar_expect_tx(&k_full[st], kKVBytes + parts * TB);  // release: s_kind
+                    for (int gg = 0; gg < G; ++gg) {
+                        if (tiles[gg] < 0) {
+                            const uint32_t fv = tiles[gg] == -1 ? ~0u : 0u;
+                            for (int c16 = static_cast<int>(lane); c16 < TB / 16; c16 += 32)
+                                asm volatile("st.shared.v4.b32 [%0], {%1, %1, %1, %1};" ::"r"(
+                                                 tc::smem_u32(sMask + st * kMaskBytes + gg * TB + 16 * c16)),
+                                             "r"(fv)
+                                             : "memory");
+                        }
+                    }
+                    __syncwarp();
+                    if (lane == 0) {
+                        tc::mbar_expect_tx(&k_full[st], kKVBytes + parts * TB);  // release: the filled bit rows
 #pragma unroll
                         for (int gg = 0; gg < G; ++gg) {
                             const int col = cols[gg] * BN;
@@ -443,7 +459,6 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
         const int my_head = kPair ? static_cast<int>(lane >> 4) : 0;
         const uint32_t trow = tmem + ((q * 32) << 16);
         const float sl2 = p.scale_log2;
-        const uint32_t kind_a = tc::smem_u32(s_kind);
         int g = 0;
         for (int k = 0; k < nitems; ++k) {
             int rb, bh, l0, L, nsteps;
@@ -456,36 +471,21 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
                 if (tr) SF_TRACE(j, 0);
                 tc::mbar_wait(&k_full[st], (g / kStages) & 1);
                 if (tr) SF_TRACE(j, 1);
-                // this row's 64 mask bits: full tile -> ones, part tile -> its staged pool row,
-                // padding -> 0
+                // this row's 64 mask bits (the producer staged every tile's rows: full -> ones,
+                // part -> its pool rows, padding -> 0)
                 uint32_t bits[2];
                 {
-                    const int4 kd = lds_v4(kind_a + 16u * st);
-                    const int kinds[4] = {kd.x, kd.y, kd.z, kd.w};
                     const uint32_t mb = tc::smem_u32(sMask + st * kMaskBytes);
                     if constexpr (BN == 16) {
 #pragma unroll
-                        for (int w = 0; w < 2; ++w) {
-                            uint32_t v = 0;
-#pragma unroll
-                            for (int gg = 0; gg < 2; ++gg) {
-                                const int t = kinds[2 * w + gg];
-                                const uint32_t b16 =
-                                    t == -1 ? 0xffffu : (t >= 0 ? lds_u16(mb + (2 * w + gg) * TB + r * 2) : 0u);
-                                v |= b16 << (16 * gg);
-                            }
-                            bits[w] = v;
-                        }
+                        for (int w = 0; w < 2; ++w)
+                            bits[w] = lds_u16(mb + (2 * w) * TB + r * 2) | (lds_u16(mb + (2 * w + 1) * TB + r * 2) << 16);
                     } else if constexpr (BN == 32) {
 #pragma unroll
-                        for (int w = 0; w < 2; ++w) {
-                            const int t = kinds[w];
-                            bits[w] = t == -1 ? ~0u : (t >= 0 ? lds_u32(mb + w * TB + r * 4) : 0u);
-                        }
+                        for (int w = 0; w < 2; ++w) bits[w] = lds_u32(mb + w * TB + r * 4);
                     } else {
-                        const int t = kinds[0];
 #pragma unroll
-                        for (int w = 0; w < 2; ++w) bits[w] = t == -1 ? ~0u : (t >= 0 ? lds_u32(mb + r * 8 + 4 * w) : 0u);
+                        for (int w = 0; w < 2; ++w) bits[w] = lds_u32(mb + r * 8 + 4 * w);
                     }
                 }
                 tc::mbar_wait(&s_full[sb], (g / kSBuf) & 1);

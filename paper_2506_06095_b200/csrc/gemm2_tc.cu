@@ -72,8 +72,8 @@ __global__ void __launch_bounds__(Cfg2<LN>::THREADS, 1) gemm2_kernel(const __gri
     uint64_t* tfull = empty + C::STAGES;  // [2]
     uint64_t* tempty = tfull + 2;        // [2] (leader's are used)
     uint64_t* lnb = tempty + 2;          // [2 parity]
-    uint64_t* abar = lnb + 4;            // [EPI_WARPS]: residual box landed
-    uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(abar + C::EPI_WARPS);
+    uint64_t* abar = lnb + 4;            // [EPI_WARPS][2]: residual box landed
+    uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(abar + 2 * C::EPI_WARPS);
     float* red = reinterpret_cast<float*>(smem + C::STAGES * (C::A_BYTES + C::B_BYTES) + C::STG_BYTES + C::BAR_BYTES);
 
     pdl_enter();
@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(Cfg2<LN>::THREADS, 1) gemm2_kernel(const __gri
         }
         if (LN)  // one arrive per epilogue warp of every CTA holding these rows
             for (int b = 0; b < 2; ++b) tc::mbar_init(&lnb[b], C::EPI_WARPS * nct);
-        for (int w = 0; w < C::EPI_WARPS; ++w) tc::mbar_init(&abar[w], 1);
+        for (int w = 0; w < 2 * C::EPI_WARPS; ++w) tc::mbar_init(&abar[w], 1);
         tc::fence_barrier_init();
     }
     if (warp == 1) tc::tmem_alloc2<C::TMEM_COLS>(tmem_ptr);
@@ -211,7 +211,7 @@ __global__ void __launch_bounds__(Cfg2<LN>::THREADS, 1) gemm2_kernel(const __gri
         // this warp's staging boxes (box 0: residual in / output out; box 1: LN out_pre_ln)
         unsigned char* const boxp = sStg + (warp - 4) * (C::NBOX * 2048u);
         const uint32_t box = tc::smem_u32(boxp);
-        uint64_t* const my_abar = &abar[warp - 4];
+        uint64_t* const my_abar = &abar[2 * (warp - 4)];
         uint32_t aph = 0;
         auto aux_issue = [&](int col, int row0) {  // lane 0: residual box -> box 0 once its last store read it
             if (lane == 0) {
@@ -280,15 +280,31 @@ __global__ void __launch_bounds__(Cfg2<LN>::THREADS, 1) gemm2_kernel(const __gri
                 if (warp == 4 && lane == 0) GTRACE(i, 6);
             } else {
                 // LayerNorm over the row split across nct CTAs x GROUPS warps: each thread owns
-                // one row and 128 columns. Pass 1: x = acc + bias + aux back into TMEM, local sum;
-                // pass 2: local M2 about the local mean; one exchange of (mean, M2) partials and a
-                // Chan combination (numerically the two-pass variance); pass 3: normalise, store.
+                // one row and CPT chunks of 32 columns. Pass 1 below; then one exchange of (mean,
+                // M2) partials and a Chan combination (numerically the two-pass variance); pass 3:
+                // normalise, store.
                 const int par = i & 1;
                 const uint32_t my_y = rank >> 1;
-                constexpr float kCols = 32.f * (CHUNKS / GROUPS);
-                float sum = 0.f;
-                for (int c = c_begin; c < c_end; ++c) {
-                    if (p.aux) aux_issue(n0 + c * 32, row0);
+                // pass 1, per 32-column chunk: x = acc + bias (+act) + residual back into TMEM and
+                // the chunk's (mean, M2) from registers; the chunks combine by Chan's formula, so
+                // no second TMEM pass is needed for the variance. The residual boxes are double-
+                // buffered: chunk c+1's load flies while c is added.
+                constexpr int CPT = CHUNKS / GROUPS;
+                uint32_t bph[2] = {0u, 0u};
+                auto res_issue = [&](int b_, int col) {
+                    __syncwarp();  // every lane's reads of the box are done
+                    if (lane == 0) {
+                        tc::bulk_wait_read<0>();
+                        tc::mbar_expect_tx(&my_abar[b_], 2048);
+                        tc::tma_load_2d(boxp + b_ * 2048, &p.taux, &my_abar[b_], col, row0);
+                    }
+                };
+                if (p.aux) res_issue(0, n0 + c_begin * 32);
+                float cmean[CPT], cm2[CPT];
+#pragma unroll
+                for (int cc = 0; cc < CPT; ++cc) {
+                    const int c = c_begin + cc;
+                    if (p.aux && cc + 1 < CPT) res_issue((cc + 1) & 1, n0 + (c + 1) * 32);
                     tc::tmem_ld32(taddr + c * 32, r);
                     tc::tmem_ld_wait();
                     const float4* b4 = reinterpret_cast<const float4*>(sprm + c * 32);
@@ -304,29 +320,52 @@ __global__ void __launch_bounds__(Cfg2<LN>::THREADS, 1) gemm2_kernel(const __gri
 #pragma unroll
                         for (int j = 0; j < 32; ++j) x[j] = act_fn(x[j], p.act);
                     }
-                    if (p.aux) aux_add(x);
+                    if (p.aux) {
+                        const int b_ = cc & 1;
+                        tc::mbar_wait(&my_abar[b_], bph[b_]);
+                        bph[b_] ^= 1u;
+                        const uint32_t bx = box + b_ * 2048u;
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            uint4 u;
+                            const uint32_t ad = bx + lane * 64u + ((static_cast<uint32_t>(j) ^ ((lane >> 1) & 3)) << 4);
+                            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                                         : "=r"(u.x), "=r"(u.y), "=r"(u.z), "=r"(u.w) : "r"(ad));
+                            const T* h = reinterpret_cast<const T*>(&u);
+#pragma unroll
+                            for (int e = 0; e < 8; ++e) x[8 * j + e] += DT<T>::to_f(h[e]);
+                        }
+                    }
                     float s4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
                     for (int j = 0; j < 32; ++j) {
                         s4[j & 3] += x[j];
                         r[j] = __float_as_uint(x[j]);
                     }
-                    sum += (s4[0] + s4[1]) + (s4[2] + s4[3]);
                     tc::tmem_st32(taddr + c * 32, r);
-                }
-                tc::tmem_st_wait();
-                const float lmean = sum / kCols;
-                float m4[4] = {0.f, 0.f, 0.f, 0.f};
-                for (int c = c_begin; c < c_end; ++c) {
-                    tc::tmem_ld32(taddr + c * 32, r);
-                    tc::tmem_ld_wait();
+                    const float mc = ((s4[0] + s4[1]) + (s4[2] + s4[3])) * (1.f / 32.f);
+                    float q4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
                     for (int j = 0; j < 32; ++j) {
-                        const float d = __uint_as_float(r[j]) - lmean;
-                        m4[j & 3] = fmaf(d, d, m4[j & 3]);
+                        const float d = x[j] - mc;
+                        q4[j & 3] = fmaf(d, d, q4[j & 3]);
                     }
+                    cmean[cc] = mc;
+                    cm2[cc] = (q4[0] + q4[1]) + (q4[2] + q4[3]);
                 }
-                const float2 mine = make_float2(lmean, (m4[0] + m4[1]) + (m4[2] + m4[3]));
+                tc::tmem_st_wait();
+                float lmean = 0.f;
+#pragma unroll
+                for (int cc = 0; cc < CPT; ++cc) lmean += cmean[cc];
+                lmean *= 1.f / CPT;
+                float lm2 = 0.f;
+#pragma unroll
+                for (int cc = 0; cc < CPT; ++cc) {
+                    const float d = cmean[cc] - lmean;
+                    lm2 += cm2[cc] + 32.f * d * d;
+                }
+                constexpr float kCols = 32.f * CPT;
+                const float2 mine = make_float2(lmean, lm2);
                 // exchange: every lane writes its row's partial into each row-sharing CTA, then one
                 // arrive per warp and peer (release.cluster after the warp's stores)
                 float2* slot = part + par * (kMaxNct * 2 * BM);
@@ -354,13 +393,17 @@ __global__ void __launch_bounds__(Cfg2<LN>::THREADS, 1) gemm2_kernel(const __gri
                     m2 += v.y + kCols * d * d;
                 }
                 const float inv = 1.0f / sqrtf(m2 / static_cast<float>(p.N) + kLnEps);
-                float y[32];
-                for (int c = c_begin; c < c_end; ++c) {
-                    __syncwarp();
-                    tc::tmem_ld32(taddr + c * 32, r);
-                    tc::tmem_ld_wait();
-                    if (c == c_end - 1) release(acc);
+                // pass 3: normalise and store; the next chunk's TMEM load is in flight while this
+                // chunk is staged, and the two boxes alternate so a store only waits for the one
+                // before last (out_pre_ln: both boxes per chunk)
+                tc::tmem_ld32(taddr + c_begin * 32, r);
+#pragma unroll
+                for (int cc = 0; cc < CPT; ++cc) {
+                    const int c = c_begin + cc;
                     const int col = n0 + c * 32;
+                    tc::tmem_ld_wait();
+                    if (cc == CPT - 1) release(acc);
+                    float y[32];
                     const float4* g4 = reinterpret_cast<const float4*>(sprm + BN2 + c * 32);
                     const float4* e4 = reinterpret_cast<const float4*>(sprm + 2 * BN2 + c * 32);
 #pragma unroll
@@ -375,8 +418,17 @@ __global__ void __launch_bounds__(Cfg2<LN>::THREADS, 1) gemm2_kernel(const __gri
                         y[4 * j + 2] = (x[4 * j + 2] - mean) * inv * g.z + e.z;
                         y[4 * j + 3] = (x[4 * j + 3] - mean) * inv * g.w + e.w;
                     }
-                    store_box(0, &p.tc, y, col, row0, false);
-                    if (p.out_pre_ln) store_box(1, &p.tpre, x, col, row0, true);
+                    if (cc + 1 < CPT) {
+                        __syncwarp();
+                        tc::tmem_ld32(taddr + (c + 1) * 32, r);
+                    }
+                    if (p.out_pre_ln) {
+                        store_box(0, &p.tc, y, col, row0, false);
+                        store_box(1, &p.tpre, x, col, row0, true);
+                    } else {
+                        if (lane == 0) tc::bulk_wait_read<1>();
+                        store_box(cc & 1, &p.tc, y, col, row0, true);
+                    }
                 }
             }
         }

@@ -18,7 +18,7 @@ L.sf_debug_gemm_trace.argtypes = [C.c_void_p]
 M = 16384
 ln = lambda N: {"ln_gamma": torch.rand(N, device="cuda") + 0.5, "ln_beta": torch.rand(N, device="cuda") - 0.5}
 for name, N, K, kw in (("qkv", 2304, 768, {}), ("ffn1_gelu", 3072, 768, {"act": "gelu"}),
-                       ("ffn2", 768, 3072, {}), ("out_ln", 768, 768, ln(768)), ("ffn2_ln", 768, 3072, ln(768))):
+                       ("ffn2", 768, 3072, {}), ("out_ln", 768, 768, ln(768)), ("out_ln_aux", 768, 768, {**ln(768), "aux": torch.randn(M, 768, device="cuda").half()}), ("ffn2_ln", 768, 3072, ln(768))):
     x = torch.randn(M, K, device="cuda").half()
     w = (torch.randn(N, K, device="cuda") * 0.02).half()
     b = torch.randn(N, device="cuda")
