@@ -35,9 +35,21 @@ constexpr int kMaxNct = 4;  // LN cluster 2 x nct <= 8 CTAs (portable cluster si
     do {                                                                                           \
         if (p.trace && blockIdx.y == 0 && px == 0 && (i) < 64) p.trace[(i) * 8 + (ev)] = clock64(); \
     } while (0)
+// per-CTA globaltimer (ns): entry, after the PDL wait, before teardown, cluster arrive, cluster wait
+#define GSPAN(ev)                                                                                       \
+    do {                                                                                                \
+        if (p.trace && threadIdx.x == 0) {                                                              \
+            unsigned long long t_;                                                                      \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                      \
+            p.trace[512 + 8 * (blockIdx.y * gridDim.x + blockIdx.x) + (ev)] = t_;                      \
+        }                                                                                               \
+    } while (0)
 #else
 #define GTRACE(i, ev) \
     do {              \
+    } while (0)
+#define GSPAN(ev) \
+    do {          \
     } while (0)
 #endif
 
@@ -76,7 +88,12 @@ __global__ void __launch_bounds__(Cfg2<LN>::THREADS, 1) gemm2_kernel(const __gri
     uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(abar + 2 * C::EPI_WARPS);
     float* red = reinterpret_cast<float*>(smem + C::STAGES * (C::A_BYTES + C::B_BYTES) + C::STG_BYTES + C::BAR_BYTES);
 
+    GSPAN(0);
+#ifdef SF_GEMM_TRACE
+    const long long c_entry = clock64();
+#endif
     pdl_enter();
+    GSPAN(1);
     const uint32_t warp = tc::warp_id();
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t rank = tc::cluster_rank();
@@ -436,7 +453,22 @@ __global__ void __launch_bounds__(Cfg2<LN>::THREADS, 1) gemm2_kernel(const __gri
     if (warp >= 4 && lane == 0) tc::bulk_wait<0>();  // staged stores done before smem goes away
     tc::fence_before_sync();
     __syncthreads();
-    tc::cluster_sync_all();  // the peer's MMAs / remote arrives are done before TMEM goes away
+    GSPAN(2);
+#ifdef SF_GEMM_TRACE
+    {
+        const long long c0 = clock64();
+        asm volatile("barrier.cluster.arrive.release;" ::: "memory");
+        const long long c1 = clock64();
+        GSPAN(3);
+        if (p.trace && threadIdx.x == 0) p.trace[512 + 8 * (blockIdx.y * gridDim.x + blockIdx.x) + 5] = c1 - c0;
+        if (p.trace && threadIdx.x == 128) p.trace[512 + 8 * (blockIdx.y * gridDim.x + blockIdx.x) + 6] = c1 - c0;
+    }
+    asm volatile("barrier.cluster.wait.acquire;" ::: "memory");
+    GSPAN(4);
+    if (p.trace && threadIdx.x == 0) p.trace[512 + 8 * (blockIdx.y * gridDim.x + blockIdx.x) + 7] = clock64() - c_entry;
+#else
+    tc::cluster_sync_all();
+#endif  // the peer's MMAs / remote arrives are done before TMEM goes away
     if (warp == 1) tc::tmem_dealloc2<C::TMEM_COLS>(tmem);
 }
 

@@ -25,12 +25,20 @@ for name, N, K, kw in (("qkv", 2304, 768, {}), ("ffn1_gelu", 3072, 768, {"act": 
     out = torch.empty(M, N, device="cuda").half()
     for _ in range(3):
         fused.gemm_fused(x, w, out, bias=b, tile_n=fused.TILE_PAIR, **kw)
-    buf = torch.zeros(64 * 8, dtype=torch.int64, device="cuda")
+    buf = torch.zeros(64 * 8 + 8 * 1024, dtype=torch.int64, device="cuda")
     L.sf_debug_gemm_trace(buf.data_ptr())
     fused.gemm_fused(x, w, out, bias=b, tile_n=fused.TILE_PAIR, **kw)
     torch.cuda.synchronize()
     L.sf_debug_gemm_trace(None)
-    t = buf.view(64, 8).cpu().numpy().astype("int64")
+    allb = buf.cpu().numpy().astype("int64")
+    sp = allb[512:].reshape(-1, 8)[:, 1:3]
+    sp = sp[sp[:, 0] > 0]
+    if len(sp):
+        t0s, dur = sp[:, 0].min(), (sp[:, 1] - sp[:, 0]) / 1e3
+        print(f"{name}: {len(sp)} CTAs, start spread {(sp[:, 0].max() - t0s) / 1e3:.1f} us, "
+              f"span min/median/max {dur.min():.1f}/{sorted(dur)[len(dur) // 2]:.1f}/{dur.max():.1f} us, "
+              f"last end {(sp[:, 1].max() - t0s) / 1e3:.1f} us")
+    t = allb[:512].reshape(64, 8)
     t0 = t[0, 0]
     print(f"{name}: M={M} N={N} K={K}  (cycles from tile 0 producer start)")
     prev = None
