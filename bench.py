@@ -499,6 +499,14 @@ def main():
     g = torch.Generator(device="cuda").manual_seed(7 + rank)
     x = (torch.rand(s.rows, s.hidden, device="cuda", generator=g) * 2 - 1).half()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
+    clean = torch.zeros(256 << 20, dtype=torch.uint8, device="cuda")
+
+    def l2_flush():
+        # write a buffer larger than L2 (evicts everything the previous step left), then read
+        # another one, so the flush's own dirty lines are written back here, outside the step
+        # events, instead of inside the next step: the step starts from a cold, clean L2
+        flush.zero_()
+        clean.max()
 
     for _ in range(args.warmup):
         L.forward(x)
@@ -521,7 +529,7 @@ def main():
     with ClockSampler(0 if shared else local) as clk:
         time.sleep(0.3)  # the sampler's first reading lands inside the timed region
         for a, b in evs:
-            flush.zero_()
+            l2_flush()
             a.record()
             L.replay()
             b.record()
@@ -529,7 +537,7 @@ def main():
         # per-kernel device times: the same K steps again through the instrumented graph (event
         # nodes between the launches cost ~1 us each, so the headline above runs without them)
         for _ in range(args.steps):
-            flush.zero_()
+            l2_flush()
             L.replay(timed=True)
             torch.cuda.synchronize()
             for k, v in L.kernel_ms().items():
@@ -643,7 +651,7 @@ def main():
             "config": {"workload": cfg["desc"], "model": cfg["model"], "global_batch": cfg["bs"] * world,
                        "seq_len": cfg["seq"], "hidden": cfg["hidden"], "heads": cfg["heads"],
                        "parallelism": f"dp{world} (batch x heads sharded, no collective)",
-                       "l2": "flushed (256 MB write) between timed steps, outside the step events",
+                       "l2": "flushed between timed steps, outside the step events: 256 MB write, then a 256 MB read so the flush's dirty lines are written back before the step (cold, clean L2)",
                        "kernel_timing": "event-record nodes between the launches of an instrumented copy of the step's CUDA graph, K extra steps, mean"},
             "e2e": {"value": tokens / (e2e_ms / 1e3), "unit": "tokens/s",
                     "h2d_bytes_per_step": int(hx.numel() * 2), "d2h_bytes_per_step": int(hy[0].numel() * 2),

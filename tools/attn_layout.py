@@ -29,3 +29,17 @@ for name, args in (("contiguous", (qc, kc, vc, oc)), ("fused-qkv views", (qs, ks
         e0.record(); sf.block_sparse_sdpa(q, k, v, b, out=o); e1.record(); torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1) * 1e3)
     print(f"{name:16s}: {t:6.1f} us (graph, warm L2)   {sorted(ts)[len(ts)//2]:6.1f} us (single launch, L2 flushed)")
+
+# the layer's order: L2 flushed, then the QKV GEMM writes qkv, then the attention reads it
+from paper_2506_06095_b200 import fused
+x = torch.randn(bs * n, H, device="cuda").half()
+wqkv = (torch.randn(3 * H, H, device="cuda") * 0.02).half()
+bqkv = torch.randn(3 * H, device="cuda")
+ts = []
+for _ in range(20):
+    flush.zero_()
+    fused.gemm_fused(x, wqkv, qkv, bias=bqkv)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(); sf.block_sparse_sdpa(qs, ks, vs, b, out=os_); e1.record(); torch.cuda.synchronize()
+    ts.append(e0.elapsed_time(e1) * 1e3)
+print(f"{'after QKV GEMM':16s}: {sorted(ts)[len(ts)//2]:6.1f} us (single launch, L2 flushed before the GEMM)")
