@@ -367,6 +367,23 @@ sf_status gemm_dispatch(const sf_gemm_args& a, cudaStream_t st) {
     // small problems: 128-wide tiles when 256-wide ones would leave most SMs idle (twice the CTAs
     // on a latency-bound GEMM, e.g. the M = 512 layers of cfg1)
     const bool few = ceil_div(a.M, BM) * ceil_div(a.N, 256) < num_sms();
+    const bool ln_clusters = (a.N % 256 == 0 && a.N / 256 <= kMaxCluster) || (a.N % 128 == 0 && a.N / 128 <= kMaxCluster);
+    if (ln && a.N <= 4096 && (!ln_clusters || ceil_div(a.M, BM) * ceil_div(a.N, 128) < num_sms() / 4)) {
+        // a LayerNorm row cluster per 128 rows would occupy under a quarter of the SMs (or the row
+        // does not split into <= 8 CTAs of 128/256 columns): the GEMM (+bias/act/residual) and a
+        // MiChain LayerNorm pass over its output (in place, or from out_pre_ln) as two launches
+        // (cfg1: 68.5 -> 61.6 us per layer step)
+        sf_gemm_args g = a;
+        g.epi.ln_gamma = g.epi.ln_beta = nullptr;
+        g.epi.out_pre_ln = nullptr;
+        void* mid = a.epi.out_pre_ln ? a.epi.out_pre_ln : a.out;
+        g.out = mid;
+        SF_TRY((launch_gemm<T, 128, false>(g, st)));
+        sf_gemm_epilogue e{};
+        e.ln_gamma = a.epi.ln_gamma;
+        e.ln_beta = a.epi.ln_beta;
+        return sf_mi_chain(a.M, a.N, a.dtype, mid, a.ldout, &e, a.out, a.ldout, st);
+    }
     if (ln) {
         const bool fit256 = a.N % 256 == 0 && a.N / 256 <= kMaxCluster;
         const bool fit128 = a.N % 128 == 0 && a.N / 128 <= kMaxCluster;

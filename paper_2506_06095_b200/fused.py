@@ -34,7 +34,9 @@ TILE_AUTO, TILE_PAIR = 0, 1  # sf_gemm_args.tile_n: SF_TILE_AUTO / SF_TILE_PAIR 
 def gemm_fused(x: torch.Tensor, w_nk: torch.Tensor, out: Optional[torch.Tensor] = None, *, bias=None,
                act: str = "none", aux=None, ln_gamma=None, ln_beta=None, out_pre_ln=None, tile_n: int = 0,
                stream=None) -> torch.Tensor:
-    """out = LN(act(x @ w_nk.T + bias) + aux) — the CiMi template, one tcgen05 kernel."""
+    """out = LN(act(x @ w_nk.T + bias) + aux) — the CiMi template: one tcgen05 kernel (LayerNorm in
+    the cluster epilogue), or with tile_n auto on small grids / unclusterable rows, the GEMM followed
+    by a MiChain LayerNorm pass."""
     M, K = x.shape
     N, K2 = w_nk.shape
     if K != K2:

@@ -128,6 +128,29 @@ def test_gemm_shape_errors(fz):
     x = torch.zeros(128, 64, dtype=torch.float16, device="cuda")
     with pytest.raises(_lib.ShapeError):
         fz.gemm_fused(x, torch.zeros(128, 32, dtype=torch.float16, device="cuda"))
-    with pytest.raises(_lib.ShapeError):  # LN over a row that cannot be split into <= 8 CTAs of 128/256
-        fz.gemm_fused(x, torch.zeros(96, 64, dtype=torch.float16, device="cuda"),
+    with pytest.raises(_lib.ShapeError):  # LN over a row that cannot be split into <= 8 CTAs of 128
+        fz.gemm_fused(x, torch.zeros(96, 64, dtype=torch.float16, device="cuda"), tile_n=128,
                       ln_gamma=torch.ones(96, device="cuda"), ln_beta=torch.zeros(96, device="cuda"))
+
+
+@pytest.mark.parametrize("M,N,K,pre", [(96, 96, 64, False), (512, 768, 768, True), (300, 800, 128, False)])
+def test_gemm_ln_split_auto(fz, M, N, K, pre):
+    """tile_n auto with a LayerNorm that the cluster epilogue cannot (or should not) take: GEMM +
+    bias + residual, then a MiChain LayerNorm pass (in place, or from out_pre_ln)."""
+    import torch
+    g = torch.Generator(device="cpu").manual_seed(M + N)
+    r = lambda *s: (torch.rand(*s, generator=g) * 2 - 1)
+    x, w, aux = r(M, K).half(), (r(N, K) / K ** 0.5).half(), r(M, N).half()
+    bias, gam, bet = r(N), r(N) + 1.5, r(N)
+    s = x.float() @ w.float().t() + bias + aux.float()
+    mu, var = s.mean(1, keepdim=True), s.var(1, unbiased=False, keepdim=True)
+    ref = (s - mu) / torch.sqrt(var + 1e-5) * gam + bet
+    dev = lambda t: t.cuda()
+    pre_t = torch.empty(M, N, dtype=torch.float16, device="cuda") if pre else None
+    out = fz.gemm_fused(dev(x), dev(w), bias=dev(bias), aux=dev(aux), ln_gamma=dev(gam), ln_beta=dev(bet),
+                        out_pre_ln=pre_t)
+    torch.cuda.synchronize()
+    err = (out.float().cpu() - ref).abs()
+    assert err.max().item() <= 2e-2 and err.sum().item() / ref.abs().sum().item() <= 1e-3
+    if pre:
+        assert (pre_t.float().cpu() - s).abs().max().item() <= 2e-2
