@@ -61,7 +61,7 @@ def test_gemm_bias_act(fz, oracle, act, tile):
 
 
 @pytest.mark.parametrize("N,K", [(768, 768), (768, 3072), (512, 256), (256, 128), (1024, 256)])
-@pytest.mark.parametrize("tile", [0, PAIR])
+@pytest.mark.parametrize("tile", [0, 128, 256, PAIR])
 def test_gemm_bias_add_layernorm(fz, oracle, N, K, tile):
     import torch
     M = 384

@@ -76,6 +76,17 @@ def test_layer_matches_chain_oracle(sf, oracle, model, compat, ln_split):
     parity(L.forward(x), ref)
 
 
+@pytest.mark.parametrize("model", ["bert-layer", "gpt-layer"])
+def test_layer_cluster_layernorm_path(sf, oracle, model):
+    """M = 4096 rows: the out-projection / FFN2 LayerNorms run in the GEMM's cluster epilogue
+    (the small layers above take the GEMM + MiChain path)."""
+    from paper_2506_06095_b200 import layer
+    bs, seq, hid, heads = 4, 1024, 256, 4
+    terms = [dict(pattern="bigbird", seq_len=seq, global_width=32, band_width=32, filling_rate=0.1, seed=0)]
+    L, x, ref = build(sf, layer, oracle, model, bs, seq, hid, heads, terms, False)
+    parity(L.forward(x), ref)
+
+
 def test_layer_cuda_graph_replay(sf, oracle):
     import torch
     from paper_2506_06095_b200 import layer
