@@ -137,7 +137,7 @@ def cpu_reference(cfg, threads, reps):
         times.append(time.perf_counter() - t0)
     best = min(times)
     tokens = threads * seq
-    sample = (f"{threads} independent sequences x {seq} tokens ({threads} of the batch's {cfg['bs']} sequences), "
+    sample = (f"{threads} independent sequences x {seq} tokens (one per host thread; the batch holds {cfg['bs']}), "
               f"1 layer {cfg['model']} unfused chain, BSR 16x16 (the reference's own a100/rtx4090 plan); "
               f"best of {reps}")
     return tokens / best, kind, sample, threads
@@ -151,7 +151,9 @@ def run_reference_arm(args, cfg):
     o, r = Oracle(), Reference()
     m = o.mask(cfg["mask"])
     seq, hid, heads = cfg["seq"], cfg["hidden"], cfg["heads"]
-    threads = max(1, min(os.cpu_count() or 1, args.steps))
+    # all host threads this process may use (std::threads in the reference shim, so torchrun's
+    # OMP_NUM_THREADS=1 does not apply)
+    threads = max(1, len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1))
     kind = "reference" if r.available else "port"
 
     def run(n):  # n independent sequences through the chain, concurrently on n host threads
@@ -163,22 +165,23 @@ def run_reference_arm(args, cfg):
             for _ in range(n):
                 run_chain(o, cfg["model"], gd, gd["input"], m, 1, seq, heads, hid // heads, 16, 16, threads=1)
 
-    # a step = one sequence (seq tokens) through the reference's unfused chain; steps run
-    # concurrently over all host cores, W warm-up sequences first, then exactly K timed ones
+    # a step = one sequence (seq tokens) through the reference's unfused chain; sequences run in
+    # waves of one per host thread (every core busy; K rounded up to whole waves, all of them
+    # timed), one warm-up wave first
     if args.warmup:
-        run(min(threads, args.warmup))
+        run(threads)
+    waves = max(1, -(-args.steps // threads))
     t0 = time.perf_counter()
-    left = args.steps
-    while left > 0:
-        n = min(threads, left)
-        run(n)
-        left -= n
+    for _ in range(waves):
+        run(threads)
     wall = time.perf_counter() - t0
-    value = args.steps * seq / wall
-    sample = (f"{args.steps} sequences x {seq} tokens ({cfg['model']}, unfused CpuBackend::run_chain, BSR 16x16 = "
-              f"the reference's own a100/rtx4090 plan) on {threads} host threads")
+    n_seq = waves * threads
+    value = n_seq * seq / wall
+    sample = (f"{n_seq} sequences x {seq} tokens ({waves} wave(s) of {threads} concurrent sequences >= the "
+              f"{args.steps} steps asked; {cfg['model']}, unfused CpuBackend::run_chain, BSR 16x16 = the "
+              f"reference's own a100/rtx4090 plan) on {threads} host threads")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * wall / args.steps,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * wall / n_seq,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (GraphData seeds)",
             "config": {"workload": cfg["desc"], "model": cfg["model"], "global_batch": cfg["bs"], "seq_len": cfg["seq"]},
@@ -660,7 +663,8 @@ def main():
             "gpu_launches": int(launches), "roofline": roof, "kernels_ms": parts, "mha": mha,
             "clocks": clk.summary()}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, kind, sample, thr = cpu_reference(cfg, min(os.cpu_count() or 1, cfg["bs"]), 1)
+        host = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+        v, kind, sample, thr = cpu_reference(cfg, max(1, host), 1)
         line["cpu_baseline"] = {"value": v, "unit": "tokens/s", "cores": thr, "kind": kind, "sample": sample}
     if rank == 0:
         print(json.dumps(line), flush=True)
