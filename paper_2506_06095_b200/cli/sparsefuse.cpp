@@ -8,9 +8,10 @@
 //   sparsefuse fuse encode 0-1,1-3,3-4
 //   sparsefuse fuse decode 0110
 //   sparsefuse attn verify <mask flags> [--bs B] [--heads H] [--head-size D] [--seed S]
+//   sparsefuse report show <report.jsonl> [--line K] [--output text|json]
 //   mask flags: --pattern P --seq-len N [--band W] [--global G] [--dilation R] [--fill F]
 //               [--block-rand B] [--seed S]   (or --sfmk file.sfmk)
-// `tune run` is sf_tune (same directory).
+// `tune run` is sf_tune (same directory); `report show` renders one of its JSON reports.
 #include <cstdio>
 #include <cstdlib>
 #include <fstream>
@@ -21,6 +22,7 @@
 
 #include "sparsefuse_b200/ops.hpp"
 #include "sparsefuse_b200/fusion.hpp"
+#include "sparsefuse_b200/io.hpp"
 
 using namespace sparsefuse;
 
@@ -189,10 +191,80 @@ int attn_verify(const Args& a) {
     return pass ? 0 : 1;
 }
 
+// report show: a human-readable summary of a tuning report (sf_tune's JSON line, the fields of
+// the reference's report); --output json re-emits the selected line unchanged
+int report_show(const Args& a) {
+    if (a.pos.empty()) usage("report show needs a report file");
+    std::ifstream f(a.pos[0]);
+    if (!f) usage("cannot open " + a.pos[0]);
+    const int want = std::atoi(a.get("line", "0").c_str());
+    std::string line;
+    for (int i = 0; std::getline(f, line); ++i)
+        if (i == want) break;
+    if (line.find_first_not_of(" \t\r") == std::string::npos) usage("no report on line " + std::to_string(want));
+    if (a.get("output", "text") == "json") {
+        std::cout << line << std::endl;
+        return 0;
+    }
+    using io_detail::Value;
+    const Value r = io_detail::Parser(line).parse();
+    auto num_of = [](const Value& v) { return v.number(); };
+    auto us = [](double s) {
+        char b[32];
+        std::snprintf(b, sizeof b, "%.1f us", s * 1e6);
+        return std::string(b);
+    };
+    const Value& hy = r.at("hyper");
+    const Value& pl = r.at("plan");
+    std::cout << r.at("graph").str() << "  bs " << num_of(hy.at("bs")) << "  seq " << num_of(hy.at("seq_len"))
+              << "  hidden " << num_of(hy.at("hidden")) << "  heads " << num_of(hy.at("heads")) << " x "
+              << num_of(hy.at("head_size")) << "  mask " << r.at("mask").str() << "  hw " << r.at("hw").str()
+              << " / backend " << r.at("backend").str() << "\n";
+    std::cout << "plan: " << pl.at("kind").str() << " (" << num_of(pl.at("block_m")) << " x " << num_of(pl.at("block_n"))
+              << "), threshold " << num_of(pl.at("threshold")) << "\n";
+    const double e2e = num_of(r.at("end_to_end_s"));
+    std::cout << "scheme " << r.at("code").str() << " (hex " << r.at("code_hex").str() << "), end-to-end " << us(e2e);
+    if (r.has("end_to_end_unfused_s")) {
+        const double u = num_of(r.at("end_to_end_unfused_s"));
+        char b[64];
+        std::snprintf(b, sizeof b, " (unfused %s, %.2fx)", us(u).c_str(), e2e > 0 ? u / e2e : 0.0);
+        std::cout << b;
+    }
+    std::cout << "\n";
+    const auto& segs = std::get<std::vector<Value>>(r.at("segments").v);
+    for (const auto& sg : segs) {
+        std::string ops;
+        for (const auto& o : std::get<std::vector<Value>>(sg.at("ops").v)) ops += (ops.empty() ? "" : "+") + o.str();
+        char b[256];
+        std::snprintf(b, sizeof b, "  [%2d,%2d) %-34s %-22s %12s%s\n", static_cast<int>(num_of(sg.at("begin"))),
+                      static_cast<int>(num_of(sg.at("end"))), ops.c_str(), sg.at("setting").str().c_str(),
+                      us(num_of(sg.at("duration_s"))).c_str(),
+                      std::get<bool>(sg.at("untuned").v) ? "  (untuned)" : "");
+        std::cout << b;
+    }
+    const Value& st = r.at("stats");
+    const double meas = num_of(st.at("measure_calls")), hits = num_of(st.at("cache_hits"));
+    char b[256];
+    std::snprintf(b, sizeof b,
+                  "search: %.0f measurements, %.0f sample evals, %.0f cache hits (%.1f%%), %.0f end-to-end runs, %.0f "
+                  "schemes, stage-1 accepted %.0f, stage-2 iterations %.0f; tuning %.3f s\n",
+                  meas, num_of(st.at("sample_evals")), hits, meas + hits > 0 ? 100.0 * hits / (meas + hits) : 0.0,
+                  num_of(st.at("e2e_calls")), num_of(st.at("schemes_evaluated")), num_of(st.at("stage1_accepted")),
+                  num_of(st.at("stage2_iterations")), num_of(r.at("tuning_wall_s")));
+    std::cout << b;
+    if (r.has("cache")) {
+        const Value& c = r.at("cache");
+        const std::string file = c.at("file").str();
+        std::cout << "cache: ctx " << c.at("ctx").str() << ", file " << (file.empty() ? "-" : file) << ", "
+                  << num_of(c.at("preloaded_entries")) << " preloaded entries\n";
+    }
+    return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
-    if (argc < 3) usage("sparsefuse <mask|plan|fuse|attn> <command> [flags]");
+    if (argc < 3) usage("sparsefuse <mask|plan|fuse|attn|report> <command> [flags]");
     const std::string grp = argv[1], cmd = argv[2];
     const Args a = parse(argc, argv, 3);
     try {
@@ -201,6 +273,10 @@ int main(int argc, char** argv) {
         if (grp == "plan" && cmd == "select") return plan_select(a);
         if (grp == "fuse" && (cmd == "encode" || cmd == "decode")) return fuse(a, cmd);
         if (grp == "attn" && cmd == "verify") return attn_verify(a);
+        if (grp == "report" && cmd == "show") return report_show(a);
+    } catch (const io_error& e) {
+        std::cout << "{\"error\": \"io_error\", \"message\": \"" << e.what() << "\"}" << std::endl;
+        return 1;
     } catch (const std::invalid_argument& e) {
         std::cout << "{\"error\": \"invalid_parameter\", \"message\": \"" << e.what() << "\"}" << std::endl;
         return 2;

@@ -47,3 +47,20 @@ def test_mask_and_plan_commands(oracle, tmp_path):
 def test_attn_verify_passes(pattern):
     rc, j = run("attn", "verify", *pattern, "--seq-len", 512, "--bs", 1, "--heads", 2)
     assert rc == 0 and j["pass"] and j["tiles_loaded"] == j["valid_tiles"]
+
+
+def test_report_show_renders_a_tuning_report():
+    """`report show` (SPEC.md cli: a human-readable summary of a `tune run` report); the fixture
+    is sf_tune's report for cfg2 measured on the B200 (profiles/r01/tune_configs_v2.jsonl)."""
+    rep = ROOT / "tests" / "golden" / "tune_report_cfg2.jsonl"
+    r = subprocess.run([str(CLI), "report", "show", str(rep)], capture_output=True, text=True, timeout=60)
+    assert r.returncode == 0
+    text = r.stdout
+    j = json.loads(rep.read_text().splitlines()[0])
+    assert j["graph"] in text and j["code"] in text and f"hex {j['code_hex']}" in text
+    assert text.count("\n  [") == len(j["segments"])
+    assert "(untuned)" in text and "cache hits" in text
+    rc, back = run("report", "show", rep, "--output", "json")
+    assert rc == 0 and back == j
+    rc, err = run("report", "show", ROOT / "tests" / "golden" / "missing.jsonl")
+    assert rc == 2 and err["error"] == "usage"

@@ -19,3 +19,22 @@ for _ in range(20):
 torch.cuda.current_stream().wait_stream(s1); torch.cuda.current_stream().wait_stream(s2)
 e1.record(); torch.cuda.synchronize()
 print("both directions concurrent:", round(n * 20 / (e0.elapsed_time(e1) / 1e3) / 1e9, 1), "GB/s each way")
+
+# the same 25 MB each way, split into 2 / 4 chunks on as many streams per direction (more than one
+# copy engine per direction?)
+for parts in (2, 4):
+    ss = [torch.cuda.Stream() for _ in range(2 * parts)]
+    ch = n // parts
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(20):
+        for i in range(parts):
+            with torch.cuda.stream(ss[i]):
+                d[i * ch:(i + 1) * ch].copy_(h[i * ch:(i + 1) * ch], non_blocking=True)
+            with torch.cuda.stream(ss[parts + i]):
+                h2[i * ch:(i + 1) * ch].copy_(d2[i * ch:(i + 1) * ch], non_blocking=True)
+    for x in ss:
+        torch.cuda.current_stream().wait_stream(x)
+    e1.record(); torch.cuda.synchronize()
+    print(f"both directions, {parts} streams each:", round(n * 20 / (e0.elapsed_time(e1) / 1e3) / 1e9, 1), "GB/s per direction")
