@@ -303,7 +303,8 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
     if (warp == 0) {
         // ------------------------------------------------------------------ producer (one warp)
         // Lanes fetch 32 load-list entries at a time; lane 0 issues the TMA for each step.
-        int g = 0, qi = 0;
+        uint32_t g = 0;  // step counters unsigned: the ring index / phase math is one LOP3 each
+        int qi = 0;
         for (int k = 0; k < nitems; ++k) {
             int rb, bh, l0, L, nsteps;
             items.get(k, rb, bh, l0, L, nsteps);
@@ -399,7 +400,7 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
             Cursor cs, cp;
             cs.next_item(items, nitems);
             cp.next_item(items, nitems);
-            int gS = 0;
+            uint32_t gS = 0;
             auto issue_s = [&]() {
                 if (cs.j == 0) {
                     tc::mbar_wait(&q_full[cs.qi & 1], (cs.qi >> 1) & 1);
@@ -425,7 +426,7 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
                 cs.advance(items, nitems);
             };
             for (int j = 0; j < kSBuf && cs.valid; ++j) issue_s();
-            for (int g = 0; cp.valid; ++g) {
+            for (uint32_t g = 0; cp.valid; ++g) {
                 const int s = g % kStages;
                 const int sb = g % kSBuf;
                 tc::mbar_wait(&p_full[sb], (g / kSBuf) & 1);  // P_g in TMEM (S_g consumed), O rescaled
@@ -459,7 +460,7 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
         const int my_head = kPair ? static_cast<int>(lane >> 4) : 0;
         const uint32_t trow = tmem + ((q * 32) << 16);
         const float sl2 = p.scale_log2;
-        int g = 0;
+        uint32_t g = 0;
         for (int k = 0; k < nitems; ++k) {
             int rb, bh, l0, L, nsteps;
             items.get(k, rb, bh, l0, L, nsteps);
