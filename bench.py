@@ -563,7 +563,7 @@ def main():
     # PCIe directions at once) and overlap neighbouring steps' compute; NB layer instances (shared
     # weights and formats) rotate the activations so no buffer is overwritten while a copy still
     # reads it, and the copy streams never wait on the compute of the step just before.
-    NB = int(os.environ.get("SF_E2E_BUFFERS", "4"))
+    NB = int(os.environ.get("SF_E2E_BUFFERS", "8"))
     hx = torch.empty(s.rows, s.hidden, dtype=torch.float16, pin_memory=True)
     hx.copy_(x.cpu())
     hy = [torch.empty_like(hx, pin_memory=True) for _ in range(NB)]
@@ -595,7 +595,7 @@ def main():
                 out_done[b].record(s_out)
 
     e2e_steps = max(4, min(args.steps, 100))
-    e2e_run(4)
+    e2e_run(e2e_steps)  # one untimed window first: the first windows of pinned-memory copies run slow
     torch.cuda.synchronize()
     if os.environ.get("SF_E2E_PROBE"):  # diagnosis: repeated e2e windows in one process
         for _ in range(6):
