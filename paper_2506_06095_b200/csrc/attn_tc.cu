@@ -27,6 +27,9 @@
 //              zero (attention.hpp:160-166).
 // Only the BSR load set is iterated: empty tiles are never touched (attention.hpp:104-109).
 #include <algorithm>
+#include <cstdlib>
+#include <map>
+#include <mutex>
 
 #include "tc.cuh"
 
@@ -47,7 +50,7 @@ constexpr int kKVBytes = kNS * kD * 2;       // one 64-key stage of K (or V)
 constexpr int kMaskBytes = kBM * 8;          // 64 bits per query row per stage
 constexpr float kRescaleLog2 = 8.0f;         // lazy-rescale threshold (P <= 2^8)
 constexpr int kSmem = 1024 + 2 * kQBytes + 2 * kStages * kKVBytes + kStages * kMaskBytes + kStages * 16 +
-                      kMaxRowBlocks * 4 + 256;
+                      kMaxRowBlocks * 4 + 512;
 
 // Geometry per query-block height. BM = 128: one (b, h) slice per work item, M = 128 MMAs.
 // BM = 64 ("head pair"): a work item is one 64-row block of TWO heads that share the block's load
@@ -65,7 +68,7 @@ struct AttnGeo {
     static constexpr int kKVB = kHeads * kNS * kD * 2;         // one stage of K (or V), all heads
     static constexpr int kMaskB = BM * 8;                      // 64 bits per query row per stage
     static constexpr int kSmemG = 1024 + 2 * kQB + 2 * kStagesG * kKVB + kStagesG * kMaskB + kStagesG * 16 +
-                                  kMaxRowBlocks * 4 + 256;
+                                  kMaxRowBlocks * 4 + 512;
 };
 
 struct AttnParams {
@@ -79,6 +82,7 @@ struct AttnParams {
     void* o;
     int64_t o_sb, o_sh, o_sn;
     float scale_log2;
+    unsigned* work;  // [2]: next item, CTAs done (dynamic schedule), or null (static deal)
     unsigned long long* trace;  // optional clock64 trace of CTA 0 (sf_debug_attn_trace)
 };
 
@@ -175,14 +179,31 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* m, uin
         : "memory");
 }
 
-// The CTA's work items, in the order every role walks them. Items (row-block rank, b*h) are
-// numbered with row blocks ranked by descending load count and dealt to the CTAs in snake order
-// (round k goes c = 0..G-1 when k is even, G-1..0 when odd), so the longest items go out first
-// and each CTA's total is balanced (an LPT-style static schedule; no atomics, graph-replayable).
+// Work items (row-block rank, b*h) are numbered with row blocks ranked by descending load count,
+// so the longest items come first. The producer warp picks the CTA's next item and publishes it
+// to the MMA and softmax roles through a small shared-memory ring (kItemRing slots with full /
+// empty barriers). With a work counter (p.work) it takes the next global index by atomicAdd —
+// greedy longest-first list scheduling, which keeps CTAs balanced when a few row blocks are much
+// longer than the rest (global rows: cfg4's items range 5-64 steps, a static deal left the
+// longest CTA 46% above the mean); the last CTA to finish resets the counter, so the launch
+// replays in a CUDA graph. Without one, items are dealt statically in snake order (round k goes
+// c = 0..G-1 when k is even, G-1..0 when odd).
+constexpr int kItemRing = 4;
 struct Items {
     const int32_t* lrp;
     const int32_t* order;  // smem: row block of each rank
     int bh_count, n_items, G;
+    // the static deal: the CTA's k-th item index, or -1 past its last
+    __device__ __forceinline__ int static_idx(int k) const {
+        return k < count() ? k * static_cast<int>(gridDim.x) + pos(k) : -1;
+    }
+    __device__ __forceinline__ void decode(int idx, int& rb, int& bh, int& l0, int& L, int& nsteps) const {
+        rb = order[idx / bh_count];
+        bh = idx % bh_count;
+        l0 = lrp[rb];
+        L = lrp[rb + 1] - l0;
+        nsteps = (L + G - 1) / G;
+    }
     __device__ __forceinline__ int pos(int k) const {
         const int c = static_cast<int>(blockIdx.x), g = static_cast<int>(gridDim.x);
         return (k & 1) ? g - 1 - c : c;
@@ -202,23 +223,42 @@ struct Items {
     }
 };
 
+// Consumer side of the item ring: the item at ring position `it` (waits for the producer to
+// publish it; `release` frees the slot once this consumer has its copy).
+struct ItemFeed {
+    const int32_t* slots;  // smem [kItemRing]
+    uint64_t* full;        // [kItemRing], one producer arrive
+    uint64_t* empty;       // [kItemRing], 2 (the MMA issuer's two cursors) + 4 (softmax warps) arrives
+    __device__ __forceinline__ int read(uint32_t it) const {
+        tc::mbar_wait(&full[it % kItemRing], (it / kItemRing) & 1);
+        return *reinterpret_cast<const volatile int32_t*>(&slots[it % kItemRing]);
+    }
+    __device__ __forceinline__ void release(uint32_t it) const { tc::mbar_arrive(&empty[it % kItemRing]); }
+};
+
 // Flat walk over the steps of the CTA's non-empty items (the MMA issuer keeps two of these: the
-// S cursor runs kSBuf steps ahead of the P.V cursor).
+// S cursor runs kSBuf steps ahead of the P.V cursor). Each cursor releases a ring slot as soon as
+// it has read it, so the S cursor can read past a run of empty items while the P.V cursor still
+// works on an earlier one.
 struct Cursor {
-    int k = -1, qi = -1, j = 0, ns = 0;
+    uint32_t it = 0;
+    int qi = -1, j = 0, ns = 0;
     bool valid = false;
-    __device__ __forceinline__ bool next_item(const Items& it, int nitems) {
+    __device__ __forceinline__ bool next_item(const Items& items, const ItemFeed& feed) {
         int rb, bh, l0, L;
         do {
-            if (++k >= nitems) return valid = false;
-            it.get(k, rb, bh, l0, L, ns);
+            const int idx = feed.read(it);
+            feed.release(it);
+            ++it;
+            if (idx < 0) return valid = false;
+            items.decode(idx, rb, bh, l0, L, ns);
         } while (ns == 0);
         ++qi;
         j = 0;
         return valid = true;
     }
-    __device__ __forceinline__ void advance(const Items& it, int nitems) {
-        if (++j == ns) next_item(it, nitems);
+    __device__ __forceinline__ void advance(const Items& items, const ItemFeed& feed) {
+        if (++j == ns) next_item(items, feed);
     }
 };
 
@@ -253,7 +293,10 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
     uint64_t* p_full = s_full + kSBuf;        // [kSBuf]
     uint64_t* o_full = p_full + kSBuf;        // [2]: P.V step g completes o_full[g&1] (parity waits are
                                               // unambiguous only within one phase of lag)
-    uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(o_full + 2);
+    uint64_t* item_full = o_full + 2;               // [kItemRing]
+    uint64_t* item_empty = item_full + kItemRing;  // [kItemRing]
+    int32_t* s_item = reinterpret_cast<int32_t*>(item_empty + kItemRing);  // [kItemRing]
+    uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(s_item + kItemRing);
 
     pdl_enter();
     const uint32_t warp = tc::warp_id();
@@ -289,6 +332,10 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
             tc::mbar_init(&s_full[s], 1);
             tc::mbar_init(&p_full[s], 128);
         }
+        for (int s = 0; s < kItemRing; ++s) {
+            tc::mbar_init(&item_full[s], 1);
+            tc::mbar_init(&item_empty[s], 6);
+        }
         tc::fence_barrier_init();
     }
     if (warp == 1) tc::tmem_alloc<256>(tmem_ptr);
@@ -298,16 +345,30 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
     const uint32_t tmem = *tmem_ptr;
     const uint32_t tO = tmem + kOCol;
     const Items items{p.load_row_ptr, s_order, p.bh, p.n_items, G};
-    const int nitems = items.count();
+    const ItemFeed feed{s_item, item_full, item_empty};
 
     if (warp == 0) {
         // ------------------------------------------------------------------ producer (one warp)
         // Lanes fetch 32 load-list entries at a time; lane 0 issues the TMA for each step.
         uint32_t g = 0;  // step counters unsigned: the ring index / phase math is one LOP3 each
         int qi = 0;
-        for (int k = 0; k < nitems; ++k) {
+        for (uint32_t it = 0;; ++it) {
+            int idx = 0;
+            if (lane == 0) {  // pick and publish the CTA's next item
+                tc::mbar_wait(&item_empty[it % kItemRing], ((it / kItemRing) & 1) ^ 1);
+                if (p.work) {
+                    idx = static_cast<int>(atomicAdd(p.work, 1u));
+                    if (idx >= p.n_items) idx = -1;
+                } else {
+                    idx = items.static_idx(static_cast<int>(it));
+                }
+                s_item[it % kItemRing] = idx;
+                tc::mbar_arrive(&item_full[it % kItemRing]);
+            }
+            idx = __shfl_sync(0xffffffffu, idx, 0);
+            if (idx < 0) break;
             int rb, bh, l0, L, nsteps;
-            items.get(k, rb, bh, l0, L, nsteps);
+            items.decode(idx, rb, bh, l0, L, nsteps);
             if (nsteps == 0) continue;
             // the unit's heads: one slice, or the pair (2u, 2u+1) (an odd last pair repeats head A)
             int hb[2], hh2[2];
@@ -398,8 +459,8 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
         constexpr uint32_t idesc_o = tc::idesc_f16(BM, kD, bf, 0, 1);   // P (TMEM) x V (MN-major)
         if (tc::elect_one()) {
             Cursor cs, cp;
-            cs.next_item(items, nitems);
-            cp.next_item(items, nitems);
+            cs.next_item(items, feed);
+            cp.next_item(items, feed);
             uint32_t gS = 0;
             auto issue_s = [&]() {
                 if (cs.j == 0) {
@@ -423,7 +484,7 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
                 tc::mma_commit(&s_full[gS % kSBuf]);
                 if (cs.j == cs.ns - 1) tc::mma_commit(&q_empty[cs.qi & 1]);  // last S of the item: Q free
                 ++gS;
-                cs.advance(items, nitems);
+                cs.advance(items, feed);
             };
             for (int j = 0; j < kSBuf && cs.valid; ++j) issue_s();
             for (uint32_t g = 0; cp.valid; ++g) {
@@ -447,7 +508,7 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
                 SF_TRACE(g, 9);
                 if (cs.valid) issue_s();
                 SF_TRACE(g, 10);
-                cp.advance(items, nitems);
+                cp.advance(items, feed);
             }
         }
     } else {
@@ -461,9 +522,13 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
         const uint32_t trow = tmem + ((q * 32) << 16);
         const float sl2 = p.scale_log2;
         uint32_t g = 0;
-        for (int k = 0; k < nitems; ++k) {
+        for (uint32_t k = 0;; ++k) {
+            const int idx = feed.read(k);
+            __syncwarp();
+            if (lane == 0) feed.release(k);
+            if (idx < 0) break;
             int rb, bh, l0, L, nsteps;
-            items.get(k, rb, bh, l0, L, nsteps);
+            items.decode(idx, rb, bh, l0, L, nsteps);
             float m = -INFINITY, l = 0.f;
             for (int j = 0; j < nsteps; ++j, ++g) {
                 const int st = g % kStages;
@@ -619,6 +684,12 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
     }
     tc::fence_before_sync();
     __syncthreads();
+    if (p.work && threadIdx.x == 0) {  // every fetch of this launch is done: the last CTA resets
+        if (atomicAdd(p.work + 1, 1u) == gridDim.x - 1) {
+            p.work[0] = 0;
+            p.work[1] = 0;
+        }
+    }
     if (warp == 1) tc::tmem_dealloc<256>(tmem);
 }
 
@@ -649,6 +720,37 @@ sf_status make_tmap_4d(CUtensorMap* map, const void* base, int n, int h, int bs,
 }  // namespace
 
 unsigned long long* g_attn_trace = nullptr;
+
+// The dynamic schedule's work counter, one per (device, stream): launches on one stream are
+// ordered (PDL included: the next launch's griddepcontrol.wait follows this one's reset), so they
+// can share it. Allocated on first use outside a stream capture; a launch captured before its
+// stream has a counter falls back to the static deal. SF_ATTN_STATIC=1 forces the static deal.
+namespace {
+unsigned* attn_work_counter(cudaStream_t st) {
+    static const bool force_static = [] {
+        const char* e = std::getenv("SF_ATTN_STATIC");
+        return e && *e == '1';
+    }();
+    if (force_static) return nullptr;
+    static std::mutex mu;
+    static std::map<std::pair<int, cudaStream_t>, unsigned*> counters;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+    std::lock_guard<std::mutex> lock(mu);
+    const auto key = std::make_pair(dev, st);
+    const auto it = counters.find(key);
+    if (it != counters.end()) return it->second;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return nullptr;
+    unsigned* w = nullptr;
+    if (cudaMalloc(&w, 2 * sizeof(unsigned)) != cudaSuccess || cudaMemsetAsync(w, 0, 2 * sizeof(unsigned), st) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    counters.emplace(key, w);
+    return w;
+}
+}  // namespace
 
 sf_status attn_tc(const sf_attn_args& a, const sf_bsr_dev& b, cudaStream_t st, bool probe_only) {
     const bool shape_ok = (b.block_m == 128 || b.block_m == 64) && (b.block_n == 16 || b.block_n == 32 || b.block_n == 64) &&
@@ -682,6 +784,7 @@ sf_status attn_tc(const sf_attn_args& a, const sf_bsr_dev& b, cudaStream_t st, b
     p.o_sn = a.o_sn;
     p.scale_log2 = a.scale * 1.4426950408889634f;
     p.trace = g_attn_trace;
+    p.work = attn_work_counter(st);
     void (*kern)(AttnParams) = nullptr;
     int smem = AttnGeo<128>::kSmemG;
     if (b.block_m == 128) {
