@@ -51,7 +51,8 @@ def summarise(path):
                 if v is not None and k.endswith("_MB"):
                     v = v / {"byte": 1e6, "Kbyte": 1e3, "Mbyte": 1.0, "Gbyte": 1e-3}.get(u, 1e6)
                 if v is not None and k == "us":
-                    v = v / {"nsecond": 1e3, "usecond": 1.0, "msecond": 1e-3}.get(u, 1.0)
+                    v = v / {"nsecond": 1e3, "ns": 1e3, "usecond": 1.0, "us": 1.0, "msecond": 1e-3,
+                             "ms": 1e-3}.get(u, 1.0)
                 d[k] = v
         stalls = {}
         for i, h in enumerate(hdr):
