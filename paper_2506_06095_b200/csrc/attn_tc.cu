@@ -723,34 +723,58 @@ unsigned long long* g_attn_trace = nullptr;
 
 // The dynamic schedule's work counter, one per (device, stream): launches on one stream are
 // ordered (PDL included: the next launch's griddepcontrol.wait follows this one's reset), so they
-// can share it. Allocated on first use outside a stream capture; a launch captured before its
-// stream has a counter falls back to the static deal. SF_ATTN_STATIC=1 forces the static deal.
+// can share it. Counters come from a per-device pool of zeroed pairs created outside any stream
+// capture (by sf_bsr_build, or by the first attention launch), so a stream first seen inside a
+// capture still gets one; with no pool (or the pool spent) the launch uses the static deal.
+// SF_ATTN_STATIC=1 forces the static deal.
 namespace {
+constexpr int kCounterPool = 1024;
+std::mutex g_counter_mu;
+std::map<int, std::pair<unsigned*, int>> g_counter_pool;                // device -> (pool, next free)
+std::map<std::pair<int, cudaStream_t>, unsigned*> g_counters;          // (device, stream) -> counter
+
+void reserve_pool_locked(int dev, cudaStream_t st) {  // st: not capturing
+    if (g_counter_pool.count(dev)) return;
+    unsigned* w = nullptr;
+    if (cudaMalloc(&w, kCounterPool * 2 * sizeof(unsigned)) != cudaSuccess ||
+        cudaMemsetAsync(w, 0, kCounterPool * 2 * sizeof(unsigned), st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess) {
+        cudaGetLastError();
+        return;
+    }
+    g_counter_pool.emplace(dev, std::make_pair(w, 0));
+}
+
 unsigned* attn_work_counter(cudaStream_t st) {
     static const bool force_static = [] {
         const char* e = std::getenv("SF_ATTN_STATIC");
         return e && *e == '1';
     }();
     if (force_static) return nullptr;
-    static std::mutex mu;
-    static std::map<std::pair<int, cudaStream_t>, unsigned*> counters;
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
-    std::lock_guard<std::mutex> lock(mu);
+    std::lock_guard<std::mutex> lock(g_counter_mu);
     const auto key = std::make_pair(dev, st);
-    const auto it = counters.find(key);
-    if (it != counters.end()) return it->second;
+    const auto it = g_counters.find(key);
+    if (it != g_counters.end()) return it->second;
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return nullptr;
-    unsigned* w = nullptr;
-    if (cudaMalloc(&w, 2 * sizeof(unsigned)) != cudaSuccess || cudaMemsetAsync(w, 0, 2 * sizeof(unsigned), st) != cudaSuccess) {
-        cudaGetLastError();
-        return nullptr;
-    }
-    counters.emplace(key, w);
+    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess) return nullptr;
+    if (cs == cudaStreamCaptureStatusNone) reserve_pool_locked(dev, st);
+    const auto pool = g_counter_pool.find(dev);
+    if (pool == g_counter_pool.end() || pool->second.second >= kCounterPool) return nullptr;
+    unsigned* w = pool->second.first + 2 * pool->second.second++;
+    g_counters.emplace(key, w);
     return w;
 }
 }  // namespace
+
+// called by sf_bsr_build (never inside a capture: it reads the output sizes back)
+void attn_reserve_counters(cudaStream_t st) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return;
+    std::lock_guard<std::mutex> lock(g_counter_mu);
+    reserve_pool_locked(dev, st);
+}
 
 sf_status attn_tc(const sf_attn_args& a, const sf_bsr_dev& b, cudaStream_t st, bool probe_only) {
     const bool shape_ok = (b.block_m == 128 || b.block_m == 64) && (b.block_n == 16 || b.block_n == 32 || b.block_n == 64) &&

@@ -317,6 +317,10 @@ unsigned blocks_for(int64_t threads, int per = 256) {
 
 using namespace sf;
 
+namespace sf {
+void attn_reserve_counters(cudaStream_t st);  // attn_tc.cu: the attention work-counter pool of this device
+}
+
 extern "C" sf_status sf_bsr_build(const uint32_t* d_bits, int32_t seq_len, int32_t block_m,
                                   int32_t block_n, sf_bsr_dev* out, void* stream) {
     if (!out) return fail(SF_INVALID_PARAMETER, "null output");
@@ -324,6 +328,7 @@ extern "C" sf_status sf_bsr_build(const uint32_t* d_bits, int32_t seq_len, int32
     if (block_m < 1 || block_n < 1) return fail(SF_INVALID_PARAMETER, "block sizes must be >= 1");
     if (seq_len < 1) return fail(SF_INVALID_PARAMETER, "seq_len must be positive");
     cudaStream_t st = as_stream(stream);
+    sf::attn_reserve_counters(st);
     Geo g{seq_len, sf_mask_words(seq_len), block_m, block_n,
           static_cast<int32_t>(ceil_div(seq_len, block_m)), static_cast<int32_t>(ceil_div(seq_len, block_n))};
     const int64_t tiles = static_cast<int64_t>(g.n_rows) * g.n_cols;
