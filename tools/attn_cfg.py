@@ -32,13 +32,14 @@ TERMS = {"cfg2": [dict(pattern="bigbird", seq_len=1024, global_width=32, band_wi
          "cfg3": [dict(pattern="strided", seq_len=2048, band_width=45)],
          "cfg4": [dict(pattern="dilated", seq_len=4096, band_width=64, dilation_rate=1),
                   dict(pattern="global", seq_len=4096, global_width=64)]}
-for cfg in sys.argv[1:] or ["cfg2", "cfg3", "cfg4"]:
-    bs, n = SHAPES[cfg]
-    h, d = 12, 64
-    dm = sf.generate_mask(TERMS[cfg])
-    plan = sf.select_plan(dm, sf.hw_preset("b200"), n, h, bs, d, mode="b200")
-    b = sf.build_bsr(dm, plan.block_m, plan.block_n)
-    q, k, v = (torch.randn(bs, h, n, d, device="cuda").half() for _ in range(3))
-    o = torch.empty_like(q)
-    us = best_us(lambda: sf.block_sparse_sdpa(q, k, v, b, out=o))
-    print(f"{cfg}: plan ({plan.block_m},{plan.block_n}) loads {b.n_load} -> {us:.1f} us")
+if __name__ == "__main__":
+    for cfg in sys.argv[1:] or ["cfg2", "cfg3", "cfg4"]:
+        bs, n = SHAPES[cfg]
+        h, d = 12, 64
+        dm = sf.generate_mask(TERMS[cfg])
+        plan = sf.select_plan(dm, sf.hw_preset("b200"), n, h, bs, d, mode="b200")
+        b = sf.build_bsr(dm, plan.block_m, plan.block_n)
+        q, k, v = (torch.randn(bs, h, n, d, device="cuda").half() for _ in range(3))
+        o = torch.empty_like(q)
+        us = best_us(lambda: sf.block_sparse_sdpa(q, k, v, b, out=o))
+        print(f"{cfg}: plan ({plan.block_m},{plan.block_n}) loads {b.n_load} -> {us:.1f} us")
