@@ -194,3 +194,42 @@ def test_b200_selector_calibration(sf):
     assert b200.threshold == ref.threshold
     small = sf.select_plan(sf.gen_sliding_window(2048, 4), sf.hw_preset("b200"), 2048, 2, 1, 64, mode="b200")
     assert small.kind == "row_wise"
+
+
+def test_dynamic_schedule_graph_replay_and_streams(sf, oracle):
+    """The tcgen05 kernel's work counter (per stream, reset by the last CTA): a skewed mask
+    (global rows ~ all columns, the rest a narrow dilated band, like cfg4) replayed many times from
+    one captured graph, eager launches on two streams, and empty row blocks at the end of the
+    longest-first order must all give the oracle's result."""
+    import torch
+    bs, h, n, d = 2, 5, 1024, 64
+    terms = [dict(pattern="dilated", seq_len=n, band_width=16, dilation_rate=1),
+             dict(pattern="global", seq_len=n, global_width=32)]
+    m = oracle.mask(terms)
+    q, k, v = fp16_inputs(oracle, bs, h, n, d, 21)
+    ref, _ = oracle.block_sparse_sdpa(q, k, v, m, 128, 16)
+    qd, kd, vd = (to_dev(x, torch.float16) for x in (q, k, v))
+    b = sf.build_bsr(sf.generate_mask(terms), 128, 16)
+    for s in (torch.cuda.Stream(), torch.cuda.Stream()):  # eager, two streams
+        with torch.cuda.stream(s):
+            for _ in range(3):
+                out = sf.block_sparse_sdpa(qd, kd, vd, b, stream=s)
+        s.synchronize()
+        parity(out, ref)
+    s = torch.cuda.Stream()  # first seen inside the capture: its counter comes from the pool
+    out = torch.zeros_like(qd)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        sf.block_sparse_sdpa(qd, kd, vd, b, out=out, stream=s)
+    for _ in range(10):
+        out.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        parity(out, ref)
+    # rows beyond a short mask's last valid row block: empty row blocks come last in the order
+    mask_e = np.zeros((n, n), np.uint8)
+    mask_e[: n // 4, : n // 2] = 1
+    ref_e, _ = oracle.block_sparse_sdpa(q, k, v, mask_e, 128, 16)
+    be = sf.build_bsr(sf.DenseMask.from_numpy(mask_e), 128, 16)
+    for _ in range(3):
+        parity(sf.block_sparse_sdpa(qd, kd, vd, be), ref_e)
