@@ -231,10 +231,10 @@ typedef struct sf_attn_stats {               /* BlockExecStats, attention.hpp:60
  * with matching block sizes or SF_PLAN_ERROR is returned. Dispatches to the tcgen05/TMA kernel
  * when (block_m, block_n, head_size, dtype) is one it implements, else the generic
  * CUDA-core block kernel (any tile shape). The tcgen05 kernel balances its work items through a
- * work counter owned by the launch stream (taken from a per-device pool that sf_bsr_build or the
- * first launch outside a capture creates; reset by the kernel itself, so captured launches
- * replay): launches on one stream are ordered and share it, so a graph captured on stream S must
- * not be replayed concurrently with other tcgen05 attention launches on S. SF_ATTN_STATIC=1
+ * device work counter that the kernel resets itself: eager launches use the counter of their
+ * stream (ordered launches), every launch captured into a CUDA graph gets a private one (so
+ * graphs may be replayed concurrently on any streams, next to eager launches). Counters come from
+ * a per-device pool that sf_bsr_build or the first eager launch creates. SF_ATTN_STATIC=1
  * selects the counter-free static deal. */
 sf_status sf_mha_blockwise(const sf_attn_args* args, const sf_bsr_dev* bsr, const sf_plan* plan,
                            sf_attn_stats* stats, void* stream);

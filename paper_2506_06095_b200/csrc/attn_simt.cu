@@ -11,6 +11,7 @@
 //   reference accepts (the tcgen05 kernel in attn_tc.cu covers block_m = 128). One CTA per
 //   (row block, b*h); one thread per query row; K/V tiles staged through shared memory; the
 //   per-load-entry tile id (-1 = full) replaces the merge walk.
+#include <cmath>
 #include <algorithm>
 #include <type_traits>
 
@@ -410,6 +411,10 @@ sf_status check_attn_args(const sf_attn_args& a) {
         return fail(SF_SHAPE_ERROR, "empty attention input");                    // tensor.hpp:47
     if (!a.q || !a.k || !a.v || !a.o) return fail(SF_INVALID_PARAMETER, "null tensor pointer");
     if (a.dtype != SF_F16 && a.dtype != SF_BF16) return fail(SF_INVALID_PARAMETER, "dtype must be f16/bf16");
+    // 0 selects the reference's 1/sqrt(head_size) (attention.hpp:77); the tcgen05 softmax takes the
+    // row max of the raw scores, which commutes with a positive scale only
+    if (!(a.scale >= 0.f) || !std::isfinite(a.scale))
+        return fail(SF_INVALID_PARAMETER, "scale must be finite and >= 0 (0 = 1/sqrt(head_size))");
     return SF_OK;
 }
 

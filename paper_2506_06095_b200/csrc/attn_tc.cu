@@ -395,14 +395,13 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
                 const int j1 = min(nsteps, (c + 32) / G);
                 for (int j = c / G; j < j1; ++j, ++g) {
                     const int st = g % kStages;
-                    int parts = 0;
-                    int cols[G], tiles[G];
-#pragma unroll
-                    for (int gg = 0; gg < G; ++gg) {
-                        cols[gg] = __shfl_sync(0xffffffffu, my_col, j * G + gg - c);
-                        tiles[gg] = __shfl_sync(0xffffffffu, my_tile, j * G + gg - c);
-                        parts += tiles[gg] >= 0;
-                    }
+                    // lane gg < G owns column block gg of the step: its K / V boxes and bit tile
+                    // are issued from G lanes in parallel (one issuing thread sustains only one
+                    // 16-row TMA box per ~160 cycles; tools/micro/tma_gather.cu)
+                    const int src = j * G + static_cast<int>(lane % G) - c;
+                    const int gcol = __shfl_sync(0xffffffffu, my_col, src);
+                    const int gtile = __shfl_sync(0xffffffffu, my_tile, src);
+                    const int parts = __popc(__ballot_sync(0xffffffffu, lane < G && gtile >= 0));
                     const uint32_t ph = ((g / kStages) & 1) ^ 1;
                     if (lane == 0) {
                         SF_TRACE(g, 4);
@@ -415,8 +414,9 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
                     // part tiles' rows arrive by bulk copy from the pool
 #pragma unroll
                     for (int gg = 0; gg < G; ++gg) {
-                        if (tiles[gg] < 0) {
-                            const uint32_t fv = tiles[gg] == -1 ? ~0u : 0u;
+                        const int tg = __shfl_sync(0xffffffffu, gtile, gg);
+                        if (tg < 0) {
+                            const uint32_t fv = tg == -1 ? ~0u : 0u;
                             for (int c16 = static_cast<int>(lane); c16 < TB / 16; c16 += 32)
                                 asm volatile("st.shared.v4.b32 [%0], {%1, %1, %1, %1};" ::"r"(
                                                  tc::smem_u32(sMask + st * kMaskBytes + gg * TB + 16 * c16)),
@@ -425,29 +425,31 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
                         }
                     }
                     __syncwarp();
+                    if (lane == 0) tc::mbar_expect_tx(&k_full[st], kKVBytes + parts * TB);  // release: the filled bit rows
+                    __syncwarp();
+                    if (lane < G) {
+                        const int gg = static_cast<int>(lane);
+#pragma unroll
+                        for (int t = 0; t < Geo::kHeads; ++t)  // head t's 64 keys at t * 8 KB
+                            tma_load_4d(sK + st * kKVBytes + t * (kNS * kD * 2) + gg * BN * kD * 2, &p.tk, &k_full[st], 0,
+                                        gcol * BN, hh2[t], hb[t]);
+                        if (gtile >= 0)
+                            tc::bulk_load(sMask + st * kMaskBytes + gg * TB, p.pool + static_cast<int64_t>(gtile) * TB, TB,
+                                          &k_full[st]);
+                    }
                     if (lane == 0) {
-                        tc::mbar_expect_tx(&k_full[st], kKVBytes + parts * TB);  // release: the filled bit rows
-#pragma unroll
-                        for (int gg = 0; gg < G; ++gg) {
-                            const int col = cols[gg] * BN;
-#pragma unroll
-                            for (int t = 0; t < Geo::kHeads; ++t)  // head t's 64 keys at t * 8 KB
-                                tma_load_4d(sK + st * kKVBytes + t * (kNS * kD * 2) + gg * BN * kD * 2, &p.tk,
-                                            &k_full[st], 0, col, hh2[t], hb[t]);
-                            if (tiles[gg] >= 0)
-                                tc::bulk_load(sMask + st * kMaskBytes + gg * TB,
-                                              p.pool + static_cast<int64_t>(tiles[gg]) * TB, TB, &k_full[st]);
-                        }
                         SF_TRACE(g, 7);
                         tc::mbar_wait(&v_empty[st], ph);
                         SF_TRACE(g, 11);
                         tc::mbar_expect_tx(&v_full[st], kKVBytes);
+                    }
+                    __syncwarp();
+                    if (lane < G) {
+                        const int gg = static_cast<int>(lane);
 #pragma unroll
-                        for (int gg = 0; gg < G; ++gg)
-#pragma unroll
-                            for (int t = 0; t < Geo::kHeads; ++t)
-                                tma_load_4d(sV + st * kKVBytes + t * (kNS * kD * 2) + gg * BN * kD * 2, &p.tv,
-                                            &v_full[st], 0, cols[gg] * BN, hh2[t], hb[t]);
+                        for (int t = 0; t < Geo::kHeads; ++t)
+                            tma_load_4d(sV + st * kKVBytes + t * (kNS * kD * 2) + gg * BN * kD * 2, &p.tv, &v_full[st], 0,
+                                        gcol * BN, hh2[t], hb[t]);
                     }
                 }
             }
@@ -721,14 +723,18 @@ sf_status make_tmap_4d(CUtensorMap* map, const void* base, int n, int h, int bs,
 
 unsigned long long* g_attn_trace = nullptr;
 
-// The dynamic schedule's work counter, one per (device, stream): launches on one stream are
-// ordered (PDL included: the next launch's griddepcontrol.wait follows this one's reset), so they
-// can share it. Counters come from a per-device pool of zeroed pairs created outside any stream
-// capture (by sf_bsr_build, or by the first attention launch), so a stream first seen inside a
-// capture still gets one; with no pool (or the pool spent) the launch uses the static deal.
-// SF_ATTN_STATIC=1 forces the static deal.
+// The dynamic schedule's work counter (next item, CTAs done). The last CTA of a launch resets it,
+// so a counter is reusable by any later launch ordered after it, never by a concurrent one:
+//  * eager launches take the counter of their (device, stream): launches on one stream are
+//    ordered (PDL included: the next launch's griddepcontrol.wait follows this one's reset);
+//  * a launch captured into a CUDA graph takes a PRIVATE counter, used by nothing else: replays
+//    of one graph exec are ordered, but graphs captured on one stream may be replayed
+//    concurrently on different streams, and next to eager launches on their capture stream.
+// Counters come from a per-device pool of zeroed pairs created outside any capture (by
+// sf_bsr_build, or by the first eager attention launch); with the pool spent the launch uses the
+// static deal. SF_ATTN_STATIC=1 forces the static deal.
 namespace {
-constexpr int kCounterPool = 1024;
+constexpr int kCounterPool = 8192;
 std::mutex g_counter_mu;
 std::map<int, std::pair<unsigned*, int>> g_counter_pool;                // device -> (pool, next free)
 std::map<std::pair<int, cudaStream_t>, unsigned*> g_counters;          // (device, stream) -> counter
@@ -740,30 +746,37 @@ void reserve_pool_locked(int dev, cudaStream_t st) {  // st: not capturing
         cudaMemsetAsync(w, 0, kCounterPool * 2 * sizeof(unsigned), st) != cudaSuccess ||
         cudaStreamSynchronize(st) != cudaSuccess) {
         cudaGetLastError();
+        if (w) cudaFree(w);
         return;
     }
     g_counter_pool.emplace(dev, std::make_pair(w, 0));
 }
 
+unsigned* take_counter_locked(int dev) {
+    const auto pool = g_counter_pool.find(dev);
+    if (pool == g_counter_pool.end() || pool->second.second >= kCounterPool) return nullptr;
+    return pool->second.first + 2 * pool->second.second++;
+}
+
+bool attn_force_static() {
+    const char* e = std::getenv("SF_ATTN_STATIC");  // read per launch so tests can switch it
+    return e && *e == '1';
+}
+
 unsigned* attn_work_counter(cudaStream_t st) {
-    static const bool force_static = [] {
-        const char* e = std::getenv("SF_ATTN_STATIC");
-        return e && *e == '1';
-    }();
-    if (force_static) return nullptr;
+    if (attn_force_static()) return nullptr;
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess) return nullptr;
     std::lock_guard<std::mutex> lock(g_counter_mu);
+    if (cs != cudaStreamCaptureStatusNone) return take_counter_locked(dev);  // private to this graph node
     const auto key = std::make_pair(dev, st);
     const auto it = g_counters.find(key);
     if (it != g_counters.end()) return it->second;
-    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess) return nullptr;
-    if (cs == cudaStreamCaptureStatusNone) reserve_pool_locked(dev, st);
-    const auto pool = g_counter_pool.find(dev);
-    if (pool == g_counter_pool.end() || pool->second.second >= kCounterPool) return nullptr;
-    unsigned* w = pool->second.first + 2 * pool->second.second++;
-    g_counters.emplace(key, w);
+    reserve_pool_locked(dev, st);
+    unsigned* w = take_counter_locked(dev);
+    if (w) g_counters.emplace(key, w);
     return w;
 }
 }  // namespace
@@ -830,7 +843,10 @@ sf_status attn_tc(const sf_attn_args& a, const sf_bsr_dev& b, cudaStream_t st, b
         SF_CUDA_TRY(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
     }
     // persistent: two CTAs per SM (smem and TMEM are sized for it), items round-robin
-    dim3 grid(static_cast<unsigned>(std::min<int64_t>(p.n_items, 2 * n_sm)));
+    int64_t ctas = std::min<int64_t>(p.n_items, 2 * n_sm);
+    if (const char* e = std::getenv("SF_ATTN_MAX_CTAS"))  // test aid: many items per CTA at small shapes
+        ctas = std::max<int64_t>(1, std::min<int64_t>(ctas, std::atoll(e)));
+    dim3 grid(static_cast<unsigned>(ctas));
     SF_CUDA_TRY(launch_pdl(kern, grid, dim3(kThreads), smem, st, nullptr, p));
     SF_LAUNCH_CHECK();
     return SF_OK;

@@ -488,6 +488,7 @@ extern "C" sf_status sf_bsr_serialize(const sf_bsr_dev* b, uint8_t* buf, int64_t
                          static_cast<int64_t>(b->n_pool) * b->tile_bytes;
     if (nbytes) *nbytes = size;
     if (!buf) return SF_OK;
+    if (cap < size) return fail(SF_INVALID_PARAMETER, "buffer smaller than the SFBR dump (query the size first)");
     std::vector<int32_t> frp(rp), fci(b->n_full), prp(rp), pci(b->n_part), pti(b->n_part), lrp(rp), lci(b->n_load);
     std::vector<uint8_t> pool(static_cast<size_t>(b->n_pool) * b->tile_bytes);
     SF_TRY(sf_bsr_to_host(b, frp.data(), fci.data(), prp.data(), pci.data(), pti.data(), lrp.data(), lci.data(),
@@ -504,7 +505,7 @@ extern "C" sf_status sf_bsr_serialize(const sf_bsr_dev* b, uint8_t* buf, int64_t
     arr(frp); arr(fci); arr(prp); arr(pci); arr(pti); arr(lrp); arr(lci);
     u32(static_cast<uint32_t>(b->n_pool));
     o.insert(o.end(), pool.begin(), pool.end());
-    std::memcpy(buf, o.data(), static_cast<size_t>(imin64(cap, static_cast<int64_t>(o.size()))));
+    std::memcpy(buf, o.data(), o.size());
     return SF_OK;
 }
 

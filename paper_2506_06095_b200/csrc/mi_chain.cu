@@ -303,6 +303,11 @@ sf_status launch(int32_t M, int32_t N, const void* x, int64_t ldx, const sf_gemm
     T* op = static_cast<T*>(out);
     const int chunks = static_cast<int>(ceil_div(N, 32 * W));  // chunks of 32 lanes x W elements
     constexpr int kMax = 4096 / (32 * W);
+    // the row kernel keeps a row in registers (N <= 4096); vectorised elementwise chains run
+    // grid-stride at any width. A width limit is a backend limit, not a shape mismatch, so the
+    // search skips such candidates (search.hpp:339) instead of aborting.
+    if (chunks > kMax && (W != 8 || e.ln_gamma))
+        return fail(SF_BACKEND_ERROR, "mi_chain: LayerNorm / unaligned rows support N <= 4096");
     if constexpr (W == 8) {
         if (!e.ln_gamma) {
             launch_ew<T>(M, N, xp, ldx, e, op, ldout, st);
@@ -349,7 +354,6 @@ using namespace sf;
 extern "C" sf_status sf_mi_chain(int32_t M, int32_t N, int32_t dtype, const void* x, int64_t ldx,
                                  const sf_gemm_epilogue* epi, void* out, int64_t ldout, void* stream) {
     if (M < 1 || N < 1) return fail(SF_SHAPE_ERROR, "empty matrix");
-    if (N > 4096) return fail(SF_SHAPE_ERROR, "mi_chain supports N <= 4096");
     sf_gemm_epilogue e = epi ? *epi : sf_gemm_epilogue{};
     if (e.ln_gamma && !e.ln_beta) return fail(SF_INVALID_PARAMETER, "LayerNorm needs gamma and beta");
     cudaStream_t st = as_stream(stream);

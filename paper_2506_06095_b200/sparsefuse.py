@@ -99,8 +99,10 @@ class DenseMask:
         n = m.shape[0]
         dm = DenseMask.empty(n, device)
         u8 = torch.from_numpy(m).to(device)
-        check(lib().sf_mask_pack_u8(u8.data_ptr(), n, dm.bits.data_ptr(), _stream(stream)))
-        torch.cuda.current_stream().synchronize()
+        st = _stream(stream)
+        check(lib().sf_mask_pack_u8(u8.data_ptr(), n, dm.bits.data_ptr(), st))
+        # the temporary u8 copy must outlive the pack kernel on the stream it ran on
+        (stream if stream is not None else torch.cuda.current_stream()).synchronize()
         return dm
 
     def to_numpy(self) -> np.ndarray:
