@@ -91,7 +91,7 @@ struct AttnParams {
 #ifdef SF_ATTN_TRACE
 #define SF_TRACE(j, ev)                                                                   \
     do {                                                                                  \
-        if (p.trace && blockIdx.x == 0 && (j) < 64) p.trace[(j) * 16 + (ev)] = clock64(); \
+        if (p.trace && blockIdx.x == 0 && (j) < 64) p.trace[(j) * 32 + (ev)] = clock64(); \
     } while (0)
 #else
 #define SF_TRACE(j, ev) \
@@ -536,7 +536,9 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
                 const int st = g % kStages;
                 const int sb = g % kSBuf;
                 const bool tr = warp == 2 && lane == 0 && k == 0;
+                const bool trw = lane == 0 && k == 0;  // per-warp events 16 + 4 (warp - 2) + {0..3}
                 if (tr) SF_TRACE(j, 0);
+                if (trw) SF_TRACE(j, 16 + 4 * (warp - 2));
                 tc::mbar_wait(&k_full[st], (g / kStages) & 1);
                 if (tr) SF_TRACE(j, 1);
                 // this row's 64 mask bits (the producer staged every tile's rows: full -> ones,
@@ -558,6 +560,7 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
                 }
                 tc::mbar_wait(&s_full[sb], (g / kSBuf) & 1);
                 if (tr) SF_TRACE(j, 2);
+                if (trw) SF_TRACE(j, 17 + 4 * (warp - 2));
                 tc::fence_after_sync();
                 uint32_t raw0[32], raw1[32];
                 tc::tmem_ld32(trow + 64 * sb, raw0);
@@ -595,6 +598,7 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
                 // max of the raw scores, then scaled: scale > 0 commutes with max (log2 domain)
                 const float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * sl2;
                 if (tr) SF_TRACE(j, 3);
+                if (trw) SF_TRACE(j, 18 + 4 * (warp - 2));
                 // lazy max update: rescale O / l only when the max grows by > 2^8 (or first time).
                 // tcgen05.ld/st are warp-collective: the rescale is voted warp-uniformly and lanes
                 // that do not need it scale by 1.
@@ -648,6 +652,7 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
                 tc::fence_before_sync();
                 tc::mbar_arrive(&p_full[sb]);
                 if (tr) SF_TRACE(j, 6);
+                if (trw) SF_TRACE(j, 19 + 4 * (warp - 2));
             }
             // ---- epilogue: out = O / l; rows without a valid column stay zero
             const int slice = kPair ? 2 * bh + my_head : bh;
@@ -855,7 +860,7 @@ sf_status attn_tc(const sf_attn_args& a, const sf_bsr_dev& b, cudaStream_t st, b
 }  // namespace sf
 
 // Debug hook (not part of the boundary): record clock64 timestamps of CTA (0,0) of subsequent
-// tcgen05 attention launches into a device buffer of >= 64*16 uint64 (NULL disables).
+// tcgen05 attention launches into a device buffer of >= 64*32 uint64 (NULL disables).
 extern "C" sf_status sf_debug_attn_trace(void* dev_buf) {
     sf::g_attn_trace = static_cast<unsigned long long*>(dev_buf);
     return SF_OK;
