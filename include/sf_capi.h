@@ -149,6 +149,22 @@ sf_status sf_bsr_to_host(const sf_bsr_dev* bsr, int32_t* full_row_ptr, int32_t* 
 sf_status sf_bsr_serialize(const sf_bsr_dev* bsr, uint8_t* buf, int64_t cap, int64_t* nbytes,
                            void* stream);
 
+/* validate_bsr (bsr.hpp:104-153) on the device: SF_INTERNAL_INCONSISTENCY carrying the
+ * reference's message for the first violation it would throw. Synchronizes. */
+sf_status sf_bsr_validate(const sf_bsr_dev* bsr, void* stream);
+
+/* to_dense (bsr.hpp:155-177): validate, then expand the full / part tiles into a device bit mask
+ * of seq_len rows x sf_mask_words(seq_len) words (edge padding discarded). */
+sf_status sf_bsr_to_dense(const sf_bsr_dev* bsr, uint32_t* d_bits, void* stream);
+
+/* Device copy of host BSR arrays (e.g. a deserialised SFBR dump or a hand-built BsrMask);
+ * `pool` holds n_pool packed tiles of ceil(block_m*block_n/8) bytes. Release with sf_bsr_free. */
+sf_status sf_bsr_from_host(int32_t seq_len, int32_t block_m, int32_t block_n, int32_t n_full, int32_t n_part,
+                           int32_t n_load, int32_t n_pool, const int32_t* full_row_ptr, const int32_t* full_col_idx,
+                           const int32_t* part_row_ptr, const int32_t* part_col_idx, const int32_t* part_tile_ids,
+                           const int32_t* load_row_ptr, const int32_t* load_col_idx, const uint8_t* pool,
+                           sf_bsr_dev* out, void* stream);
+
 typedef struct sf_csr_dev {
     int32_t seq_len;
     int64_t nnz;
@@ -250,7 +266,8 @@ int32_t sf_get_attn_impl(void);
  * Fused segment templates (backend.hpp:109-306). GEMM operands fp16 (or bf16), row-major:
  * X (M x K), W^T stored as (N x K) row-major ("K-major", what TMA/tcgen05 read), out (M x N).
  * The epilogue applies, in order: +bias[N], activation, +aux[M x N] (residual Add),
- * LayerNorm over the full row (biased variance, eps 1e-5, backend.hpp:111,141-154).
+ * LayerNorm over the full row (biased variance, eps 1e-5, backend.hpp:111,141-154) or a row
+ * Softmax (max-subtracted, backend.hpp:155-167).
  * ---------------------------------------------------------------------------------------- */
 typedef enum sf_act { SF_ACT_NONE = 0, SF_ACT_GELU = 1, SF_ACT_RELU = 2 } sf_act;
 
@@ -262,6 +279,9 @@ typedef struct sf_gemm_epilogue {
     const void* ln_gamma;    /* N fp32 or NULL: LayerNorm after the residual */
     const void* ln_beta;     /* N fp32 */
     void* out_pre_ln;        /* optional second output: the pre-LN row (residual stream) */
+    int32_t softmax;         /* nonzero: row softmax after the residual (backend.hpp:155-167),
+                                exclusive with LayerNorm; in sf_gemm_fused it runs as a MiChain
+                                pass over the GEMM output */
 } sf_gemm_epilogue;
 
 #define SF_TILE_AUTO 0

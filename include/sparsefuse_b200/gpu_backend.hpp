@@ -1,11 +1,20 @@
-// gpu_backend.hpp — the B200 MeasurementBackend (backend.hpp:391-402): every segment of a fusion
-// scheme runs as the sm_100a fused templates and is timed on the device with CUDA events, with
-// the reference CpuBackend's protocol (3 warm-ups, best of 10; backend.hpp:443-500).
+// gpu_backend.hpp — the fused-template execution layer of the C++ host API (backend.hpp:20-500):
 //
-// Data are the reference's GraphData seeds (backend.hpp:61-107): identical fp32 values, rounded
-// once to fp16 on upload (weights stored transposed, N x K, the K-major operand of tcgen05).
-// The MHA unit follows exec_mha (backend.hpp:327-356): Q = K = V = the activation viewed as
-// (bs, heads, seq, head_size), executed by the plan's kernel (block-wise BSR or row-wise CSR).
+//   * Matrix / NodeParams / GraphData (backend.hpp:24-107): the reference's host data types and
+//     seeded parameters, bit-identical values;
+//   * MhaContext, exec_mha, exec_segment (backend.hpp:309-385): the reference signatures with host
+//     Matrix in / out; the segment runs on the B200 as the sm_100a fused templates (tcgen05 GEMMs
+//     with fused epilogues, the MiChain kernel, the masked-MHA kernels) through the C ABI;
+//   * DeviceChain: the same segment execution on device-resident fp16 activations (what a serving
+//     path or the search keeps on the GPU);
+//   * GpuBackend (backend.hpp:391-402): the MeasurementBackend whose segments are timed on the
+//     device with CUDA events, with the reference CpuBackend's protocol (3 warm-ups, best of 10;
+//     backend.hpp:443-500).
+//
+// Parameters are rounded once to fp16 on upload (weights stored transposed, N x K, the K-major
+// operand of tcgen05); LayerNorm / bias parameters stay fp32. The MHA unit follows exec_mha
+// (backend.hpp:327-356): Q = K = V = the activation viewed as (bs, heads, seq, head_size),
+// executed by the plan's kernel (block-wise BSR or row-wise CSR).
 #pragma once
 
 #include <cuda_fp16.h>
@@ -17,33 +26,49 @@
 
 namespace sparsefuse {
 
-// Host copy of GraphData::make(g, seed) (fp32, the reference's shapes and seeds).
-struct GraphData {
-    struct Node {
-        std::vector<float> weight;  // inner x cols (Gemm)
-        std::vector<float> bias, gamma, beta;
-        std::vector<float> aux;     // rows x cols (Add)
-    };
-    std::int64_t rows = 0, in_cols = 0;
-    std::vector<float> input;
-    std::vector<Node> params;
+// Row-major activation matrix, single precision (backend.hpp:24-40).
+struct Matrix {
+    std::int64_t rows = 0;
+    std::int64_t cols = 0;
+    std::vector<float> a;
 
-    static std::vector<float> random_matrix(std::int64_t r, std::int64_t c, std::uint64_t seed, float lo = -1.f, float hi = 1.f) {
-        std::vector<float> m(static_cast<std::size_t>(r * c));
-        std::mt19937_64 rng(seed);
-        for (auto& x : m) x = lo + static_cast<float>(unit_real(rng)) * (hi - lo);
-        return m;
-    }
+    Matrix() = default;
+    Matrix(std::int64_t r, std::int64_t c) : rows(r), cols(c), a(static_cast<std::size_t>(r) * static_cast<std::size_t>(c), 0.0f) {}
+    float& at(std::int64_t i, std::int64_t j) { return a[static_cast<std::size_t>(i * cols + j)]; }
+    float at(std::int64_t i, std::int64_t j) const { return a[static_cast<std::size_t>(i * cols + j)]; }
+};
+
+inline Matrix random_matrix(std::int64_t rows, std::int64_t cols, std::uint64_t seed, float lo = -1.0f, float hi = 1.0f) {
+    Matrix m(rows, cols);
+    std::mt19937_64 rng(seed);
+    for (auto& x : m.a) x = lo + static_cast<float>(unit_real(rng)) * (hi - lo);
+    return m;
+}
+
+// Per-node parameters and side inputs (backend.hpp:51-58).
+struct NodeParams {
+    Matrix weight;            // Gemm: (inner x cols)
+    std::vector<float> bias;  // Bias
+    std::vector<float> gamma; // LayerNorm scale
+    std::vector<float> beta;  // LayerNorm shift
+    Matrix aux;               // Add: recorded skip input
+};
+
+// GraphData::make(g, seed) (backend.hpp:60-107): the same seeds, the same values.
+struct GraphData {
+    Matrix input;
+    std::vector<NodeParams> params;
+
     static GraphData make(const OpGraph& g, std::uint64_t seed) {
         GraphData gd;
-        if (g.nodes.empty()) return gd;
-        const OpNode& first = g.nodes.front();
-        gd.rows = first.rows;
-        gd.in_cols = first.kind == OpKind::Gemm ? first.inner : first.cols;
-        gd.input = random_matrix(gd.rows, gd.in_cols, mix_seed(seed, 0xa11));
+        const std::int64_t rows = g.nodes.empty() ? 0 : g.nodes.front().rows;
+        const std::int64_t in_cols = g.nodes.empty() ? 0
+                                     : g.nodes.front().kind == OpKind::Gemm ? g.nodes.front().inner
+                                                                            : g.nodes.front().cols;
+        gd.input = random_matrix(rows, in_cols, mix_seed(seed, 0xa11));
         gd.params.resize(g.nodes.size());
         for (const auto& n : g.nodes) {
-            Node& p = gd.params[static_cast<std::size_t>(n.id)];
+            NodeParams& p = gd.params[static_cast<std::size_t>(n.id)];
             const std::uint64_t s = mix_seed(seed, static_cast<std::uint64_t>(n.id));
             std::mt19937_64 rng(s);
             if (n.kind == OpKind::Gemm) {
@@ -65,58 +90,136 @@ struct GraphData {
     }
 };
 
-class GpuBackend : public MeasurementBackend {
+// Attention context of a chain's MhaFused unit (backend.hpp:309-322): the session mask, its plan,
+// and the device format the plan's kernel walks (BSR at the plan's tile for block-wise plans, the
+// row-wise CSR otherwise; the reference keeps a 16 x 16 BSR for row-wise plans and always runs
+// its block executor).
+struct MhaContext {
+    DenseMask mask;
+    KernelPlan plan;
+    std::optional<BsrMask> bsr;
+    std::optional<RowwiseMask> rw;
+
+    static MhaContext make(const DenseMask& mask, const KernelPlan& plan) {
+        MhaContext ctx{mask, plan, {}, {}};
+        if (plan.kind == KernelKind::BlockWise) ctx.bsr = build_bsr(mask, plan.block_m, plan.block_n);
+        else ctx.rw = build_rowwise(mask);
+        return ctx;
+    }
+};
+
+namespace detail {
+inline DeviceBuffer<__half> to_dev_half(const std::vector<float>& v, cudaStream_t st = nullptr) {
+    std::vector<__half> h(v.size());
+    for (std::size_t i = 0; i < v.size(); ++i) h[i] = __float2half(v[i]);
+    DeviceBuffer<__half> d;
+    d.upload(h.data(), h.size(), st);
+    if (st) cuda_check(cudaStreamSynchronize(st), "upload");  // the staging vector dies here
+    return d;
+}
+inline DeviceBuffer<float> to_dev(const std::vector<float>& v) {
+    DeviceBuffer<float> d;
+    d.upload(v.data(), v.size());
+    return d;
+}
+inline Matrix to_host(const __half* d, std::int64_t rows, std::int64_t cols, cudaStream_t st) {
+    const std::size_t cnt = static_cast<std::size_t>(rows * cols);
+    std::vector<__half> h(cnt);
+    cuda_check(cudaMemcpyAsync(h.data(), d, cnt * 2, cudaMemcpyDeviceToHost, st), "D2H");
+    cuda_check(cudaStreamSynchronize(st), "sync");
+    Matrix m(rows, cols);
+    for (std::size_t i = 0; i < cnt; ++i) m.a[i] = __half2float(h[i]);
+    return m;
+}
+}  // namespace detail
+
+// Segment execution on device-resident fp16 activations: one graph's parameters uploaded once,
+// every template dispatched to the sm_100a kernels on one stream.
+class DeviceChain {
 public:
-    // `mask`/`plan` define the MHA unit (the session mask); without them the reference's default
-    // applies: an all-true mask (backend.hpp:458-467), planned here with the B200 selector.
-    GpuBackend(const OpGraph& g, std::uint64_t seed, std::optional<DenseMask> mask = {}, std::optional<KernelPlan> plan = {},
-               int warmups = 3, int repeats = 10)
-        : g_(g), warmups_(warmups), repeats_(repeats) {
-        cuda_check(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking), "stream");
-        cuda_check(cudaEventCreate(&e0_), "event");
-        cuda_check(cudaEventCreate(&e1_), "event");
-        upload(GraphData::make(g, seed));
-        const auto& hy = g.hyper;
-        if (std::any_of(g.nodes.begin(), g.nodes.end(), [](const OpNode& n) { return n.kind == OpKind::MhaFused; })) {
-            mask_ = mask ? std::move(*mask) : DenseMask(static_cast<int>(hy.seq_len), true);
-            plan_ = plan ? *plan
-                         : select_plan(*mask_, hw_preset("b200"), hy.seq_len, hy.heads, hy.bs, hy.head_size, PlanMode::B200);
-            if (plan_->kind == KernelKind::BlockWise) bsr_ = build_bsr(*mask_, plan_->block_m, plan_->block_n);
-            else rw_ = build_rowwise(*mask_);
+    // `only` (optional): upload just the parameters of nodes [only->begin, only->end).
+    DeviceChain(const OpGraph& g, const GraphData& gd, cudaStream_t st, const Segment* only = nullptr) : g_(g), st_(st) {
+        rows_ = gd.input.rows;
+        std::int64_t widest = gd.input.cols;
+        nodes_.resize(g_.nodes.size());
+        for (const auto& n : g_.nodes) {
+            widest = std::max(widest, n.cols);
+            if (only && (n.id < only->begin || n.id >= only->end)) continue;
+            const NodeParams& p = gd.params[static_cast<std::size_t>(n.id)];
+            DevNode& d = nodes_[static_cast<std::size_t>(n.id)];
+            if (n.kind == OpKind::Gemm) {  // inner x cols -> cols x inner (K-major)
+                if (p.weight.rows != n.inner || p.weight.cols != n.cols) throw shape_error("gemm weight shape mismatch");
+                std::vector<float> t(p.weight.a.size());
+                for (std::int64_t k = 0; k < n.inner; ++k)
+                    for (std::int64_t c = 0; c < n.cols; ++c)
+                        t[static_cast<std::size_t>(c * n.inner + k)] = p.weight.a[static_cast<std::size_t>(k * n.cols + c)];
+                d.w_nk = detail::to_dev_half(t);
+            }
+            if (!p.bias.empty()) d.bias = detail::to_dev(p.bias);
+            if (!p.gamma.empty()) { d.gamma = detail::to_dev(p.gamma); d.beta = detail::to_dev(p.beta); }
+            if (!p.aux.a.empty()) d.aux = detail::to_dev_half(p.aux.a);
+        }
+        widest_ = widest;
+        for (auto* b : {&mid_, &stage_}) b->resize(static_cast<std::size_t>(rows_ * widest_));
+        cuda_check(cudaDeviceSynchronize(), "upload");
+    }
+
+    void set_mha(const MhaContext* mha) { mha_ = mha; }
+    std::int64_t rows() const { return rows_; }
+    std::int64_t widest() const { return widest_; }
+    cudaStream_t stream() const { return st_; }
+
+    // Width of the activation feeding node idx along the chain.
+    std::int64_t in_cols(int idx) const {
+        if (idx == 0) return g_.nodes.front().kind == OpKind::Gemm ? g_.nodes.front().inner : g_.nodes.front().cols;
+        return g_.nodes[static_cast<std::size_t>(idx) - 1].cols;
+    }
+
+    // exec_segment (backend.hpp:360-385) on device buffers: x is rows x in_cols(seg.begin), y is
+    // rows x nodes[seg.end - 1].cols, both fp16 row-major.
+    void exec_segment(const Segment& seg, const Setting& s, const __half* x, __half* y) {
+        if (seg.begin < 0 || seg.end > static_cast<int>(g_.nodes.size()) || seg.begin >= seg.end)
+            throw illegal_segment("segment out of range");
+        if (g_.contains_mha(seg.begin, seg.end)) {
+            if (seg.length() != 1) throw backend_error("MhaFused segment must be a singleton");
+            if (!mha_) throw backend_error("MhaFused segment needs an attention context");
+            exec_mha(x, y);
+            return;
+        }
+        std::vector<int> gemms;
+        for (int i = seg.begin; i < seg.end; ++i)
+            if (g_.nodes[static_cast<std::size_t>(i)].kind == OpKind::Gemm) gemms.push_back(i);
+        const std::int64_t cols0 = in_cols(seg.begin);
+        if (gemms.empty()) {  // MiChain
+            mi(group_mi(seg.begin, seg.end), 0, cols0, x, y);
+            return;
+        }
+        if (gemms.size() > 2) throw illegal_segment("segment holds more than two CI operators");
+        const __half* src = x;
+        if (gemms[0] > seg.begin) {  // pre-MI ops applied to a staged copy of the input
+            mi(group_mi(seg.begin, gemms[0]), 0, cols0, x, stage_.data());
+            src = stage_.data();
+        }
+        if (gemms.size() == 1) {  // CiMi
+            gemm(gemms[0], s, group_mi(gemms[0] + 1, seg.end), src, y);
+        } else {  // CiCi: GEMM -> mid MI -> GEMM (intermediate in HBM, DESIGN §4)
+            gemm(gemms[0], s, group_mi(gemms[0] + 1, gemms[1]), src, mid_.data());
+            gemm(gemms[1], s, group_mi(gemms[1] + 1, seg.end), mid_.data(), y);
         }
     }
-    ~GpuBackend() override {
-        cudaStreamSynchronize(st_);
-        cudaEventDestroy(e0_);
-        cudaEventDestroy(e1_);
-        cudaStreamDestroy(st_);
-    }
 
-    double measure(const OpGraph& g, const FusionScheme&, const Segment& seg, const Setting& s) override {
-        check_graph(g);
-        const __half* in = activation(seg.begin);
-        return time_best([&] { exec_segment(seg, s, in, scratch_out_.data()); });
+    // exec_mha (backend.hpp:327-356) on device buffers.
+    void exec_mha(const __half* x, __half* y) {
+        const auto& hy = g_.hyper;
+        const std::int64_t H = static_cast<std::int64_t>(hy.heads) * hy.head_size;
+        if (rows_ != hy.bs * hy.seq_len || g_.nodes.front().rows != hy.bs * hy.seq_len)
+            throw shape_error("activation shape incompatible with MHA reshape");
+        if (mha_->mask.seq_len() != hy.seq_len) throw shape_error("MHA mask seq_len mismatch");
+        sf_attn_args a{static_cast<int32_t>(hy.bs), hy.heads, static_cast<int32_t>(hy.seq_len), hy.head_size, SF_F16,
+                       x, x, x, y, hy.seq_len * H, hy.head_size, H, hy.seq_len * H, hy.head_size, H, 0.f};
+        if (mha_->plan.kind == KernelKind::BlockWise) check(sf_mha_blockwise(&a, &mha_->bsr->device->d, nullptr, nullptr, st_));
+        else check(sf_mha_rowwise(&a, &mha_->rw->device->d, st_));
     }
-    double end_to_end(const OpGraph& g, const FusionScheme& scheme, const ParamAssignment& a) override {
-        check_graph(g);
-        return time_best([&] { run_scheme(scheme, a); });
-    }
-    std::string id() const override { return "b200"; }
-    double accept_margin() const override { return 0.01; }
-
-    // Full chain under a scheme/assignment; the final activation copied to host (fp32).
-    std::vector<float> run_chain(const OpGraph& g, const FusionScheme& scheme, const ParamAssignment& a) {
-        check_graph(g);
-        const __half* y = run_scheme(scheme, a);
-        const std::size_t cnt = static_cast<std::size_t>(g_.nodes.back().rows * g_.nodes.back().cols);
-        std::vector<__half> h(cnt);
-        cuda_check(cudaMemcpyAsync(h.data(), y, cnt * 2, cudaMemcpyDeviceToHost, st_), "D2H");
-        cuda_check(cudaStreamSynchronize(st_), "sync");
-        std::vector<float> out(cnt);
-        for (std::size_t i = 0; i < cnt; ++i) out[i] = __half2float(h[i]);
-        return out;
-    }
-    const std::optional<KernelPlan>& plan() const { return plan_; }
 
 private:
     struct DevNode {
@@ -124,81 +227,8 @@ private:
         DeviceBuffer<float> bias, gamma, beta;
     };
 
-    void check_graph(const OpGraph& g) const {
-        if (g.name != g_.name || g.size() != g_.size() || g.hyper.bs != g_.hyper.bs || g.hyper.seq_len != g_.hyper.seq_len)
-            throw backend_error("GpuBackend is bound to a different graph");
-    }
-
-    static DeviceBuffer<__half> to_dev_half(const std::vector<float>& v) {
-        std::vector<__half> h(v.size());
-        for (std::size_t i = 0; i < v.size(); ++i) h[i] = __float2half(v[i]);
-        DeviceBuffer<__half> d;
-        d.upload(h.data(), h.size());
-        return d;
-    }
-    static DeviceBuffer<float> to_dev(const std::vector<float>& v) {
-        DeviceBuffer<float> d;
-        d.upload(v.data(), v.size());
-        return d;
-    }
-
-    void upload(const GraphData& gd) {
-        rows_ = gd.rows;
-        std::int64_t widest = gd.in_cols;
-        nodes_.resize(g_.nodes.size());
-        for (const auto& n : g_.nodes) {
-            widest = std::max(widest, n.cols);
-            const auto& p = gd.params[static_cast<std::size_t>(n.id)];
-            DevNode& d = nodes_[static_cast<std::size_t>(n.id)];
-            if (n.kind == OpKind::Gemm) {  // inner x cols -> cols x inner (K-major)
-                std::vector<float> t(p.weight.size());
-                for (std::int64_t k = 0; k < n.inner; ++k)
-                    for (std::int64_t c = 0; c < n.cols; ++c) t[static_cast<std::size_t>(c * n.inner + k)] = p.weight[static_cast<std::size_t>(k * n.cols + c)];
-                d.w_nk = to_dev_half(t);
-            }
-            if (!p.bias.empty()) d.bias = to_dev(p.bias);
-            if (!p.gamma.empty()) { d.gamma = to_dev(p.gamma); d.beta = to_dev(p.beta); }
-            if (!p.aux.empty()) d.aux = to_dev_half(p.aux);
-        }
-        widest_ = widest;
-        input_ = to_dev_half(gd.input);
-        for (auto* b : {&ping_, &pong_, &mid_, &stage_, &scratch_out_})
-            b->resize(static_cast<std::size_t>(rows_ * widest_));
-        cuda_check(cudaDeviceSynchronize(), "upload");
-    }
-
-    // Activation feeding op idx along the unfused chain (default settings), memoised.
-    const __half* activation(int idx) {
-        if (acts_.empty()) acts_.emplace_back();  // slot 0 = the input
-        while (static_cast<int>(acts_.size()) <= idx) {
-            const int i = static_cast<int>(acts_.size());
-            const __half* src = i == 1 ? input_.data() : acts_.back().data();
-            DeviceBuffer<__half> out(static_cast<std::size_t>(rows_ * widest_));
-            const Segment one{i - 1, i};
-            exec_segment(one, default_setting(classify_segment(one, g_)), src, out.data());
-            acts_.push_back(std::move(out));
-        }
-        cuda_check(cudaStreamSynchronize(st_), "activation");
-        return idx == 0 ? input_.data() : acts_[static_cast<std::size_t>(idx)].data();
-    }
-
-    const __half* run_scheme(const FusionScheme& scheme, const ParamAssignment& a) {
-        const __half* x = input_.data();
-        bool flip = false;
-        for (const auto& seg : scheme.segments) {
-            const auto it = a.find(seg);
-            const Setting s = it != a.end() ? it->second : default_setting(classify_segment(seg, g_));
-            __half* y = flip ? pong_.data() : ping_.data();
-            exec_segment(seg, s, x, y);
-            x = y;
-            flip = !flip;
-        }
-        return x;
-    }
-
-    // ---- segment execution on the fused templates ----
-    // MI ops group into the epilogue order bias -> activation -> add -> layernorm; a run that
-    // breaks the order starts a new group (a further one-pass MI-chain launch).
+    // MI ops group into the epilogue order bias -> activation -> add -> row op (LayerNorm or
+    // Softmax); a run that breaks the order starts a new group (a further one-pass MiChain launch).
     struct Group {
         sf_gemm_epilogue e{};
         int rank = -1;
@@ -213,7 +243,7 @@ private:
                 case OpKind::Bias: rank = 0; break;
                 case OpKind::Gelu: case OpKind::Relu: rank = 1; break;
                 case OpKind::Add: rank = 2; break;
-                case OpKind::LayerNorm: rank = 3; break;
+                case OpKind::LayerNorm: case OpKind::Softmax: rank = 3; break;  // row ops (backend.hpp:113)
                 default: throw backend_error(std::string("no B200 template for MI op ") + to_string(n.kind));
             }
             if (out.empty() || rank <= out.back().rank) out.emplace_back();
@@ -224,6 +254,7 @@ private:
             if (n.kind == OpKind::Relu) gp.e.act = SF_ACT_RELU;
             if (n.kind == OpKind::Add) { gp.e.aux = d.aux.data(); gp.e.ldaux = n.cols; }
             if (n.kind == OpKind::LayerNorm) { gp.e.ln_gamma = d.gamma.data(); gp.e.ln_beta = d.beta.data(); }
+            if (n.kind == OpKind::Softmax) gp.e.softmax = 1;
         }
         return out;
     }
@@ -262,50 +293,150 @@ private:
         if (used < post.size()) mi(post, used, n.cols, y, y);
     }
 
-    void exec_segment(const Segment& seg, const Setting& s, const __half* x, __half* y) {
-        if (g_.contains_mha(seg.begin, seg.end)) {
-            if (seg.length() != 1) throw backend_error("MhaFused segment must be a singleton");
-            exec_mha(x, y);
-            return;
-        }
-        std::vector<int> gemms;
-        for (int i = seg.begin; i < seg.end; ++i)
-            if (g_.nodes[static_cast<std::size_t>(i)].kind == OpKind::Gemm) gemms.push_back(i);
-        const std::int64_t in_cols = seg.begin == 0 ? g_.nodes.front().kind == OpKind::Gemm ? g_.nodes.front().inner : g_.nodes.front().cols
-                                                    : g_.nodes[static_cast<std::size_t>(seg.begin) - 1].cols;
-        if (gemms.empty()) {  // MiChain
-            mi(group_mi(seg.begin, seg.end), 0, in_cols, x, y);
-            return;
-        }
-        if (gemms.size() > 2) throw illegal_segment("segment holds more than two CI operators");
-        const __half* src = x;
-        if (gemms[0] > seg.begin) {  // pre-MI ops applied to a staged copy of the input
-            mi(group_mi(seg.begin, gemms[0]), 0, in_cols, x, stage_.data());
-            src = stage_.data();
-        }
-        if (gemms.size() == 1) {  // CiMi
-            gemm(gemms[0], s, group_mi(gemms[0] + 1, seg.end), src, y);
-        } else {  // CiCi: GEMM -> mid MI -> GEMM (intermediate in HBM)
-            gemm(gemms[0], s, group_mi(gemms[0] + 1, gemms[1]), src, mid_.data());
-            gemm(gemms[1], s, group_mi(gemms[1] + 1, seg.end), mid_.data(), y);
+    OpGraph g_;
+    cudaStream_t st_{};
+    std::int64_t rows_ = 0, widest_ = 0;
+    std::vector<DevNode> nodes_;
+    DeviceBuffer<__half> mid_, stage_;
+    const MhaContext* mha_ = nullptr;
+};
+
+// exec_mha (backend.hpp:327-356) with the reference signature: host activation in, host result
+// out; the attention runs on the device with the context's plan.
+inline Matrix exec_mha(const OpNode& node, const GraphHyper& hyper, const MhaContext& ctx, const Matrix& in) {
+    (void)node;
+    const std::int64_t H = static_cast<std::int64_t>(hyper.heads) * hyper.head_size;
+    if (in.cols != H || in.rows != hyper.bs * hyper.seq_len) throw shape_error("activation shape incompatible with MHA reshape");
+    if (ctx.mask.seq_len() != hyper.seq_len) throw shape_error("MHA mask seq_len mismatch");
+    cudaStream_t st = nullptr;
+    const auto x = detail::to_dev_half(in.a);
+    DeviceBuffer<__half> y(static_cast<std::size_t>(in.rows * in.cols));
+    sf_attn_args a{static_cast<int32_t>(hyper.bs), hyper.heads, static_cast<int32_t>(hyper.seq_len), hyper.head_size, SF_F16,
+                   x.data(), x.data(), x.data(), y.data(), hyper.seq_len * H, hyper.head_size, H, hyper.seq_len * H,
+                   hyper.head_size, H, 0.f};
+    if (ctx.plan.kind == KernelKind::BlockWise) check(sf_mha_blockwise(&a, &ctx.bsr->device->d, nullptr, nullptr, st));
+    else check(sf_mha_rowwise(&a, &ctx.rw->device->d, st));
+    return detail::to_host(y.data(), in.rows, in.cols, st);
+}
+
+// exec_segment (backend.hpp:360-385) with the reference signature: the segment's parameters are
+// uploaded, the segment runs as the B200 templates, the result comes back as a host Matrix.
+inline Matrix exec_segment(const OpGraph& g, const GraphData& gd, const MhaContext* mha, const Segment& seg,
+                           const Setting& setting, const Matrix& in) {
+    if (seg.begin < 0 || seg.end > static_cast<int>(g.nodes.size()) || seg.begin >= seg.end)
+        throw illegal_segment("segment out of range");
+    if (g.contains_mha(seg.begin, seg.end)) {
+        if (seg.length() != 1) throw backend_error("MhaFused segment must be a singleton");
+        if (!mha) throw backend_error("MhaFused segment needs an attention context");
+        return exec_mha(g.nodes[static_cast<std::size_t>(seg.begin)], g.hyper, *mha, in);
+    }
+    cudaStream_t st = nullptr;
+    DeviceChain dc(g, gd, st, &seg);
+    if (in.rows != dc.rows() || in.cols != dc.in_cols(seg.begin)) throw shape_error("segment input shape mismatch");
+    const auto x = detail::to_dev_half(in.a);
+    const std::int64_t out_cols = g.nodes[static_cast<std::size_t>(seg.end) - 1].cols;
+    DeviceBuffer<__half> y(static_cast<std::size_t>(in.rows * std::max(out_cols, dc.widest())));
+    dc.exec_segment(seg, setting, x.data(), y.data());
+    return detail::to_host(y.data(), in.rows, out_cols, st);
+}
+
+class GpuBackend : public MeasurementBackend {
+public:
+    // `mask`/`plan` define the MHA unit (the session mask); without them the reference's default
+    // applies: an all-true mask (backend.hpp:458-467), planned here with the B200 selector.
+    // flush_l2: before every timed repeat, write a 256 MB buffer (outside the events) so each
+    // measurement starts from a cold L2 like bench.py's steps (a hot L2 flatters short segments).
+    GpuBackend(const OpGraph& g, std::uint64_t seed, std::optional<DenseMask> mask = {}, std::optional<KernelPlan> plan = {},
+               int warmups = 3, int repeats = 10, bool flush_l2 = true)
+        : g_(g), warmups_(warmups), repeats_(repeats), flush_l2_(flush_l2) {
+        cuda_check(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking), "stream");
+        cuda_check(cudaEventCreate(&e0_), "event");
+        cuda_check(cudaEventCreate(&e1_), "event");
+        const GraphData gd = GraphData::make(g, seed);
+        chain_ = std::make_unique<DeviceChain>(g_, gd, st_);
+        input_ = detail::to_dev_half(gd.input.a);
+        const std::size_t act = static_cast<std::size_t>(chain_->rows() * chain_->widest());
+        for (auto* b : {&ping_, &pong_, &scratch_out_}) b->resize(act);
+        const auto& hy = g.hyper;
+        if (std::any_of(g.nodes.begin(), g.nodes.end(), [](const OpNode& n) { return n.kind == OpKind::MhaFused; })) {
+            DenseMask m = mask ? std::move(*mask) : DenseMask(static_cast<int>(hy.seq_len), true);
+            const KernelPlan p = plan ? *plan
+                                      : select_plan(m, hw_preset("b200"), hy.seq_len, hy.heads, hy.bs, hy.head_size,
+                                                    PlanMode::B200);
+            mha_ = std::make_unique<MhaContext>(MhaContext::make(m, p));
+            chain_->set_mha(mha_.get());
         }
     }
+    ~GpuBackend() override {
+        cudaStreamSynchronize(st_);
+        cudaEventDestroy(e0_);
+        cudaEventDestroy(e1_);
+        cudaStreamDestroy(st_);
+    }
 
-    void exec_mha(const __half* x, __half* y) {
-        const auto& hy = g_.hyper;
-        const std::int64_t H = static_cast<std::int64_t>(hy.heads) * hy.head_size;
-        if (g_.nodes.front().rows != hy.bs * hy.seq_len) throw shape_error("activation shape incompatible with MHA reshape");
-        sf_attn_args a{static_cast<int32_t>(hy.bs), hy.heads, static_cast<int32_t>(hy.seq_len), hy.head_size, SF_F16,
-                       x, x, x, y, hy.seq_len * H, hy.head_size, H, hy.seq_len * H, hy.head_size, H, 0.f};
-        if (plan_->kind == KernelKind::BlockWise) check(sf_mha_blockwise(&a, &bsr_->device->d, nullptr, nullptr, st_));
-        else check(sf_mha_rowwise(&a, &rw_->device->d, st_));
+    double measure(const OpGraph& g, const FusionScheme&, const Segment& seg, const Setting& s) override {
+        check_graph(g);
+        const __half* in = activation(seg.begin);
+        return time_best([&] { chain_->exec_segment(seg, s, in, scratch_out_.data()); });
+    }
+    double end_to_end(const OpGraph& g, const FusionScheme& scheme, const ParamAssignment& a) override {
+        check_graph(g);
+        return time_best([&] { run_scheme(scheme, a); });
+    }
+    std::string id() const override { return "b200"; }
+    double accept_margin() const override { return 0.01; }
+
+    // Full chain under a scheme/assignment; the final activation copied to host (fp32).
+    std::vector<float> run_chain(const OpGraph& g, const FusionScheme& scheme, const ParamAssignment& a) {
+        check_graph(g);
+        const __half* y = run_scheme(scheme, a);
+        return detail::to_host(y, g_.nodes.back().rows, g_.nodes.back().cols, st_).a;
+    }
+    std::optional<KernelPlan> plan() const { return mha_ ? std::optional<KernelPlan>(mha_->plan) : std::nullopt; }
+    const MhaContext* mha() const { return mha_.get(); }
+
+private:
+    void check_graph(const OpGraph& g) const {
+        if (g.name != g_.name || g.size() != g_.size() || g.hyper.bs != g_.hyper.bs || g.hyper.seq_len != g_.hyper.seq_len)
+            throw backend_error("GpuBackend is bound to a different graph");
+    }
+
+    // Activation feeding op idx along the unfused chain (default settings), memoised.
+    const __half* activation(int idx) {
+        if (acts_.empty()) acts_.emplace_back();  // slot 0 = the input
+        while (static_cast<int>(acts_.size()) <= idx) {
+            const int i = static_cast<int>(acts_.size());
+            const __half* src = i == 1 ? input_.data() : acts_.back().data();
+            DeviceBuffer<__half> out(static_cast<std::size_t>(chain_->rows() * chain_->widest()));
+            const Segment one{i - 1, i};
+            chain_->exec_segment(one, default_setting(classify_segment(one, g_)), src, out.data());
+            acts_.push_back(std::move(out));
+        }
+        cuda_check(cudaStreamSynchronize(st_), "activation");
+        return idx == 0 ? input_.data() : acts_[static_cast<std::size_t>(idx)].data();
+    }
+
+    const __half* run_scheme(const FusionScheme& scheme, const ParamAssignment& a) {
+        const __half* x = input_.data();
+        bool flip = false;
+        for (const auto& seg : scheme.segments) {
+            const auto it = a.find(seg);
+            const Setting s = it != a.end() ? it->second : default_setting(classify_segment(seg, g_));
+            __half* y = flip ? pong_.data() : ping_.data();
+            chain_->exec_segment(seg, s, x, y);
+            x = y;
+            flip = !flip;
+        }
+        return x;
     }
 
     template <typename F>
     double time_best(F&& f) {
         for (int i = 0; i < warmups_; ++i) f();
         float best = std::numeric_limits<float>::infinity();
+        if (flush_l2_ && !flush_.size()) flush_.resize(kFlushBytes);
         for (int i = 0; i < repeats_; ++i) {
+            if (flush_l2_) cuda_check(cudaMemsetAsync(flush_.data(), i & 0xff, kFlushBytes, st_), "L2 flush");
             cuda_check(cudaEventRecord(e0_, st_), "event");
             f();
             cuda_check(cudaEventRecord(e1_, st_), "event");
@@ -317,18 +448,17 @@ private:
         return static_cast<double>(best) * 1e-3;  // seconds, like CpuBackend
     }
 
+    static constexpr std::size_t kFlushBytes = 256u << 20;  // > the 126 MB L2
     OpGraph g_;
     int warmups_, repeats_;
+    bool flush_l2_;
+    DeviceBuffer<std::uint8_t> flush_;
     cudaStream_t st_{};
     cudaEvent_t e0_{}, e1_{};
-    std::int64_t rows_ = 0, widest_ = 0;
-    std::vector<DevNode> nodes_;
-    DeviceBuffer<__half> input_, ping_, pong_, mid_, stage_, scratch_out_;
+    std::unique_ptr<DeviceChain> chain_;
+    std::unique_ptr<MhaContext> mha_;
+    DeviceBuffer<__half> input_, ping_, pong_, scratch_out_;
     std::vector<DeviceBuffer<__half>> acts_;
-    std::optional<DenseMask> mask_;
-    std::optional<KernelPlan> plan_;
-    std::optional<BsrMask> bsr_;
-    std::optional<RowwiseMask> rw_;
 };
 
 }  // namespace sparsefuse

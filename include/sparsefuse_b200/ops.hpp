@@ -243,6 +243,52 @@ inline RowwiseMask build_rowwise(const DenseMask& mask) {
     return r;
 }
 
+// Device copy of a host-constructed BsrMask (e.g. read from an SFBR dump); shape checks that the
+// packed device form cannot express are done here, with validate_bsr's messages.
+inline std::shared_ptr<BsrDevice> upload_bsr(const BsrMask& b) {
+    const std::size_t rp = static_cast<std::size_t>(b.n_rows) + 1;
+    if (b.full_row_ptr.size() != rp) throw internal_inconsistency("full: bad row_ptr shape");
+    if (b.part_row_ptr.size() != rp) throw internal_inconsistency("part: bad row_ptr shape");
+    if (b.load_row_ptr.size() != rp) throw internal_inconsistency("load: bad row_ptr shape");
+    if (b.part_tile_ids.size() != b.part_col_idx.size())
+        throw internal_inconsistency("part_tile_ids not parallel to part_col_idx");
+    const std::size_t nbits = static_cast<std::size_t>(b.block_m) * b.block_n, tb = (nbits + 7) / 8;
+    std::vector<std::uint8_t> packed;
+    packed.reserve(b.part_mask_pool.size() * tb);
+    for (const auto& t : b.part_mask_pool) {
+        if (t.size() != nbits) throw internal_inconsistency("pool tile has wrong size");
+        const auto p = pack_bits(t);
+        packed.insert(packed.end(), p.begin(), p.end());
+    }
+    auto dev = std::make_shared<BsrDevice>();
+    check(sf_bsr_from_host(b.seq_len, b.block_m, b.block_n, static_cast<int32_t>(b.full_col_idx.size()),
+                           static_cast<int32_t>(b.part_col_idx.size()), static_cast<int32_t>(b.load_col_idx.size()),
+                           static_cast<int32_t>(b.part_mask_pool.size()), b.full_row_ptr.data(), b.full_col_idx.data(),
+                           b.part_row_ptr.data(), b.part_col_idx.data(), b.part_tile_ids.data(), b.load_row_ptr.data(),
+                           b.load_col_idx.data(), packed.data(), &dev->d, nullptr));
+    return dev;
+}
+
+// validate_bsr (bsr.hpp:104-153): the structural checks run on the device copy; a mask whose host
+// arrays were edited after the build is re-uploaded first.
+inline void validate_bsr(const BsrMask& b, bool use_device_copy = false) {
+    if (use_device_copy && b.device) {
+        check(sf_bsr_validate(&b.device->d, nullptr));
+        return;
+    }
+    const auto dev = upload_bsr(b);
+    check(sf_bsr_validate(&dev->d, nullptr));
+}
+
+// to_dense (bsr.hpp:155-177): the exact inverse of build_bsr, expanded on the device.
+inline DenseMask to_dense(const BsrMask& b) {
+    const auto dev = upload_bsr(b);
+    DenseMask m(b.seq_len);
+    check(sf_bsr_to_dense(&dev->d, m.mutable_device_bits(), nullptr));
+    cuda_check(cudaDeviceSynchronize(), "to_dense");
+    return m;
+}
+
 struct BlockStats {  // bsr.hpp:179-196
     std::int64_t full_count = 0, part_count = 0, empty_count = 0;
     double valid_block_ratio = 0.0;

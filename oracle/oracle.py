@@ -250,6 +250,11 @@ class Oracle:
     def relu(self, x):
         x = np.ascontiguousarray(x, np.float32).copy(); self.lib.sfo_relu(_ptr(x, C.c_float), x.size); return x
 
+    def softmax(self, x):  # apply_row_op Softmax, backend.hpp:155-167
+        x = np.ascontiguousarray(x, np.float32).copy()
+        self.lib.sfo_softmax_rows(_ptr(x, C.c_float), x.shape[0], x.shape[1])
+        return x
+
     def layernorm(self, x, g, b):
         x = np.ascontiguousarray(x, np.float32).copy()
         g = np.ascontiguousarray(g, np.float32); b = np.ascontiguousarray(b, np.float32)
@@ -285,7 +290,37 @@ class Reference:
         L.ref_run_chain.argtypes = [C.c_char_p, C.c_int64, C.c_int64, C.c_int64, C.c_int, C.c_int, C.c_uint64,
                                     C.POINTER(C.c_uint8), C.c_int, C.c_int, C.c_char_p, C.POINTER(C.c_float), C.c_int]
         L.ref_exec_segment.argtypes = [C.c_char_p, C.c_int64, C.c_int64, C.c_int64, C.c_int, C.c_int, C.c_uint64,
-                                       C.c_int, C.c_int, C.POINTER(C.c_float), C.POINTER(C.c_float)]
+                                       C.c_int, C.c_int, C.POINTER(C.c_float), C.POINTER(C.c_float),
+                                       C.POINTER(C.c_uint8), C.c_int, C.c_int]
+
+    def exec_segment(self, model, bs, seq, hidden, heads, head_size, seed, seg, x, out_cols, mask=None, tile=(16, 16)):
+        """exec_segment (backend.hpp:360-385) of nodes [seg[0], seg[1]) of a preset or "spec:" graph on
+        GraphData(seed) (fp32, the reference's CPU executors); `mask` builds the MHA context."""
+        x = np.ascontiguousarray(x, np.float32)
+        out = np.zeros((x.shape[0], out_cols), np.float32)
+        m = None if mask is None else np.ascontiguousarray(mask, np.uint8)
+        st = self.lib.ref_exec_segment(model.encode(), bs, seq, hidden, heads, head_size, seed, seg[0], seg[1],
+                                       _ptr(x, C.c_float), _ptr(out, C.c_float),
+                                       None if m is None else _ptr(m, C.c_uint8), tile[0], tile[1])
+        if st:
+            raise ValueError(f"ref_exec_segment status {st}")
+        return out
+
+    def validate_bsr(self, seq_len, bm, bn, a: dict):
+        """validate_bsr of host arrays (keys as BsrMask.to_host(), `part_mask_pool` unpacked 0/1 tiles):
+        (status, message)."""
+        i32 = lambda k: np.ascontiguousarray(a[k], np.int32)
+        arrs = [i32(k) for k in ("full_row_ptr", "full_col_idx", "part_row_ptr", "part_col_idx", "part_tile_ids",
+                                 "load_row_ptr", "load_col_idx")]
+        pool = np.ascontiguousarray(a["part_mask_pool"], np.uint8).reshape(-1)
+        args = []
+        for x in arrs:
+            args += [_ptr(x, C.c_int32), x.size]
+        msg = C.create_string_buffer(256)
+        self.lib.ref_validate_bsr.argtypes = [C.c_int] * 3 + [C.POINTER(C.c_int32), C.c_int64] * 7 + [
+            C.POINTER(C.c_uint8), C.c_int64, C.c_char_p, C.c_int64]
+        st = self.lib.ref_validate_bsr(seq_len, bm, bn, *args, _ptr(pool, C.c_uint8), len(a["part_mask_pool"]), msg, 256)
+        return st, msg.value.decode()
 
     def mask(self, terms) -> np.ndarray:
         arr = terms_array(terms)

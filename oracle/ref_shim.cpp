@@ -298,14 +298,44 @@ int ref_run_chain(const char* model, int64_t bs, int64_t seq, int64_t hidden, in
     });
 }
 
-// exec_segment (backend.hpp:360) of one segment of a preset graph on GraphData(seed), fed the
-// chain activation at seg_begin; used to pin the fused-template restatement.
+// A preset graph, or "spec:<nodes>" — a linear chain over rows = bs*seq starting at width
+// `hidden`, nodes comma-separated: g<cols> Gemm (inner = current width), b Bias, a Add,
+// l LayerNorm, e Gelu, r Relu, s Softmax, m MhaFused. The same grammar is parsed by
+// tests/cpp/host_api_test.cpp for the C++ API under test.
+OpGraph graph_of(const std::string& model, const GraphHyper& hy) {
+    if (model.rfind("spec:", 0) != 0) return build_preset_graph(model, hy);
+    OpGraph g;
+    g.name = model;
+    g.hyper = hy;
+    const std::int64_t rows = hy.bs * hy.seq_len;
+    std::int64_t w = hy.hidden_dim;
+    std::stringstream ss(model.substr(5));
+    std::string tok;
+    while (std::getline(ss, tok, ',')) {
+        const int id = static_cast<int>(g.nodes.size());
+        switch (tok.at(0)) {
+            case 'g': { const std::int64_t c = std::stoll(tok.substr(1)); g.nodes.push_back({id, OpKind::Gemm, rows, c, w}); w = c; break; }
+            case 'b': g.nodes.push_back({id, OpKind::Bias, rows, w, 0}); break;
+            case 'a': g.nodes.push_back({id, OpKind::Add, rows, w, 0}); break;
+            case 'l': g.nodes.push_back({id, OpKind::LayerNorm, rows, w, 0}); break;
+            case 'e': g.nodes.push_back({id, OpKind::Gelu, rows, w, 0}); break;
+            case 'r': g.nodes.push_back({id, OpKind::Relu, rows, w, 0}); break;
+            case 's': g.nodes.push_back({id, OpKind::Softmax, rows, w, 0}); break;
+            case 'm': g.nodes.push_back({id, OpKind::MhaFused, rows, w, 0}); break;
+            default: throw invalid_parameter("bad graph spec token " + tok);
+        }
+    }
+    return g;
+}
+
+// exec_segment (backend.hpp:360) of one segment of a preset / spec graph on GraphData(seed), fed
+// `in`; with a mask (n x n uint8, may be null) the MHA context is built at block (bm, bn).
 int ref_exec_segment(const char* model, int64_t bs, int64_t seq, int64_t hidden, int heads,
                      int head_size, uint64_t seed, int seg_begin, int seg_end, const float* in,
-                     float* out) {
+                     float* out, const uint8_t* mask, int bm, int bn) {
     return guard([&] {
         GraphHyper hy{bs, seq, hidden, heads, head_size, 0};
-        const OpGraph g = build_preset_graph(model, hy);
+        const OpGraph g = graph_of(model, hy);
         const GraphData gd = GraphData::make(g, seed);
         const Segment seg{seg_begin, seg_end};
         const TemplateKind kind = classify_segment(seg, g);
@@ -314,7 +344,15 @@ int ref_exec_segment(const char* model, int64_t bs, int64_t seq, int64_t hidden,
                      ? g.nodes[static_cast<size_t>(seg_begin)].inner
                      : g.nodes[static_cast<size_t>(seg_begin)].cols);
         std::memcpy(x.a.data(), in, x.a.size() * 4);
-        const Matrix r = exec_segment(g, gd, nullptr, seg, default_setting(kind), x);
+        std::optional<MhaContext> ctx;
+        if (mask) {
+            KernelPlan plan;
+            plan.kind = KernelKind::BlockWise;
+            plan.block_m = bm;
+            plan.block_n = bn;
+            ctx = MhaContext::make(from_u8(mask, static_cast<int>(seq)), plan);
+        }
+        const Matrix r = exec_segment(g, gd, ctx ? &*ctx : nullptr, seg, default_setting(kind), x);
         std::memcpy(out, r.a.data(), r.a.size() * 4);
     });
 }
@@ -376,6 +414,41 @@ int ref_cache_session(const char* model, int64_t bs, int64_t seq, uint64_t model
         std::strncpy(out, str.c_str(), static_cast<size_t>(cap - 1));
         out[cap - 1] = '\0';
     });
+}
+
+// validate_bsr (bsr.hpp:104-153) of host arrays, e.g. a built BSR with one field corrupted: returns
+// the status and the exception message (empty when valid).
+int ref_validate_bsr(int seq_len, int bm, int bn, const int32_t* frp, int64_t n_frp, const int32_t* fci, int64_t n_fci,
+                     const int32_t* prp, int64_t n_prp, const int32_t* pci, int64_t n_pci, const int32_t* pti,
+                     int64_t n_pti, const int32_t* lrp, int64_t n_lrp, const int32_t* lci, int64_t n_lci,
+                     const uint8_t* pool_tiles, int64_t n_pool, char* msg, int64_t cap) {
+    msg[0] = '\0';
+    try {
+        BsrMask b;
+        b.seq_len = seq_len;
+        b.block_m = bm;
+        b.block_n = bn;
+        b.n_rows = (seq_len + bm - 1) / bm;
+        b.n_cols = (seq_len + bn - 1) / bn;
+        b.full_row_ptr.assign(frp, frp + n_frp);
+        b.full_col_idx.assign(fci, fci + n_fci);
+        b.part_row_ptr.assign(prp, prp + n_prp);
+        b.part_col_idx.assign(pci, pci + n_pci);
+        b.part_tile_ids.assign(pti, pti + n_pti);
+        b.load_row_ptr.assign(lrp, lrp + n_lrp);
+        b.load_col_idx.assign(lci, lci + n_lci);
+        const size_t tb = static_cast<size_t>(bm) * bn;
+        for (int64_t t = 0; t < n_pool; ++t)
+            b.part_mask_pool.emplace_back(pool_tiles + t * tb, pool_tiles + (t + 1) * tb);
+        validate_bsr(b);
+        return SF_OK;
+    } catch (const internal_inconsistency& e) {
+        std::strncpy(msg, e.what(), static_cast<size_t>(cap - 1));
+        msg[cap - 1] = '\0';
+        return SF_INTERNAL_INCONSISTENCY;
+    } catch (...) {
+        return SF_BACKEND_ERROR;
+    }
 }
 
 }  // extern "C"

@@ -82,7 +82,8 @@ class AttnStats(C.Structure):
 
 class GemmEpilogue(C.Structure):
     _fields_ = [("bias", C.c_void_p), ("act", C.c_int32), ("aux", C.c_void_p), ("ldaux", C.c_int64),
-                ("ln_gamma", C.c_void_p), ("ln_beta", C.c_void_p), ("out_pre_ln", C.c_void_p)]
+                ("ln_gamma", C.c_void_p), ("ln_beta", C.c_void_p), ("out_pre_ln", C.c_void_p),
+                ("softmax", C.c_int32)]
 
 
 class GemmArgs(C.Structure):
@@ -108,6 +109,9 @@ SIGNATURES = {
     "sf_bsr_free": (C.c_int, [C.POINTER(BsrDev), _P]),
     "sf_bsr_to_host": (C.c_int, [C.POINTER(BsrDev)] + [_P] * 8 + [_P]),
     "sf_bsr_serialize": (C.c_int, [C.POINTER(BsrDev), _P, _I64, C.POINTER(_I64), _P]),
+    "sf_bsr_validate": (C.c_int, [C.POINTER(BsrDev), _P]),
+    "sf_bsr_to_dense": (C.c_int, [C.POINTER(BsrDev), _P, _P]),
+    "sf_bsr_from_host": (C.c_int, [_I32] * 7 + [_P] * 8 + [C.POINTER(BsrDev), _P]),
     "sf_mask_serialize": (C.c_int, [_P, _I32, _P, _I64, C.POINTER(_I64), _P]),
     "sf_mask_deserialize": (C.c_int, [_P, _I64, C.POINTER(_I32), _P, _P]),
     "sf_rowwise_build": (C.c_int, [_P, _I32, C.POINTER(CsrDev), _P]),

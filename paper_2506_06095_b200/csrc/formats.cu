@@ -301,6 +301,161 @@ __global__ void row_compact_kernel(const uint32_t* __restrict__ bits, int32_t n,
     }
 }
 
+// ---- validate_bsr / to_dense (bsr.hpp:104-177) ----
+// The first violation the reference's validate_bsr would throw is the smallest 64-bit key
+// (check group, row, position): groups in the reference's order (full, part, load CSRs, then the
+// tile ids, the pool, the per-row union), rows ascending, within a CSR row "decreasing row_ptr"
+// before the entries' "out of range" / "not strictly increasing" in column order.
+enum : uint32_t {
+    kVFront = 0, kVDecr = 1, kVRange = 2, kVIncr = 3, kVLen = 4,        // per CSR group (x 5 + group)
+    kVIdRange = 15, kVPoolMixed = 16, kVLoadSum = 17, kVOverlap = 18, kVUnion = 19
+};
+__device__ __forceinline__ unsigned long long vkey(uint32_t group, int64_t row, uint32_t pos, uint32_t code) {
+    return (static_cast<unsigned long long>(group) << 58) | (static_cast<unsigned long long>(row & 0x3ffffff) << 32) |
+           (static_cast<unsigned long long>(pos & 0xffffff) << 8) | code;
+}
+
+struct VCsr {
+    const int32_t* ptr;
+    const int32_t* col;
+    int32_t len;
+};
+
+// one thread per (CSR, row): group g in {0 full, 1 part, 2 load}
+__global__ void validate_csr_kernel(VCsr f, VCsr pa, VCsr lo, int32_t n_rows, int32_t n_cols,
+                                    unsigned long long* err) {
+    const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= 3ll * (n_rows + 1)) return;
+    const uint32_t gi = static_cast<uint32_t>(t / (n_rows + 1));
+    const int64_t r = t - static_cast<int64_t>(gi) * (n_rows + 1);
+    const VCsr c = gi == 0 ? f : (gi == 1 ? pa : lo);
+    const uint32_t G = gi;  // key group
+    if (r == n_rows) {  // trailing checks of check_csr: front == 0, col length == ptr.back()
+        if (c.ptr[0] != 0) atomicMin(err, vkey(G, 0, 0, gi * 5 + kVFront));
+        if (c.ptr[n_rows] != c.len) atomicMin(err, vkey(G, n_rows, 0, gi * 5 + kVLen));
+        return;
+    }
+    const int32_t a = c.ptr[r], b = c.ptr[r + 1];
+    if (a > b) {
+        atomicMin(err, vkey(G, r, 0, gi * 5 + kVDecr));
+        return;
+    }
+    for (int32_t k = a; k < b; ++k) {
+        const uint32_t pos = static_cast<uint32_t>(k - a) * 2 + 1;
+        if (k < 0 || k >= c.len) {  // the reference would read past the column array here
+            atomicMin(err, vkey(G, n_rows, 0, gi * 5 + kVLen));
+            return;
+        }
+        const int32_t v = c.col[k];
+        if (v < 0 || v >= n_cols) {
+            atomicMin(err, vkey(G, r, pos, gi * 5 + kVRange));
+            return;
+        }
+        if (k > a && v <= c.col[k - 1]) {
+            atomicMin(err, vkey(G, r, pos + 1, gi * 5 + kVIncr));
+            return;
+        }
+    }
+}
+
+// tile ids in pool range (group 3), pool tiles mixed (group 4), per-row sum / disjointness /
+// union (group 5). Launched only when the three CSRs passed (their indices are then safe).
+__global__ void validate_rest_kernel(VCsr f, VCsr pa, VCsr lo, const int32_t* __restrict__ tile_ids, int32_t n_pool,
+                                     const uint8_t* __restrict__ pool, int32_t tile_bytes, int64_t nbits,
+                                     int32_t n_rows, unsigned long long* err) {
+    const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t < pa.len) {
+        const int32_t id = tile_ids[t];
+        if (id < 0 || id >= n_pool) atomicMin(err, vkey(3, 0, static_cast<uint32_t>(t), kVIdRange));
+    }
+    if (t < n_pool) {
+        int64_t ones = 0;
+        const uint8_t* tp = pool + t * tile_bytes;
+        for (int64_t byte = 0; byte * 8 < nbits; ++byte) {
+            uint32_t v = tp[byte];
+            const int64_t left = nbits - byte * 8;
+            if (left < 8) v &= (1u << left) - 1u;
+            ones += __popc(v);
+        }
+        if (ones == 0 || ones == nbits) atomicMin(err, vkey(4, t, 0, kVPoolMixed));
+    }
+    if (t < n_rows) {
+        const int32_t f0 = f.ptr[t], f1 = f.ptr[t + 1], p0 = pa.ptr[t], p1 = pa.ptr[t + 1];
+        const int32_t l0 = lo.ptr[t], l1 = lo.ptr[t + 1];
+        if (l1 != f1 + p1) {  // the reference compares the raw prefix values
+            atomicMin(err, vkey(5, t, 0, kVLoadSum));
+            return;
+        }
+        // both lists are strictly increasing (checked): merge, look for a common column, then
+        // compare the merged run with the load row
+        int32_t i = f0, j = p0, k = l0;
+        uint32_t code = 0;
+        while (i < f1 || j < p1) {
+            int32_t v;
+            if (j >= p1 || (i < f1 && f.col[i] < pa.col[j])) v = f.col[i++];
+            else if (i >= f1 || pa.col[j] < f.col[i]) v = pa.col[j++];
+            else { code = kVOverlap; break; }
+            if (code == 0 && (k >= l1 || lo.col[k] != v)) code = kVUnion;
+            ++k;
+        }
+        if (code == 0 && k != l1) code = kVUnion;
+        // std::equal(merged, load + ptr[r]) only reads merged.size() load entries: a longer load
+        // row passes the union check itself (the sum check above already fixed the lengths)
+        if (code) atomicMin(err, vkey(5, t, 0, code));
+    }
+}
+
+// to_dense: one thread per (full or part entry, tile row); ORs the row's block_n bits into the
+// bit-packed mask (neighbouring tiles may share a 32-bit word)
+__global__ void to_dense_kernel(const int32_t* __restrict__ frp, const int32_t* __restrict__ fci, int32_t n_full,
+                                const int32_t* __restrict__ prp, const int32_t* __restrict__ pci,
+                                const int32_t* __restrict__ pti, int32_t n_part, const uint8_t* __restrict__ pool,
+                                int32_t tile_bytes, Geo g, uint32_t* __restrict__ out) {
+    const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t entries = static_cast<int64_t>(n_full) + n_part;
+    if (t >= entries * g.bm) return;
+    const int64_t e = t / g.bm;
+    const int di = static_cast<int>(t - e * g.bm);
+    const bool full = e < n_full;
+    const int64_t k = full ? e : e - n_full;
+    const int32_t* rp = full ? frp : prp;
+    // row block of entry k: the last row whose pointer is <= k (binary search)
+    int lo_ = 0, hi_ = g.n_rows;
+    while (hi_ - lo_ > 1) {
+        const int mid = (lo_ + hi_) >> 1;
+        if (rp[mid] <= k) lo_ = mid; else hi_ = mid;
+    }
+    const int64_t br = lo_;
+    const int64_t bc = full ? fci[k] : pci[k];
+    const int64_t i = br * g.bm + di;
+    if (i >= g.n) return;
+    const uint8_t* tile = full ? nullptr : pool + static_cast<int64_t>(pti[k]) * tile_bytes;
+    uint32_t* row = out + i * g.words;
+    for (int dj0 = 0; dj0 < g.bn; dj0 += 32) {
+        const int64_t j0 = bc * g.bn + dj0;
+        if (j0 >= g.n) break;
+        const int len = static_cast<int>(imin64(imin64(32, g.bn - dj0), g.n - j0));
+        uint32_t v;
+        if (full) {
+            v = len == 32 ? ~0u : ((1u << len) - 1u);
+        } else {  // bits [di*bn + dj0, +len) of the LSB-first packed tile
+            const int64_t b0 = static_cast<int64_t>(di) * g.bn + dj0;
+            uint64_t w = 0;
+            for (int q = 0; q < 5; ++q) {
+                const int64_t byte = (b0 >> 3) + q;
+                if (byte < tile_bytes) w |= static_cast<uint64_t>(tile[byte]) << (8 * q);
+            }
+            v = static_cast<uint32_t>(w >> (b0 & 7));
+            if (len < 32) v &= (1u << len) - 1u;
+        }
+        // place bits j0..j0+len-1 into the row's words
+        const int64_t w0 = j0 >> 5;
+        const int sh = static_cast<int>(j0 & 31);
+        if (v << sh) atomicOr(&row[w0], v << sh);
+        if (sh && sh + len > 32 && (v >> (32 - sh))) atomicOr(&row[w0 + 1], v >> (32 - sh));
+    }
+}
+
 template <typename T>
 T* carve(char*& p, int64_t count) {
     T* r = reinterpret_cast<T*>(p);
@@ -557,5 +712,137 @@ extern "C" sf_status sf_csr_to_host(const sf_csr_dev* csr, int32_t* row_ptr, int
     if (col_idx && csr->nnz > 0)
         SF_CUDA_TRY(cudaMemcpyAsync(col_idx, csr->col_idx, csr->nnz * 4ll, cudaMemcpyDeviceToHost, st));
     SF_CUDA_TRY(cudaStreamSynchronize(st));
+    return SF_OK;
+}
+
+static const char* validate_message(unsigned long long key) {
+    const uint32_t code = static_cast<uint32_t>(key & 0xff);
+    static const char* csr_msg[5] = {"bad row_ptr shape", "decreasing row_ptr", "col out of range",
+                                     "cols not strictly increasing", "col length mismatch"};
+    static const char* what[3] = {"full: ", "part: ", "load: "};
+    static thread_local std::string m;
+    if (code < 15) {
+        m = std::string(what[code / 5]) + csr_msg[code % 5];
+        return m.c_str();
+    }
+    switch (code) {
+        case kVIdRange: return "part tile id out of pool range";
+        case kVPoolMixed: return "pool tile is not mixed";
+        case kVLoadSum: return "load_row_ptr is not the sum of full and part";
+        case kVOverlap: return "full and part columns overlap";
+        default: return "load columns are not the union of full and part";
+    }
+}
+
+extern "C" sf_status sf_bsr_validate(const sf_bsr_dev* b, void* stream) {
+    if (!b || !b->full_row_ptr || !b->part_row_ptr || !b->load_row_ptr)
+        return fail(SF_INVALID_PARAMETER, "null BSR");
+    if (b->n_rows < 0 || b->n_cols < 0 || b->block_m < 1 || b->block_n < 1)
+        return fail(SF_INTERNAL_INCONSISTENCY, "full: bad row_ptr shape");
+    cudaStream_t st = as_stream(stream);
+    unsigned long long* err = nullptr;
+    SF_CUDA_TRY(pool_malloc(reinterpret_cast<void**>(&err), 8, st));
+    SF_CUDA_TRY(cudaMemsetAsync(err, 0xff, 8, st));
+    const VCsr f{b->full_row_ptr, b->full_col_idx, b->n_full}, pa{b->part_row_ptr, b->part_col_idx, b->n_part},
+        lo{b->load_row_ptr, b->load_col_idx, b->n_load};
+    validate_csr_kernel<<<blocks_for(3ll * (b->n_rows + 1)), 256, 0, st>>>(f, pa, lo, b->n_rows, b->n_cols, err);
+    SF_LAUNCH_CHECK();
+    unsigned long long h = ~0ull;
+    SF_CUDA_TRY(cudaMemcpyAsync(&h, err, 8, cudaMemcpyDeviceToHost, st));
+    SF_CUDA_TRY(cudaStreamSynchronize(st));
+    if (h == ~0ull) {
+        const int64_t span = imax64(imax64(b->n_part, b->n_pool), b->n_rows);
+        validate_rest_kernel<<<blocks_for(span), 256, 0, st>>>(
+            f, pa, lo, b->part_tile_ids, b->n_pool, b->pool, b->tile_bytes,
+            static_cast<int64_t>(b->block_m) * b->block_n, b->n_rows, err);
+        SF_LAUNCH_CHECK();
+        SF_CUDA_TRY(cudaMemcpyAsync(&h, err, 8, cudaMemcpyDeviceToHost, st));
+        SF_CUDA_TRY(cudaStreamSynchronize(st));
+    }
+    SF_CUDA_TRY(cudaFreeAsync(err, st));
+    if (h != ~0ull) return fail(SF_INTERNAL_INCONSISTENCY, validate_message(h));
+    return SF_OK;
+}
+
+extern "C" sf_status sf_bsr_to_dense(const sf_bsr_dev* b, uint32_t* d_bits, void* stream) {
+    SF_TRY(sf_bsr_validate(b, stream));  // to_dense validates first (bsr.hpp:156)
+    if (!d_bits) return fail(SF_INVALID_PARAMETER, "null output mask");
+    cudaStream_t st = as_stream(stream);
+    const Geo g{b->seq_len, sf_mask_words(b->seq_len), b->block_m, b->block_n, b->n_rows, b->n_cols};
+    SF_CUDA_TRY(cudaMemsetAsync(d_bits, 0, static_cast<size_t>(b->seq_len) * g.words * 4, st));
+    const int64_t work = (static_cast<int64_t>(b->n_full) + b->n_part) * b->block_m;
+    if (work > 0) {
+        to_dense_kernel<<<blocks_for(work), 256, 0, st>>>(b->full_row_ptr, b->full_col_idx, b->n_full, b->part_row_ptr,
+                                                           b->part_col_idx, b->part_tile_ids, b->n_part, b->pool,
+                                                           b->tile_bytes, g, d_bits);
+        SF_LAUNCH_CHECK();
+    }
+    return SF_OK;
+}
+
+// Device copy of host BSR arrays (a deserialised or hand-built BsrMask). load_tile is derived on
+// the host from the full / part lists (-1 where a load column is not a part column).
+extern "C" sf_status sf_bsr_from_host(int32_t seq_len, int32_t block_m, int32_t block_n, int32_t n_full, int32_t n_part,
+                                      int32_t n_load, int32_t n_pool, const int32_t* full_row_ptr,
+                                      const int32_t* full_col_idx, const int32_t* part_row_ptr,
+                                      const int32_t* part_col_idx, const int32_t* part_tile_ids,
+                                      const int32_t* load_row_ptr, const int32_t* load_col_idx, const uint8_t* pool,
+                                      sf_bsr_dev* out, void* stream) {
+    if (!out) return fail(SF_INVALID_PARAMETER, "null output");
+    *out = sf_bsr_dev{};
+    if (seq_len < 1 || block_m < 1 || block_n < 1) return fail(SF_INVALID_PARAMETER, "bad BSR geometry");
+    if (n_full < 0 || n_part < 0 || n_load < 0 || n_pool < 0) return fail(SF_INVALID_PARAMETER, "negative BSR counts");
+    cudaStream_t st = as_stream(stream);
+    const int32_t n_rows = static_cast<int32_t>(ceil_div(seq_len, block_m));
+    const int32_t tile_bytes = static_cast<int32_t>(ceil_div(static_cast<int64_t>(block_m) * block_n, 8));
+    const int64_t rp = n_rows + 1;
+    std::vector<int32_t> load_tile(static_cast<size_t>(std::max(1, n_load)), -1);
+    for (int64_t r = 0; r < n_rows; ++r) {  // map each load column to its part pool id, if any
+        const int32_t p0 = part_row_ptr[r], p1 = part_row_ptr[r + 1];
+        for (int32_t k = load_row_ptr[r]; k < load_row_ptr[r + 1] && k < n_load; ++k)
+            for (int32_t q = std::max(0, p0); q < p1 && q < n_part; ++q)
+                if (part_col_idx[q] == load_col_idx[k]) load_tile[static_cast<size_t>(k)] = part_tile_ids[q];
+    }
+    const int64_t out_bytes = 3 * ceil_div(rp * 4, 256) * 256 + ceil_div(std::max(1, n_full) * 4ll, 256) * 256 +
+                              2 * ceil_div(std::max(1, n_part) * 4ll, 256) * 256 +
+                              2 * ceil_div(std::max(1, n_load) * 4ll, 256) * 256 +
+                              ceil_div(imax64(1, static_cast<int64_t>(n_pool) * tile_bytes), 256) * 256;
+    char* ob = nullptr;
+    SF_CUDA_TRY(pool_malloc(reinterpret_cast<void**>(&ob), out_bytes, st));
+    char* p = ob;
+    out->full_row_ptr = carve<int32_t>(p, rp);
+    out->part_row_ptr = carve<int32_t>(p, rp);
+    out->load_row_ptr = carve<int32_t>(p, rp);
+    out->full_col_idx = carve<int32_t>(p, std::max(1, n_full));
+    out->part_col_idx = carve<int32_t>(p, std::max(1, n_part));
+    out->part_tile_ids = carve<int32_t>(p, std::max(1, n_part));
+    out->load_col_idx = carve<int32_t>(p, std::max(1, n_load));
+    out->load_tile = carve<int32_t>(p, std::max(1, n_load));
+    out->pool = carve<uint8_t>(p, imax64(1, static_cast<int64_t>(n_pool) * tile_bytes));
+    out->_alloc = ob;
+    auto up = [&](void* dst, const void* src, int64_t bytes) -> sf_status {
+        if (bytes > 0 && src) SF_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
+        return SF_OK;
+    };
+    SF_TRY(up(out->full_row_ptr, full_row_ptr, rp * 4));
+    SF_TRY(up(out->part_row_ptr, part_row_ptr, rp * 4));
+    SF_TRY(up(out->load_row_ptr, load_row_ptr, rp * 4));
+    SF_TRY(up(out->full_col_idx, full_col_idx, n_full * 4ll));
+    SF_TRY(up(out->part_col_idx, part_col_idx, n_part * 4ll));
+    SF_TRY(up(out->part_tile_ids, part_tile_ids, n_part * 4ll));
+    SF_TRY(up(out->load_col_idx, load_col_idx, n_load * 4ll));
+    SF_TRY(up(out->load_tile, load_tile.data(), n_load * 4ll));
+    SF_TRY(up(out->pool, pool, static_cast<int64_t>(n_pool) * tile_bytes));
+    SF_CUDA_TRY(cudaStreamSynchronize(st));  // the host staging vector dies here
+    out->seq_len = seq_len;
+    out->block_m = block_m;
+    out->block_n = block_n;
+    out->n_rows = n_rows;
+    out->n_cols = static_cast<int32_t>(ceil_div(seq_len, block_n));
+    out->n_full = n_full;
+    out->n_part = n_part;
+    out->n_load = n_load;
+    out->n_pool = n_pool;
+    out->tile_bytes = tile_bytes;
     return SF_OK;
 }

@@ -446,7 +446,19 @@ extern "C" sf_status sf_gemm_fused(const sf_gemm_args* a, void* stream) {
     if ((reinterpret_cast<uintptr_t>(a->x) | reinterpret_cast<uintptr_t>(a->w) | reinterpret_cast<uintptr_t>(a->out)) & 15)
         return fail(SF_INVALID_PARAMETER, "GEMM operands must be 16-byte aligned");
     if (a->epi.ln_gamma && !a->epi.ln_beta) return fail(SF_INVALID_PARAMETER, "LayerNorm needs gamma and beta");
+    if (a->epi.softmax && (a->epi.ln_gamma || a->epi.out_pre_ln))
+        return fail(SF_INVALID_PARAMETER, "Softmax excludes LayerNorm / out_pre_ln");
     cudaStream_t st = as_stream(stream);
+    if (a->epi.softmax) {
+        // the row softmax needs the whole row's max and sum: GEMM (+bias/act/residual), then a
+        // MiChain softmax pass over the output in place (the split LayerNorm path's shape)
+        sf_gemm_args g = *a;
+        g.epi.softmax = 0;
+        SF_TRY(sf_gemm_fused(&g, stream));
+        sf_gemm_epilogue e{};
+        e.softmax = 1;
+        return sf_mi_chain(a->M, a->N, a->dtype, a->out, a->ldout, &e, a->out, a->ldout, stream);
+    }
     if (a->dtype == SF_F16) return gemm_dispatch<__half>(*a, st);
     if (a->dtype == SF_BF16) return gemm_dispatch<__nv_bfloat16>(*a, st);
     return fail(SF_INVALID_PARAMETER, "dtype must be f16/bf16");

@@ -1,5 +1,6 @@
 // mi_chain.cu — the MiChain template (backend.hpp:228-235): a run of memory-intensive ops
-// (Bias, GELU/ReLU, Add, LayerNorm) applied to each row in ONE pass over HBM.
+// (Bias, GELU/ReLU, Add, then a LayerNorm or Softmax row op) applied to each row in ONE pass
+// over HBM.
 //
 // One warp per row, 8 rows per 256-thread CTA. Each lane holds chunks of 8 consecutive
 // elements (16-byte vector loads/stores; a scalar variant covers ragged widths), so a row is read once and written once however many
@@ -19,6 +20,11 @@ __device__ __forceinline__ float gelu_erf(float x) { return gelu_fast(x); }  // 
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
     for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
     return v;
 }
 
@@ -83,7 +89,33 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) mi_chain_kernel(int32_t M, 
             for (int i = 0; i < W; ++i) v[k][i] = 0.f;
         }
     }
-    if (e.ln_gamma) {
+    if (e.softmax) {  // apply_row_op Softmax (backend.hpp:155-167): max, exp(x - max), / sum
+        float m = -INFINITY;
+#pragma unroll
+        for (int k = 0; k < V; ++k)
+            if ((k * 32 + lane) * W < N)
+#pragma unroll
+                for (int i = 0; i < W; ++i) m = fmaxf(m, v[k][i]);
+        m = warp_max(m);
+        float s = 0.f;
+#pragma unroll
+        for (int k = 0; k < V; ++k)
+            if ((k * 32 + lane) * W < N)
+#pragma unroll
+                for (int i = 0; i < W; ++i) {
+                    v[k][i] = __expf(v[k][i] - m);
+                    s += v[k][i];
+                }
+        const float inv = 1.0f / warp_sum(s);
+#pragma unroll
+        for (int k = 0; k < V; ++k) {
+            const int c = (k * 32 + lane) * W;
+            if (c >= N) continue;
+#pragma unroll
+            for (int i = 0; i < W; ++i) v[k][i] *= inv;
+            storew<T, W>(out + row * ldout + c, v[k]);
+        }
+    } else if (e.ln_gamma) {
         float s = 0.f;
 #pragma unroll
         for (int k = 0; k < V; ++k)
@@ -306,15 +338,16 @@ sf_status launch(int32_t M, int32_t N, const void* x, int64_t ldx, const sf_gemm
     // the row kernel keeps a row in registers (N <= 4096); vectorised elementwise chains run
     // grid-stride at any width. A width limit is a backend limit, not a shape mismatch, so the
     // search skips such candidates (search.hpp:339) instead of aborting.
-    if (chunks > kMax && (W != 8 || e.ln_gamma))
-        return fail(SF_BACKEND_ERROR, "mi_chain: LayerNorm / unaligned rows support N <= 4096");
+    const bool row_op = e.ln_gamma || e.softmax;
+    if (chunks > kMax && (W != 8 || row_op))
+        return fail(SF_BACKEND_ERROR, "mi_chain: LayerNorm / Softmax / unaligned rows support N <= 4096");
     if constexpr (W == 8) {
-        if (!e.ln_gamma) {
+        if (!row_op) {
             launch_ew<T>(M, N, xp, ldx, e, op, ldout, st);
             SF_LAUNCH_CHECK();
             return SF_OK;
         }
-        if (chunks <= 4) {
+        if (chunks <= 4 && !e.softmax) {
             if (chunks == 1) launch_rows<T, 1>(M, N, xp, ldx, e, op, ldout, st);
             else if (chunks == 2) launch_rows<T, 2>(M, N, xp, ldx, e, op, ldout, st);
             else if (chunks == 3) launch_rows<T, 3>(M, N, xp, ldx, e, op, ldout, st);
@@ -356,6 +389,8 @@ extern "C" sf_status sf_mi_chain(int32_t M, int32_t N, int32_t dtype, const void
     if (M < 1 || N < 1) return fail(SF_SHAPE_ERROR, "empty matrix");
     sf_gemm_epilogue e = epi ? *epi : sf_gemm_epilogue{};
     if (e.ln_gamma && !e.ln_beta) return fail(SF_INVALID_PARAMETER, "LayerNorm needs gamma and beta");
+    if (e.ln_gamma && e.softmax) return fail(SF_INVALID_PARAMETER, "LayerNorm and Softmax are separate row ops");
+    if (e.softmax && e.out_pre_ln) return fail(SF_INVALID_PARAMETER, "out_pre_ln belongs to LayerNorm");
     cudaStream_t st = as_stream(stream);
     if (dtype == SF_F16) return launch_any<__half>(M, N, x, ldx, e, out, ldout, st);
     if (dtype == SF_BF16) return launch_any<__nv_bfloat16>(M, N, x, ldx, e, out, ldout, st);

@@ -20,12 +20,13 @@ def _ptr(t: Optional[torch.Tensor]) -> Optional[int]:
     return None if t is None else t.data_ptr()
 
 
-def epilogue(bias=None, act: str = "none", aux=None, ln_gamma=None, ln_beta=None, out_pre_ln=None) -> GemmEpilogue:
+def epilogue(bias=None, act: str = "none", aux=None, ln_gamma=None, ln_beta=None, out_pre_ln=None,
+             softmax: bool = False) -> GemmEpilogue:
     for t in (bias, ln_gamma, ln_beta):
         if t is not None and t.dtype != torch.float32:
             raise _lib.InvalidParameter("bias / LayerNorm parameters must be float32")
     return GemmEpilogue(_ptr(bias), SF_ACT[act], _ptr(aux), aux.stride(0) if aux is not None else 0,
-                        _ptr(ln_gamma), _ptr(ln_beta), _ptr(out_pre_ln))
+                        _ptr(ln_gamma), _ptr(ln_beta), _ptr(out_pre_ln), 1 if softmax else 0)
 
 
 TILE_AUTO, TILE_PAIR = 0, 1  # sf_gemm_args.tile_n: SF_TILE_AUTO / SF_TILE_PAIR (or 128 / 256)
@@ -33,7 +34,7 @@ TILE_AUTO, TILE_PAIR = 0, 1  # sf_gemm_args.tile_n: SF_TILE_AUTO / SF_TILE_PAIR 
 
 def gemm_fused(x: torch.Tensor, w_nk: torch.Tensor, out: Optional[torch.Tensor] = None, *, bias=None,
                act: str = "none", aux=None, ln_gamma=None, ln_beta=None, out_pre_ln=None, tile_n: int = 0,
-               stream=None) -> torch.Tensor:
+               softmax: bool = False, stream=None) -> torch.Tensor:
     """out = LN(act(x @ w_nk.T + bias) + aux) — the CiMi template: one tcgen05 kernel (LayerNorm in
     the cluster epilogue), or with tile_n auto on small grids / unclusterable rows, the GEMM followed
     by a MiChain LayerNorm pass."""
@@ -47,18 +48,19 @@ def gemm_fused(x: torch.Tensor, w_nk: torch.Tensor, out: Optional[torch.Tensor] 
         if t.stride(1) != 1:
             raise _lib.ShapeError("GEMM operands must be row-major")
     a = GemmArgs(M, N, K, _dtype_code(x), x.data_ptr(), x.stride(0), w_nk.data_ptr(), w_nk.stride(0),
-                 out.data_ptr(), out.stride(0), epilogue(bias, act, aux, ln_gamma, ln_beta, out_pre_ln), tile_n)
+                 out.data_ptr(), out.stride(0), epilogue(bias, act, aux, ln_gamma, ln_beta, out_pre_ln, softmax), tile_n)
     check(lib().sf_gemm_fused(C.byref(a), _stream(stream)))
     return out
 
 
 def mi_chain(x: torch.Tensor, out: Optional[torch.Tensor] = None, *, bias=None, act: str = "none", aux=None,
-             ln_gamma=None, ln_beta=None, out_pre_ln=None, stream=None) -> torch.Tensor:
-    """The MiChain template: bias -> act -> +aux -> LayerNorm in one pass."""
+             ln_gamma=None, ln_beta=None, out_pre_ln=None, softmax: bool = False, stream=None) -> torch.Tensor:
+    """The MiChain template: bias -> act -> +aux -> LayerNorm or Softmax (row ops, backend.hpp:140-167)
+    in one pass."""
     M, N = x.shape
     if out is None:
         out = torch.empty_like(x)
-    e = epilogue(bias, act, aux, ln_gamma, ln_beta, out_pre_ln)
+    e = epilogue(bias, act, aux, ln_gamma, ln_beta, out_pre_ln, softmax)
     check(lib().sf_mi_chain(M, N, _dtype_code(x), x.data_ptr(), x.stride(0), C.byref(e), out.data_ptr(),
                             out.stride(0), _stream(stream)))
     return out

@@ -226,6 +226,41 @@ class BsrMask:
         return bytes(buf)
 
 
+def bsr_from_host(arrays: dict, seq_len: int, block_m: int, block_n: int, stream=None) -> BsrMask:
+    """Device copy of host BSR arrays (the reference's BsrMask fields; `part_mask_pool` as unpacked
+    0/1 tiles of block_m*block_n, or `pool_packed` as pack_bits bytes)."""
+    a = {k: np.ascontiguousarray(v, np.int32) for k, v in arrays.items()
+         if k not in ("part_mask_pool", "pool_packed")}
+    if "pool_packed" in arrays:
+        pool = np.ascontiguousarray(arrays["pool_packed"], np.uint8)
+    else:
+        tiles = np.asarray(arrays.get("part_mask_pool", np.zeros((0, block_m * block_n))), np.uint8)
+        pool = (np.packbits(tiles.reshape(len(tiles), -1), axis=1, bitorder="little")
+                if len(tiles) else np.zeros((0, (block_m * block_n + 7) // 8), np.uint8))
+    n_pool = pool.shape[0] if pool.ndim == 2 else 0
+    ptr = lambda x: x.ctypes.data if x.size else None
+    dev = BsrDev()
+    check(lib().sf_bsr_from_host(seq_len, block_m, block_n, a["full_col_idx"].size, a["part_col_idx"].size,
+                                 a["load_col_idx"].size, n_pool, ptr(a["full_row_ptr"]), ptr(a["full_col_idx"]),
+                                 ptr(a["part_row_ptr"]), ptr(a["part_col_idx"]), ptr(a["part_tile_ids"]),
+                                 ptr(a["load_row_ptr"]), ptr(a["load_col_idx"]), ptr(pool), C.byref(dev),
+                                 _stream(stream)))
+    return BsrMask(dev)
+
+
+def validate_bsr(b: BsrMask, stream=None) -> None:
+    """validate_bsr (bsr.hpp:104-153) on the device; raises InternalInconsistency with the
+    reference's message."""
+    check(lib().sf_bsr_validate(C.byref(b.dev), _stream(stream)))
+
+
+def to_dense(b: BsrMask, stream=None) -> DenseMask:
+    """to_dense (bsr.hpp:155-177): the exact inverse of build_bsr, on the device."""
+    m = DenseMask.empty(b.seq_len)
+    check(lib().sf_bsr_to_dense(C.byref(b.dev), m.bits.data_ptr(), _stream(stream)))
+    return m
+
+
 def build_bsr(mask: DenseMask, block_m: int, block_n: int, stream=None) -> BsrMask:
     dev = BsrDev()
     check(lib().sf_bsr_build(mask.bits.data_ptr(), mask.seq_len, block_m, block_n, C.byref(dev), _stream(stream)))

@@ -6,8 +6,10 @@
 //       Python test compares with the reference's run_pipeline (oracle/_ref).
 //   host_api_test gpu-basics       masks / formats / selector / attention through the C++ API
 //   host_api_test gpu-backend      GpuBackend: chain on the device + a device-timed search
+//   host_api_test exec-segment ... exec_segment / exec_mha (host Matrix API) on one segment
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <iostream>
 #include <sstream>
 
@@ -230,6 +232,86 @@ static int cmd_gpu_backend() {
     return 0;
 }
 
+// Same grammar as oracle/ref_shim.cpp graph_of: a preset, or "spec:<nodes>".
+static OpGraph graph_of(const std::string& model, const GraphHyper& hy) {
+    if (model.rfind("spec:", 0) != 0) return build_preset_graph(model, hy);
+    OpGraph g;
+    g.name = model;
+    g.hyper = hy;
+    const std::int64_t rows = hy.bs * hy.seq_len;
+    std::int64_t w = hy.hidden_dim;
+    std::stringstream ss(model.substr(5));
+    std::string tok;
+    while (std::getline(ss, tok, ',')) {
+        const int id = static_cast<int>(g.nodes.size());
+        OpNode n{id, OpKind::Bias, rows, w, 0};
+        switch (tok.at(0)) {
+            case 'g': n.kind = OpKind::Gemm; n.inner = w; n.cols = w = std::stoll(tok.substr(1)); break;
+            case 'b': n.kind = OpKind::Bias; break;
+            case 'a': n.kind = OpKind::Add; break;
+            case 'l': n.kind = OpKind::LayerNorm; break;
+            case 'e': n.kind = OpKind::Gelu; break;
+            case 'r': n.kind = OpKind::Relu; break;
+            case 's': n.kind = OpKind::Softmax; break;
+            case 'm': n.kind = OpKind::MhaFused; break;
+            default: throw invalid_parameter("bad graph spec token " + tok);
+        }
+        g.nodes.push_back(n);
+    }
+    return g;
+}
+
+static std::vector<char> read_file(const std::string& path) {
+    std::FILE* f = std::fopen(path.c_str(), "rb");
+    REQUIRE(f);
+    std::vector<char> b;
+    char buf[1 << 16];
+    std::size_t k;
+    while ((k = std::fread(buf, 1, sizeof buf, f)) > 0) b.insert(b.end(), buf, buf + k);
+    std::fclose(f);
+    return b;
+}
+
+// exec-segment <model> <bs> <seq> <hidden> <heads> <head_size> <seed> <seg_begin> <seg_end> <in.f32>
+//              <out.f32> [<mask.u8> <bm> <bn>]
+// The reference-signature free functions (exec_segment / exec_mha with host Matrix in / out and an
+// MhaContext) on GraphData(seed); the Python test compares the output with the reference's own
+// exec_segment (oracle/_ref).
+static int cmd_exec_segment(int argc, char** argv) {
+    if (argc < 12) return 2;
+    GraphHyper hy{std::atoll(argv[3]), std::atoll(argv[4]), std::atoll(argv[5]), std::atoi(argv[6]), std::atoi(argv[7]), 0};
+    const OpGraph g = graph_of(argv[2], hy);
+    const GraphData gd = GraphData::make(g, std::strtoull(argv[8], nullptr, 10));
+    const Segment seg{std::atoi(argv[9]), std::atoi(argv[10])};
+    const OpNode& first = g.nodes.at(static_cast<std::size_t>(seg.begin));
+    Matrix x(first.rows, first.kind == OpKind::Gemm ? first.inner : first.cols);
+    const auto raw = read_file(argv[11]);
+    REQUIRE(raw.size() == x.a.size() * 4);
+    std::memcpy(x.a.data(), raw.data(), raw.size());
+    std::optional<MhaContext> ctx;
+    if (argc >= 16) {
+        const auto mb = read_file(argv[13]);
+        const int n = static_cast<int>(hy.seq_len);
+        REQUIRE(mb.size() == static_cast<std::size_t>(n) * n);
+        DenseMask m(n);
+        for (int i = 0; i < n; ++i)
+            for (int j = 0; j < n; ++j)
+                if (mb[static_cast<std::size_t>(i) * n + j]) m.set(i, j, true);
+        KernelPlan plan;
+        plan.kind = KernelKind::BlockWise;
+        plan.block_m = std::atoi(argv[14]);
+        plan.block_n = std::atoi(argv[15]);
+        ctx = MhaContext::make(m, plan);
+    }
+    const Matrix y = exec_segment(g, gd, ctx ? &*ctx : nullptr, seg, default_setting(classify_segment(seg, g)), x);
+    std::FILE* f = std::fopen(argv[12], "wb");
+    REQUIRE(f);
+    std::fwrite(y.a.data(), 4, y.a.size(), f);
+    std::fclose(f);
+    std::cout << "exec-segment ok " << y.rows << "x" << y.cols << "\n";
+    return 0;
+}
+
 int main(int argc, char** argv) {
     if (argc < 2) return 2;
     const std::string cmd = argv[1];
@@ -238,6 +320,7 @@ int main(int argc, char** argv) {
         if (cmd == "cache") return cmd_cache(argc, argv);
         if (cmd == "gpu-basics") return cmd_gpu_basics();
         if (cmd == "gpu-backend") return cmd_gpu_backend();
+        if (cmd == "exec-segment") return cmd_exec_segment(argc, argv);
     } catch (const std::exception& e) {
         std::fprintf(stderr, "exception: %s\n", e.what());
         return 1;

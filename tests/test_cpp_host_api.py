@@ -67,3 +67,74 @@ def test_gpu_measurement_backend_drives_the_search():
     r = subprocess.run([_bin(), "gpu-backend"], capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stderr + r.stdout
     assert "gpu-backend ok" in r.stdout
+
+
+SEGMENT_CASES = [  # (graph, segment, template) at bs 2, seq 256, hidden 256, 4 heads x 64
+    ("bert-layer", (1, 2), "CiMi: out-projection GEMM"),
+    ("bert-layer", (1, 5), "CiMi: GEMM + bias + residual + LayerNorm"),
+    ("bert-layer", (5, 12), "CiCi: FFN1 + GELU -> FFN2 + bias + residual + LayerNorm"),
+    ("gpt-layer", (0, 1), "MiChain: LayerNorm"),
+    ("t5-layer", (6, 12), "CiCi: FFN with ReLU"),
+    ("spec:g512,b,s", (0, 3), "CiMi + Softmax row op"),
+    ("spec:b,e,a,s", (0, 4), "MiChain ending in Softmax"),
+    ("spec:l,g256,b,r", (0, 4), "CiMi with a LayerNorm prologue"),
+    ("bert-layer", (0, 1), "MhaFused unit (exec_mha), BigBird mask, BSR 128x16"),
+]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("model,seg,what", SEGMENT_CASES)
+def test_exec_segment_matches_reference(reference, tmp_path, model, seg, what):
+    """exec_segment / exec_mha through the C++ host API (include/sparsefuse_b200/gpu_backend.hpp,
+    reference signatures, host Matrix in / out, executed by the sm_100a templates) against the
+    reference's own exec_segment (backend.hpp:360-385) on the same GraphData seeds and input.
+    Bar: the north-star fp16 tolerance (max-abs 2e-2, mean-rel 1e-3) vs the fp32 reference."""
+    import numpy as np
+    bs, seq, hid, heads, hs, seed = 2, 256, 256, 4, 64, 5
+    rng = np.random.default_rng(11)
+    in_cols, out_cols = _seg_widths(model, seg, hid)
+    x = (rng.random((bs * seq, in_cols), np.float32) * 2 - 1).astype(np.float16).astype(np.float32)
+    mask = None
+    extra = []
+    if "Mha" in what:
+        from oracle.oracle import Oracle
+        mask = Oracle().mask([dict(pattern="bigbird", seq_len=seq, global_width=16, band_width=16,
+                                   filling_rate=0.1, seed=2)])
+        (tmp_path / "m.u8").write_bytes(mask.astype(np.uint8).tobytes())
+        extra = [str(tmp_path / "m.u8"), "128", "16"]
+    (tmp_path / "x.f32").write_bytes(x.tobytes())
+    r = subprocess.run([_bin(), "exec-segment", model, str(bs), str(seq), str(hid), str(heads), str(hs), str(seed),
+                        str(seg[0]), str(seg[1]), str(tmp_path / "x.f32"), str(tmp_path / "y.f32")] + extra,
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr + r.stdout
+    ours = np.frombuffer((tmp_path / "y.f32").read_bytes(), np.float32).reshape(bs * seq, out_cols)
+    ref = reference.exec_segment(model, bs, seq, hid, heads, hs, seed, seg, x, out_cols, mask=mask, tile=(128, 16))
+    d = np.abs(ours.astype(np.float64) - ref)
+    ma, mr = float(d.max()), float(d.sum() / np.abs(ref).sum())
+    assert ma <= 2e-2 and mr <= 1e-3, (what, ma, mr)
+
+
+def _seg_widths(model, seg, hid):
+    """(input width of node seg[0], output width of node seg[1]-1) for presets / spec graphs."""
+    if model.startswith("spec:"):
+        w, ws = hid, []
+        for tok in model[5:].split(","):
+            wi = w
+            if tok[0] == "g":
+                w = int(tok[1:])
+            ws.append((wi, w))
+    else:
+        ff = 4 * hid
+        kinds = {"bert-layer": ["m", "g", "b", "a", "l", "g4", "b4", "e4", "g", "b", "a", "l"],
+                 "gpt-layer": ["l", "m", "g", "b", "a", "l", "g4", "b4", "e4", "g", "b", "a"]}
+        kinds["t5-layer"] = kinds["gpt-layer"]
+        ws = []
+        w = hid
+        for k in kinds[model]:
+            wi = w
+            if k == "g4":
+                w = ff
+            elif k == "g":
+                w = hid
+            ws.append((wi, w))
+    return ws[seg[0]][0], ws[seg[1] - 1][1]

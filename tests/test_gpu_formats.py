@@ -67,13 +67,73 @@ def test_small_bsr_dumps_match_golden(sf):
 
 
 def test_randomized_round_trip_1000(sf, oracle):
-    # test_bsr.cpp:65-84: 1000 random masks, n <= 96, bm, bn <= 24 — device bytes == oracle bytes
+    # test_bsr.cpp:65-84: 1000 random masks, n <= 96, bm, bn <= 24 — device bytes == oracle bytes,
+    # validate_bsr passes and to_dense(build_bsr(m)) == m, all on the device
     rng = np.random.default_rng(2024)
     for it in range(1000):
         n = int(rng.integers(1, 97)); bm = int(rng.integers(1, 25)); bn = int(rng.integers(1, 25))
         m = (rng.random((n, n)) < rng.random()).astype(np.uint8)
         b = sf.build_bsr(sf.DenseMask.from_numpy(m), bm, bn)
         assert b.sfbr() == oracle.bsr(m, bm, bn)["sfbr"], (it, n, bm, bn)
+        sf.validate_bsr(b)
+        assert np.array_equal(sf.to_dense(b).to_numpy(), m), (it, n, bm, bn)
+        if it % 50 == 0:  # host arrays -> device copy -> to_dense (read_bsr-style masks)
+            h = sf.bsr_from_host(b.to_host(), n, bm, bn)
+            assert h.sfbr() == b.sfbr()
+            assert np.array_equal(sf.to_dense(h).to_numpy(), m)
+
+
+def _corruptions(a, n_cols, n_pool):
+    """(name, corrupted copy) pairs over a built BSR's host arrays; each breaks one invariant."""
+    def cp():
+        return {k: np.array(v, copy=True) for k, v in a.items()}
+    out = []
+    if len(a["full_col_idx"]):
+        c = cp(); c["full_col_idx"][0] = n_cols; out.append(("full col out of range", c))
+        c = cp(); fr = c["full_row_ptr"]; r = int(np.argmax(np.diff(fr) >= 1)); fr[r + 1] = fr[r] - 1
+        out.append(("full row_ptr decreasing", c))
+    if (np.diff(a["part_row_ptr"]) >= 2).any():
+        c = cp(); r = int(np.argmax(np.diff(c["part_row_ptr"]) >= 2)); k = int(c["part_row_ptr"][r])
+        c["part_col_idx"][[k, k + 1]] = c["part_col_idx"][[k + 1, k]]; out.append(("part cols unordered", c))
+    if len(a["part_tile_ids"]):
+        c = cp(); c["part_tile_ids"][0] = n_pool; out.append(("tile id past pool", c))
+        c = cp(); c["part_mask_pool"] = c["part_mask_pool"].copy(); c["part_mask_pool"][0][:] = 1
+        out.append(("pool tile all ones", c))
+    c = cp(); lc = c["load_col_idx"]; lr = c["load_row_ptr"]
+    for r in range(len(lr) - 1):  # shift one load column to a free neighbour, keeping order
+        row = lc[lr[r]:lr[r + 1]]
+        if len(row) and row[-1] + 1 < n_cols:
+            row[-1] += 1
+            break
+    out.append(("load not the union", c))
+    c = cp(); c["load_row_ptr"][-1] += 1; out.append(("load_row_ptr.back() + 1 (test_bsr.cpp:94-98)", c))
+    return out
+
+
+@pytest.mark.parametrize("terms,tile", [([dict(pattern="bigbird", seq_len=256, global_width=16, band_width=16,
+                                               filling_rate=0.2, seed=3)], (16, 16)),
+                                        ([dict(pattern="sliding", seq_len=64, band_width=8)], (16, 16)),
+                                        ([dict(pattern="dilated", seq_len=200, band_width=24, dilation_rate=2)], (32, 8))])
+def test_validate_bsr_rejects_corruptions_like_the_reference(sf, oracle, reference, terms, tile):
+    """validate_bsr / to_dense on corrupted structures (test_bsr.cpp:94-98): the device check raises
+    InternalInconsistency with the same message the reference's validate_bsr throws."""
+    from paper_2506_06095_b200 import _lib
+    dm = sf.generate_mask(terms)
+    n = dm.seq_len
+    b = sf.build_bsr(dm, *tile)
+    a = b.to_host()
+    a.pop("pool_packed")
+    assert reference.validate_bsr(n, *tile, a) == (0, "")
+    for name, c in _corruptions(a, b.n_cols, b.n_pool):
+        st, msg = reference.validate_bsr(n, *tile, c)
+        assert st == 6, name  # SF_INTERNAL_INCONSISTENCY
+        h = sf.bsr_from_host(c, n, *tile)
+        with pytest.raises(_lib.InternalInconsistency) as e:
+            sf.validate_bsr(h)
+        with pytest.raises(_lib.InternalInconsistency):
+            sf.to_dense(h)
+        if "back() + 1" not in name:  # that one reads past the column array in the reference (UB)
+            assert str(e.value) == msg, (name, str(e.value), msg)
 
 
 def test_extremes_and_dedup(sf, oracle):

@@ -122,6 +122,33 @@ def test_mi_chain(fz, oracle, M, N, ln):
     parity(fz.mi_chain(dev(x), **kw), ref)
 
 
+@pytest.mark.parametrize("M,N", [(1000, 768), (37, 100), (9, 4096), (300, 1024), (50, 3072)])
+def test_mi_chain_softmax(fz, oracle, M, N):
+    """Softmax MI op (backend.hpp:113,155-167) after bias -> GELU -> residual, one MiChain pass."""
+    import torch
+    x = r16(oracle.random_matrix(M, N, 22))
+    b = oracle.random_matrix(1, N, 23, -0.5, 0.5)[0]
+    aux = r16(oracle.random_matrix(M, N, 24))
+    ref = oracle.softmax(oracle.add(oracle.gelu(oracle.bias(x, b)), aux))
+    out = fz.mi_chain(dev(x), bias=dev(b, torch.float32), act="gelu", aux=dev(aux), softmax=True)
+    # probabilities ~1/N: the north-star max-abs bar holds trivially, mean-rel carries the check
+    parity(out, ref)
+    assert abs(out.float().sum(1).mean().item() - 1.0) < 1e-2
+
+
+@pytest.mark.parametrize("tile", [0, PAIR])
+def test_gemm_softmax(fz, oracle, tile):
+    """CiMi with a trailing Softmax: GEMM + bias, then the row softmax pass."""
+    import torch
+    M, N, K = 512, 768, 256
+    x = r16(oracle.random_matrix(M, K, 31))
+    w = r16(oracle.random_matrix(K, N, 32, -0.1, 0.1))
+    b = oracle.random_matrix(1, N, 33, -0.5, 0.5)[0]
+    ref = oracle.softmax(oracle.bias(x.astype(np.float64) @ w.astype(np.float64), b))
+    out = fz.gemm_fused(dev(x), dev(np.ascontiguousarray(w.T)), bias=dev(b, torch.float32), softmax=True, tile_n=tile)
+    parity(out, ref)
+
+
 def test_gemm_shape_errors(fz):
     import torch
     from paper_2506_06095_b200 import _lib
