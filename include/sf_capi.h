@@ -137,6 +137,15 @@ sf_status sf_bsr_build(const uint32_t* d_bits, int32_t seq_len, int32_t block_m,
                        sf_bsr_dev* out, void* stream);
 sf_status sf_bsr_free(sf_bsr_dev* bsr, void* stream);
 
+/* Graph-capturable rebuilds (masks that change per request): sf_bsr_workspace allocates a BSR
+ * sized for the whole tile grid (n_full / n_part / n_load / n_pool then hold capacities);
+ * sf_bsr_build_async rebuilds it from a device mask with no host synchronisation, so the call can
+ * sit inside a CUDA graph; the arrays equal sf_bsr_build's and d_counts[4] (device, optional)
+ * receives n_full, n_part, n_load, n_pool. The attention executors walk the row pointers, so a
+ * workspace BSR can be passed to sf_mha_blockwise directly (its stats report capacities). */
+sf_status sf_bsr_workspace(int32_t seq_len, int32_t block_m, int32_t block_n, sf_bsr_dev* ws, void* stream);
+sf_status sf_bsr_build_async(const uint32_t* d_bits, sf_bsr_dev* ws, int32_t* d_counts, void* stream);
+
 /* Copy a device BSR into host arrays sized from the counts in `bsr` (any pointer may be NULL
  * to skip). `pool` receives n_pool*tile_bytes packed bytes. Synchronizes. */
 sf_status sf_bsr_to_host(const sf_bsr_dev* bsr, int32_t* full_row_ptr, int32_t* full_col_idx,

@@ -288,7 +288,8 @@ class Reference:
         L.ref_graph_param.argtypes = [C.c_char_p, C.c_int64, C.c_int64, C.c_int64, C.c_int, C.c_int, C.c_uint64,
                                       C.c_int, C.c_int, C.POINTER(C.c_float), C.c_int64, C.POINTER(C.c_int64)]
         L.ref_run_chain.argtypes = [C.c_char_p, C.c_int64, C.c_int64, C.c_int64, C.c_int, C.c_int, C.c_uint64,
-                                    C.POINTER(C.c_uint8), C.c_int, C.c_int, C.c_char_p, C.POINTER(C.c_float), C.c_int]
+                                    C.POINTER(C.c_uint8), C.c_int, C.c_int, C.c_char_p, C.POINTER(C.c_float), C.c_int,
+                                    C.POINTER(C.c_double)]
         L.ref_exec_segment.argtypes = [C.c_char_p, C.c_int64, C.c_int64, C.c_int64, C.c_int, C.c_int, C.c_uint64,
                                        C.c_int, C.c_int, C.POINTER(C.c_float), C.POINTER(C.c_float),
                                        C.POINTER(C.c_uint8), C.c_int, C.c_int]
@@ -418,14 +419,18 @@ class Reference:
             raise ValueError(f"ref_cache_session status {st}")
         return buf.value.decode()
 
-    def run_chain(self, model, bs, seq, hidden, heads, head_size, seed, mask, bm, bn, code="", threads=1):
+    def run_chain(self, model, bs, seq, hidden, heads, head_size, seed, mask, bm, bn, code="", threads=1,
+                  timing=False):
+        """CpuBackend::run_chain output of copy 0; with timing=True also the wall seconds of the
+        concurrent run_chain calls alone (backend construction excluded)."""
         mask = np.ascontiguousarray(mask, np.uint8)
         out = np.zeros((bs * seq, hidden), np.float32)
+        sec = C.c_double(0.0)
         st = self.lib.ref_run_chain(model.encode(), bs, seq, hidden, heads, head_size, seed, _ptr(mask, C.c_uint8),
-                                    bm, bn, code.encode(), _ptr(out, C.c_float), threads)
+                                    bm, bn, code.encode(), _ptr(out, C.c_float), threads, C.byref(sec))
         if st:
             raise ValueError(f"ref_run_chain status {st}")
-        return out
+        return (out, sec.value) if timing else out
 
 
 CONFIG_MASKS = {

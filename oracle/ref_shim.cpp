@@ -12,6 +12,8 @@
 #include <sparsefuse/planner.hpp>
 #include <sparsefuse/search.hpp>
 
+#include <barrier>
+#include <chrono>
 #include <cstring>
 #include <sstream>
 #include <thread>
@@ -268,10 +270,12 @@ int ref_graph_param(const char* model, int64_t bs, int64_t seq, int64_t hidden, 
 // code (empty = unfused) with default settings, the MHA context built from `mask` at the
 // given plan tile. Output rows*hidden floats. n_threads > 1 runs `n_threads` independent
 // copies of the chain (one sequence each when bs == 1) for throughput timing; out receives
-// copy 0.
+// copy 0. `seconds` (optional) receives the wall time of the run_chain calls alone: every thread
+// first builds its CpuBackend (GraphData::make regenerates all weights, backend.hpp:408-410,456),
+// then all start together at a barrier; the clock runs from the barrier to the last join.
 int ref_run_chain(const char* model, int64_t bs, int64_t seq, int64_t hidden, int heads,
                   int head_size, uint64_t seed, const uint8_t* mask, int bm, int bn,
-                  const char* code, float* out, int n_threads) {
+                  const char* code, float* out, int n_threads, double* seconds) {
     return guard([&] {
         GraphHyper hy{bs, seq, hidden, heads, head_size, 0};
         const OpGraph g = build_preset_graph(model, hy);
@@ -283,18 +287,21 @@ int ref_run_chain(const char* model, int64_t bs, int64_t seq, int64_t hidden, in
         const MhaContext ctx = MhaContext::make(dm, plan);
         const FusionScheme scheme = (code && *code) ? make_scheme(decode(code)) : unfused_scheme(g.size());
         validate_scheme(scheme, g);
+        const int nt = std::max(1, n_threads);
+        std::barrier start(nt + 1);
+        std::chrono::steady_clock::time_point t0;
         auto one = [&](float* dst) {
             CpuBackend be(g, seed, ctx);
+            start.arrive_and_wait();
             const Matrix r = be.run_chain(g, scheme, {});
             if (dst) std::memcpy(dst, r.a.data(), r.a.size() * 4);
         };
-        if (n_threads <= 1) {
-            one(out);
-        } else {
-            std::vector<std::thread> th;
-            for (int t = 0; t < n_threads; ++t) th.emplace_back(one, t == 0 ? out : nullptr);
-            for (auto& x : th) x.join();
-        }
+        std::vector<std::thread> th;
+        for (int t = 0; t < nt; ++t) th.emplace_back(one, t == 0 ? out : nullptr);
+        start.arrive_and_wait();
+        t0 = std::chrono::steady_clock::now();
+        for (auto& x : th) x.join();
+        if (seconds) *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     });
 }
 

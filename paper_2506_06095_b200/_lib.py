@@ -110,6 +110,8 @@ SIGNATURES = {
     "sf_bsr_to_host": (C.c_int, [C.POINTER(BsrDev)] + [_P] * 8 + [_P]),
     "sf_bsr_serialize": (C.c_int, [C.POINTER(BsrDev), _P, _I64, C.POINTER(_I64), _P]),
     "sf_bsr_validate": (C.c_int, [C.POINTER(BsrDev), _P]),
+    "sf_bsr_workspace": (C.c_int, [_I32, _I32, _I32, C.POINTER(BsrDev), _P]),
+    "sf_bsr_build_async": (C.c_int, [_P, C.POINTER(BsrDev), _P, _P]),
     "sf_bsr_to_dense": (C.c_int, [C.POINTER(BsrDev), _P, _P]),
     "sf_bsr_from_host": (C.c_int, [_I32] * 7 + [_P] * 8 + [C.POINTER(BsrDev), _P]),
     "sf_mask_serialize": (C.c_int, [_P, _I32, _P, _I64, C.POINTER(_I64), _P]),

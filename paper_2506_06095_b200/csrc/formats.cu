@@ -181,11 +181,11 @@ __device__ __forceinline__ bool tiles_equal_warp(const uint32_t* __restrict__ bi
 // the warp compares contents on a hash match. Each slot ends holding the smallest row-major tile
 // id of its content class (atomicMin), which fixes the pool order to first occurrence
 // (bsr.hpp:83-91).
-__global__ void dedup_insert_kernel(const uint32_t* __restrict__ bits, Geo g, int32_t n_part,
+__global__ void dedup_insert_kernel(const uint32_t* __restrict__ bits, Geo g, const int32_t* __restrict__ n_part_dev,
                                     const int32_t* __restrict__ part_lin, const uint64_t* __restrict__ hash,
                                     int32_t* table, uint32_t cap_mask, int32_t* part_slot) {
     const int64_t k = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    if (k >= n_part) return;
+    if (k >= *n_part_dev) return;
     const int lane = threadIdx.x & 31;
     const int32_t lin = part_lin[k];
     const uint64_t h = hash[lin];
@@ -204,43 +204,46 @@ __global__ void dedup_insert_kernel(const uint32_t* __restrict__ bits, Geo g, in
     if (lane == 0) part_slot[k] = static_cast<int32_t>(s);
 }
 
-__global__ void first_flag_kernel(int32_t n_part, const int32_t* __restrict__ part_lin,
+// first-occurrence flags over the part list, 0 past the device count (so a scan over the
+// capacity equals a scan over the list)
+__global__ void first_flag_kernel(int64_t cap, const int32_t* __restrict__ n_part_dev, const int32_t* __restrict__ part_lin,
                                   const int32_t* __restrict__ table, const int32_t* __restrict__ part_slot,
                                   int32_t* first) {
     const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (k >= n_part) return;
-    first[k] = table[part_slot[k]] == part_lin[k] ? 1 : 0;
+    if (k >= cap) return;
+    first[k] = k < *n_part_dev && table[part_slot[k]] == part_lin[k] ? 1 : 0;
 }
 
-__global__ void slot_id_kernel(int32_t n_part, const int32_t* __restrict__ first,
+__global__ void slot_id_kernel(const int32_t* __restrict__ n_part_dev, const int32_t* __restrict__ first,
                                const int32_t* __restrict__ first_scan, const int32_t* __restrict__ part_slot,
                                int32_t* slot_id, int32_t* pool_src) {
     const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (k >= n_part) return;
+    if (k >= *n_part_dev) return;
     if (first[k]) {
         slot_id[part_slot[k]] = first_scan[k];
         pool_src[first_scan[k]] = static_cast<int32_t>(k);
     }
 }
 
-__global__ void tile_ids_kernel(int32_t n_part, const int32_t* __restrict__ part_slot,
+__global__ void tile_ids_kernel(const int32_t* __restrict__ n_part_dev, const int32_t* __restrict__ part_slot,
                                 const int32_t* __restrict__ slot_id, int32_t* tile_ids) {
     const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (k >= n_part) return;
+    if (k >= *n_part_dev) return;
     tile_ids[k] = slot_id[part_slot[k]];
 }
 
-__global__ void load_tile_kernel(int32_t n_load, const int32_t* __restrict__ load_part,
+__global__ void load_tile_kernel(const int32_t* __restrict__ n_load_dev, const int32_t* __restrict__ load_part,
                                  const int32_t* __restrict__ tile_ids, int32_t* load_tile) {
     const int64_t l = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (l >= n_load) return;
+    if (l >= *n_load_dev) return;
     const int32_t k = load_part[l];
     load_tile[l] = k < 0 ? -1 : tile_ids[k];
 }
 
-// One warp per pool tile; lanes produce bytes of pack_bits(tile).
-// Launched for every part tile (an upper bound of the pool); the pool size is read on device, so
-// the build needs no host round trip between the dedup and the pool write.
+// One warp per pool tile; each lane assembles whole 32-bit words of pack_bits(tile) (cells 32w ..
+// 32w + 31, LSB first) from the tile's row segments with 64-bit row extracts, then stores the
+// word's bytes. Launched for every part tile (an upper bound of the pool); the pool size is read
+// on device, so the build needs no host round trip between the dedup and the pool write.
 __global__ void pool_write_kernel(const uint32_t* __restrict__ bits, Geo g, const int32_t* __restrict__ n_pool_dev,
                                   const int32_t* __restrict__ pool_src,
                                   const int32_t* __restrict__ part_lin, int32_t tile_bytes,
@@ -251,16 +254,26 @@ __global__ void pool_write_kernel(const uint32_t* __restrict__ bits, Geo g, cons
     const int64_t lin = part_lin[pool_src[w]];
     const int64_t br = lin / g.n_cols, bc = lin - br * g.n_cols;
     const int64_t nbits = static_cast<int64_t>(g.bm) * g.bn;
-    for (int64_t byte = lane; byte < tile_bytes; byte += 32) {
+    const int64_t jlim = imin64(g.n, bc * g.bn + g.bn);
+    uint8_t* dst = pool + w * tile_bytes;
+    for (int64_t word = lane; word * 4 < tile_bytes; word += 32) {
         uint32_t v = 0;
-        for (int b = 0; b < 8; ++b) {
-            const int64_t t = byte * 8 + b;
-            if (t >= nbits) break;
+        int64_t t = word * 32;
+        const int64_t tend = imin64(nbits, t + 32);
+        while (t < tend) {
             const int64_t di = t / g.bn, dj = t - di * g.bn;
-            const int64_t i = br * g.bm + di, j = bc * g.bn + dj;
-            if (i < g.n && j < g.n && ((bits[i * g.words + (j >> 5)] >> (j & 31)) & 1u)) v |= 1u << b;
+            const int len = static_cast<int>(imin64(g.bn - dj, tend - t));  // <= 32
+            const int64_t i = br * g.bm + di;
+            if (i < g.n) {
+                const uint64_t seg = row_bits64(bits + i * g.words, bc * g.bn + dj, jlim);
+                const uint32_t m = len == 32 ? ~0u : ((1u << len) - 1u);
+                v |= (static_cast<uint32_t>(seg) & m) << (t - word * 32);
+            }
+            t += len;
         }
-        pool[w * tile_bytes + byte] = static_cast<uint8_t>(v);
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+            if (word * 4 + b < tile_bytes) dst[word * 4 + b] = static_cast<uint8_t>(v >> (8 * b));
     }
 }
 
@@ -476,123 +489,212 @@ namespace sf {
 void attn_reserve_counters(cudaStream_t st);  // attn_tc.cu: the attention work-counter pool of this device
 }
 
+namespace {
+// Phase-1 scratch: per-tile class + hash, per-row counts and row pointers, device totals
+// (n_full, n_part, n_load, n_pool).
+struct Scratch1 {
+    uint8_t* cls;
+    uint64_t* hash;
+    int32_t *fcnt, *pcnt, *lcnt, *fptr, *pptr, *lptr, *totals;
+};
+int64_t scratch1_bytes(int64_t tiles, int64_t n_rows) {
+    return ceil_div(tiles, 256) * 256 + ceil_div(tiles * 8, 256) * 256 + 6 * (ceil_div((n_rows + 1) * 4, 256) * 256) + 256;
+}
+Scratch1 carve_scratch1(char*& p, int64_t tiles, int64_t n_rows) {
+    Scratch1 s;
+    s.cls = carve<uint8_t>(p, tiles);
+    s.hash = carve<uint64_t>(p, tiles);
+    s.fcnt = carve<int32_t>(p, n_rows + 1);
+    s.pcnt = carve<int32_t>(p, n_rows + 1);
+    s.lcnt = carve<int32_t>(p, n_rows + 1);
+    s.fptr = carve<int32_t>(p, n_rows + 1);
+    s.pptr = carve<int32_t>(p, n_rows + 1);
+    s.lptr = carve<int32_t>(p, n_rows + 1);
+    s.totals = carve<int32_t>(p, 4);
+    return s;
+}
+// Phase-2 (dedup) scratch for up to part_cap part tiles and load_cap loads.
+struct Scratch2 {
+    int32_t *part_lin, *part_slot, *first, *first_scan, *pool_src, *table, *slot_id, *load_part;
+    uint32_t cap;
+};
+uint32_t table_cap(int64_t part_cap) {
+    uint32_t cap = 16;
+    while (cap < static_cast<uint32_t>(imax64(1, part_cap)) * 2u) cap <<= 1;
+    return cap;
+}
+int64_t scratch2_bytes(int64_t part_cap, int64_t load_cap) {
+    const int64_t np1 = imax64(1, part_cap);
+    return 5 * ceil_div((np1 + 1) * 4, 256) * 256 + 2 * ceil_div(table_cap(part_cap) * 4ll, 256) * 256 +
+           ceil_div(imax64(1, load_cap) * 4, 256) * 256;
+}
+Scratch2 carve_scratch2(char*& p, int64_t part_cap, int64_t load_cap) {
+    Scratch2 s;
+    const int64_t np1 = imax64(1, part_cap);
+    s.cap = table_cap(part_cap);
+    s.part_lin = carve<int32_t>(p, np1);
+    s.part_slot = carve<int32_t>(p, np1);
+    s.first = carve<int32_t>(p, np1);
+    s.first_scan = carve<int32_t>(p, np1 + 1);
+    s.pool_src = carve<int32_t>(p, np1);
+    s.table = carve<int32_t>(p, s.cap);
+    s.slot_id = carve<int32_t>(p, s.cap);
+    s.load_part = carve<int32_t>(p, imax64(1, load_cap));
+    return s;
+}
+// Output arrays of a BSR with room for the given counts.
+int64_t out_bytes(int64_t n_rows, int64_t n_full, int64_t n_part, int64_t n_load, int64_t pool_bytes) {
+    const int64_t rp = n_rows + 1;
+    return 3 * ceil_div(rp * 4, 256) * 256 + ceil_div(imax64(1, n_full) * 4, 256) * 256 +
+           2 * ceil_div(imax64(1, n_part) * 4, 256) * 256 + 2 * ceil_div(imax64(1, n_load) * 4, 256) * 256 +
+           ceil_div(imax64(1, pool_bytes), 256) * 256;
+}
+void carve_out(char*& p, sf_bsr_dev* out, int64_t n_rows, int64_t n_full, int64_t n_part, int64_t n_load,
+               int64_t pool_bytes) {
+    const int64_t rp = n_rows + 1;
+    out->full_row_ptr = carve<int32_t>(p, rp);
+    out->part_row_ptr = carve<int32_t>(p, rp);
+    out->load_row_ptr = carve<int32_t>(p, rp);
+    out->full_col_idx = carve<int32_t>(p, imax64(1, n_full));
+    out->part_col_idx = carve<int32_t>(p, imax64(1, n_part));
+    out->part_tile_ids = carve<int32_t>(p, imax64(1, n_part));
+    out->load_col_idx = carve<int32_t>(p, imax64(1, n_load));
+    out->load_tile = carve<int32_t>(p, imax64(1, n_load));
+    out->pool = carve<uint8_t>(p, imax64(1, pool_bytes));
+}
+
+// classify -> per-row counts -> the three row-pointer scans (written to fptr/pptr/lptr), device totals
+sf_status bsr_phase1(const uint32_t* d_bits, const Geo& g, const Scratch1& s, int32_t* fptr, int32_t* pptr,
+                     int32_t* lptr, cudaStream_t st) {
+    const int64_t tiles = static_cast<int64_t>(g.n_rows) * g.n_cols;
+    classify_kernel<<<blocks_for(tiles * 32), 256, 0, st>>>(d_bits, g, s.cls, s.hash);
+    SF_LAUNCH_CHECK();
+    row_count_kernel<<<g.n_rows, 256, 0, st>>>(s.cls, g, s.fcnt, s.pcnt, s.lcnt);
+    SF_LAUNCH_CHECK();
+    scan_exclusive3_kernel<<<dim3(1, 3), 1024, 0, st>>>(s.fcnt, s.pcnt, s.lcnt, fptr, pptr, lptr, g.n_rows, s.totals);
+    SF_LAUNCH_CHECK();
+    return SF_OK;
+}
+
+// compaction, content dedup, pool ids, pool bytes, load tile kinds; every count read on device
+// (totals), launches sized by the capacities
+sf_status bsr_phase2(const uint32_t* d_bits, const Geo& g, const sf_bsr_dev* out, const int32_t* fptr,
+                     const int32_t* pptr, const int32_t* lptr, const Scratch1& s1, const Scratch2& s2,
+                     int64_t part_cap, int64_t load_cap, int32_t tile_bytes, cudaStream_t st) {
+    SF_CUDA_TRY(cudaMemsetAsync(s2.table, 0xff, s2.cap * 4ll, st));
+    if (load_cap > 0) {
+        compact_kernel<<<g.n_rows, 256, 0, st>>>(s1.cls, g, fptr, pptr, lptr, out->full_col_idx, out->part_col_idx,
+                                                 out->load_col_idx, s2.part_lin, s2.load_part);
+        SF_LAUNCH_CHECK();
+    }
+    const int32_t* n_part = s1.totals + 1;
+    const int32_t* n_load = s1.totals + 2;
+    int32_t* n_pool = s1.totals + 3;
+    if (part_cap > 0) {
+        dedup_insert_kernel<<<blocks_for(part_cap * 32), 256, 0, st>>>(d_bits, g, n_part, s2.part_lin, s1.hash,
+                                                                       s2.table, s2.cap - 1, s2.part_slot);
+        SF_LAUNCH_CHECK();
+        first_flag_kernel<<<blocks_for(part_cap), 256, 0, st>>>(part_cap, n_part, s2.part_lin, s2.table, s2.part_slot,
+                                                               s2.first);
+        SF_LAUNCH_CHECK();
+        SF_TRY(scan_exclusive(s2.first, s2.first_scan, part_cap, n_pool, st));
+        slot_id_kernel<<<blocks_for(part_cap), 256, 0, st>>>(n_part, s2.first, s2.first_scan, s2.part_slot, s2.slot_id,
+                                                            s2.pool_src);
+        SF_LAUNCH_CHECK();
+        tile_ids_kernel<<<blocks_for(part_cap), 256, 0, st>>>(n_part, s2.part_slot, s2.slot_id, out->part_tile_ids);
+        SF_LAUNCH_CHECK();
+        pool_write_kernel<<<blocks_for(part_cap * 32), 256, 0, st>>>(d_bits, g, n_pool, s2.pool_src, s2.part_lin,
+                                                                     tile_bytes, out->pool);
+        SF_LAUNCH_CHECK();
+    } else {
+        SF_CUDA_TRY(cudaMemsetAsync(n_pool, 0, 4, st));
+    }
+    if (load_cap > 0) {
+        load_tile_kernel<<<blocks_for(load_cap), 256, 0, st>>>(n_load, s2.load_part, out->part_tile_ids, out->load_tile);
+        SF_LAUNCH_CHECK();
+    }
+    return SF_OK;
+}
+
+bool bsr_args_ok(const uint32_t* d_bits, int32_t seq_len, int32_t block_m, int32_t block_n, sf_status* st) {
+    if (block_m < 1 || block_n < 1) { *st = fail(SF_INVALID_PARAMETER, "block sizes must be >= 1"); return false; }
+    if (seq_len < 1) { *st = fail(SF_INVALID_PARAMETER, "seq_len must be positive"); return false; }
+    if (!d_bits) { *st = fail(SF_INVALID_PARAMETER, "null mask"); return false; }
+    const int64_t tiles = ceil_div(seq_len, block_m) * ceil_div(seq_len, block_n);
+    if (tiles > (1ll << 31) - 1) { *st = fail(SF_INVALID_PARAMETER, "tile grid too large"); return false; }
+    return true;
+}
+}  // namespace
+
 extern "C" sf_status sf_bsr_build(const uint32_t* d_bits, int32_t seq_len, int32_t block_m,
                                   int32_t block_n, sf_bsr_dev* out, void* stream) {
     if (!out) return fail(SF_INVALID_PARAMETER, "null output");
     *out = sf_bsr_dev{};
-    if (block_m < 1 || block_n < 1) return fail(SF_INVALID_PARAMETER, "block sizes must be >= 1");
-    if (seq_len < 1) return fail(SF_INVALID_PARAMETER, "seq_len must be positive");
+    sf_status bad = SF_OK;
+    if (!bsr_args_ok(d_bits, seq_len, block_m, block_n, &bad)) return bad;
     cudaStream_t st = as_stream(stream);
     sf::attn_reserve_counters(st);
     Geo g{seq_len, sf_mask_words(seq_len), block_m, block_n,
           static_cast<int32_t>(ceil_div(seq_len, block_m)), static_cast<int32_t>(ceil_div(seq_len, block_n))};
     const int64_t tiles = static_cast<int64_t>(g.n_rows) * g.n_cols;
-    if (tiles > (1ll << 31) - 1) return fail(SF_INVALID_PARAMETER, "tile grid too large");
-
-    // scratch 1: per-tile class + hash, per-row counts, row pointers, counts
-    char* s1 = nullptr;
-    const int64_t s1_bytes = ceil_div(tiles, 256) * 256 + ceil_div(tiles * 8, 256) * 256 +
-                             6 * (ceil_div((g.n_rows + 1) * 4, 256) * 256) + 256;
-    SF_CUDA_TRY(pool_malloc(reinterpret_cast<void**>(&s1), s1_bytes, st));
-    char* p = s1;
-    uint8_t* cls = carve<uint8_t>(p, tiles);
-    uint64_t* hash = carve<uint64_t>(p, tiles);
-    int32_t* fcnt = carve<int32_t>(p, g.n_rows + 1);
-    int32_t* pcnt = carve<int32_t>(p, g.n_rows + 1);
-    int32_t* lcnt = carve<int32_t>(p, g.n_rows + 1);
-    int32_t* fptr = carve<int32_t>(p, g.n_rows + 1);
-    int32_t* pptr = carve<int32_t>(p, g.n_rows + 1);
-    int32_t* lptr = carve<int32_t>(p, g.n_rows + 1);
-    int32_t* totals = carve<int32_t>(p, 4);
-
-    classify_kernel<<<blocks_for(tiles * 32), 256, 0, st>>>(d_bits, g, cls, hash);
-    SF_LAUNCH_CHECK();
-    row_count_kernel<<<g.n_rows, 256, 0, st>>>(cls, g, fcnt, pcnt, lcnt);
-    SF_LAUNCH_CHECK();
-    scan_exclusive3_kernel<<<dim3(1, 3), 1024, 0, st>>>(fcnt, pcnt, lcnt, fptr, pptr, lptr, g.n_rows, totals);
-    SF_LAUNCH_CHECK();
-    int32_t h_tot[3] = {0, 0, 0};
-    SF_CUDA_TRY(cudaMemcpyAsync(h_tot, totals, 12, cudaMemcpyDeviceToHost, st));
-    SF_CUDA_TRY(cudaStreamSynchronize(st));
-    const int32_t n_full = h_tot[0], n_part = h_tot[1], n_load = h_tot[2];
     const int32_t tile_bytes = static_cast<int32_t>(ceil_div(static_cast<int64_t>(block_m) * block_n, 8));
 
-    // output block (owned by the sf_bsr_dev)
-    const int64_t rp = g.n_rows + 1;
-    const int64_t out_bytes = 3 * ceil_div(rp * 4, 256) * 256 + ceil_div(std::max(1, n_full) * 4ll, 256) * 256 +
-                              2 * ceil_div(std::max(1, n_part) * 4ll, 256) * 256 +
-                              2 * ceil_div(std::max(1, n_load) * 4ll, 256) * 256 +
-                              ceil_div(imax64(1, static_cast<int64_t>(n_part) * tile_bytes), 256) * 256;
+    // phase 1, then the exact output sizes read back (this entry's one host round trip; use
+    // sf_bsr_build_async on a worst-case workspace to rebuild inside a CUDA graph)
+    char* s1b = nullptr;
+    SF_CUDA_TRY(pool_malloc(reinterpret_cast<void**>(&s1b), scratch1_bytes(tiles, g.n_rows), st));
+    char* p = s1b;
+    const Scratch1 s1 = carve_scratch1(p, tiles, g.n_rows);
+    sf_status rc = bsr_phase1(d_bits, g, s1, s1.fptr, s1.pptr, s1.lptr, st);
+    int32_t h_tot[3] = {0, 0, 0};
+    if (rc == SF_OK && cudaMemcpyAsync(h_tot, s1.totals, 12, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+        rc = fail(SF_CUDA_ERROR, "cudaMemcpyAsync (BSR sizes)");
+    if (rc == SF_OK && cudaStreamSynchronize(st) != cudaSuccess) rc = fail(SF_CUDA_ERROR, "cudaStreamSynchronize");
+    if (rc != SF_OK) {
+        cudaFreeAsync(s1b, st);
+        return rc;
+    }
+    const int32_t n_full = h_tot[0], n_part = h_tot[1], n_load = h_tot[2];
+
+    // outputs (owned by the sf_bsr_dev), sized exactly; the pool for the worst case of n_part
     char* ob = nullptr;
-    SF_CUDA_TRY(pool_malloc(reinterpret_cast<void**>(&ob), out_bytes, st));
+    char* s2b = nullptr;
+    const int64_t pool_cap = static_cast<int64_t>(n_part) * tile_bytes;
+    if (pool_malloc(reinterpret_cast<void**>(&ob), out_bytes(g.n_rows, n_full, n_part, n_load, pool_cap), st) !=
+            cudaSuccess ||
+        pool_malloc(reinterpret_cast<void**>(&s2b), scratch2_bytes(n_part, n_load), st) != cudaSuccess) {
+        cudaGetLastError();
+        if (ob) cudaFreeAsync(ob, st);
+        cudaFreeAsync(s1b, st);
+        return fail(SF_CUDA_ERROR, "BSR output allocation failed");
+    }
     p = ob;
-    out->full_row_ptr = carve<int32_t>(p, rp);
-    out->part_row_ptr = carve<int32_t>(p, rp);
-    out->load_row_ptr = carve<int32_t>(p, rp);
-    out->full_col_idx = carve<int32_t>(p, std::max(1, n_full));
-    out->part_col_idx = carve<int32_t>(p, std::max(1, n_part));
-    out->part_tile_ids = carve<int32_t>(p, std::max(1, n_part));
-    out->load_col_idx = carve<int32_t>(p, std::max(1, n_load));
-    out->load_tile = carve<int32_t>(p, std::max(1, n_load));
-    out->pool = carve<uint8_t>(p, imax64(1, static_cast<int64_t>(n_part) * tile_bytes));
+    carve_out(p, out, g.n_rows, n_full, n_part, n_load, pool_cap);
     out->_alloc = ob;
+    p = s2b;
+    const Scratch2 s2 = carve_scratch2(p, n_part, n_load);
     // the three row-pointer arrays are carved identically (256-byte aligned, back to back) in the
     // scratch and in the output block: one copy moves all three
-    SF_CUDA_TRY(cudaMemcpyAsync(out->full_row_ptr, fptr,
-                                static_cast<size_t>(reinterpret_cast<char*>(out->load_row_ptr) - reinterpret_cast<char*>(out->full_row_ptr)) + rp * 4,
-                                cudaMemcpyDeviceToDevice, st));
-
-    // scratch 2: dedup
-    uint32_t cap = 16;
-    while (cap < static_cast<uint32_t>(std::max(1, n_part)) * 2u) cap <<= 1;
-    char* s2 = nullptr;
-    const int64_t np1 = std::max(1, n_part);
-    const int64_t s2_bytes = 5 * ceil_div((np1 + 1) * 4, 256) * 256 + 2 * ceil_div(cap * 4ll, 256) * 256 +
-                             ceil_div(std::max(1, n_load) * 4ll, 256) * 256;
-    SF_CUDA_TRY(pool_malloc(reinterpret_cast<void**>(&s2), s2_bytes, st));
-    p = s2;
-    int32_t* part_lin = carve<int32_t>(p, np1);
-    int32_t* part_slot = carve<int32_t>(p, np1);
-    int32_t* first = carve<int32_t>(p, np1);
-    int32_t* first_scan = carve<int32_t>(p, np1 + 1);
-    int32_t* pool_src = carve<int32_t>(p, np1);
-    int32_t* table = carve<int32_t>(p, cap);
-    int32_t* slot_id = carve<int32_t>(p, cap);
-    int32_t* load_part = carve<int32_t>(p, std::max(1, n_load));
-    SF_CUDA_TRY(cudaMemsetAsync(table, 0xff, cap * 4ll, st));
-
-    if (n_load > 0) {
-        compact_kernel<<<g.n_rows, 256, 0, st>>>(cls, g, fptr, pptr, lptr, out->full_col_idx,
-                                                 out->part_col_idx, out->load_col_idx, part_lin, load_part);
-        SF_LAUNCH_CHECK();
-    }
+    rc = cudaMemcpyAsync(out->full_row_ptr, s1.fptr,
+                         static_cast<size_t>(reinterpret_cast<char*>(out->load_row_ptr) -
+                                             reinterpret_cast<char*>(out->full_row_ptr)) + (g.n_rows + 1) * 4ll,
+                         cudaMemcpyDeviceToDevice, st) == cudaSuccess
+             ? SF_OK
+             : fail(SF_CUDA_ERROR, "cudaMemcpyAsync (row pointers)");
+    if (rc == SF_OK) rc = bsr_phase2(d_bits, g, out, s1.fptr, s1.pptr, s1.lptr, s1, s2, n_part, n_load, tile_bytes, st);
     int32_t n_pool = 0;
-    if (n_part > 0) {
-        dedup_insert_kernel<<<blocks_for(static_cast<int64_t>(n_part) * 32), 256, 0, st>>>(
-            d_bits, g, n_part, part_lin, hash, table, cap - 1, part_slot);
-        SF_LAUNCH_CHECK();
-        first_flag_kernel<<<blocks_for(n_part), 256, 0, st>>>(n_part, part_lin, table, part_slot, first);
-        SF_LAUNCH_CHECK();
-        SF_TRY(scan_exclusive(first, first_scan, n_part, totals + 3, st));
-        slot_id_kernel<<<blocks_for(n_part), 256, 0, st>>>(n_part, first, first_scan, part_slot, slot_id, pool_src);
-        SF_LAUNCH_CHECK();
-        tile_ids_kernel<<<blocks_for(n_part), 256, 0, st>>>(n_part, part_slot, slot_id, out->part_tile_ids);
-        SF_LAUNCH_CHECK();
-        pool_write_kernel<<<blocks_for(static_cast<int64_t>(n_part) * 32), 256, 0, st>>>(
-            d_bits, g, totals + 3, pool_src, part_lin, tile_bytes, out->pool);
-        SF_LAUNCH_CHECK();
+    if (rc == SF_OK && n_part > 0) {  // the pool size for the host struct: the build's trailing sync
+        if (cudaMemcpyAsync(&n_pool, s1.totals + 3, 4, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+            cudaStreamSynchronize(st) != cudaSuccess)
+            rc = fail(SF_CUDA_ERROR, "BSR pool size read-back");
     }
-    if (n_load > 0) {
-        load_tile_kernel<<<blocks_for(n_load), 256, 0, st>>>(n_load, load_part, out->part_tile_ids, out->load_tile);
-        SF_LAUNCH_CHECK();
+    cudaFreeAsync(s2b, st);
+    cudaFreeAsync(s1b, st);
+    if (rc != SF_OK) {
+        cudaFreeAsync(ob, st);
+        *out = sf_bsr_dev{};
+        return rc;
     }
-    if (n_part > 0) {  // the pool size for the host struct: the build's one trailing sync
-        SF_CUDA_TRY(cudaMemcpyAsync(&n_pool, totals + 3, 4, cudaMemcpyDeviceToHost, st));
-        SF_CUDA_TRY(cudaStreamSynchronize(st));
-    }
-    SF_CUDA_TRY(cudaFreeAsync(s2, st));
-    SF_CUDA_TRY(cudaFreeAsync(s1, st));
-
     out->seq_len = seq_len;
     out->block_m = block_m;
     out->block_n = block_n;
@@ -603,6 +705,56 @@ extern "C" sf_status sf_bsr_build(const uint32_t* d_bits, int32_t seq_len, int32
     out->n_load = n_load;
     out->n_pool = n_pool;
     out->tile_bytes = tile_bytes;
+    return SF_OK;
+}
+
+// Worst-case workspace: outputs sized for the whole tile grid (every tile full, part and loaded;
+// the pool for every tile), followed by both scratch blocks, in one owned allocation.
+extern "C" sf_status sf_bsr_workspace(int32_t seq_len, int32_t block_m, int32_t block_n, sf_bsr_dev* ws,
+                                      void* stream) {
+    if (!ws) return fail(SF_INVALID_PARAMETER, "null output");
+    *ws = sf_bsr_dev{};
+    sf_status bad = SF_OK;
+    const uint32_t dummy = 0;
+    if (!bsr_args_ok(&dummy, seq_len, block_m, block_n, &bad)) return bad;
+    cudaStream_t st = as_stream(stream);
+    sf::attn_reserve_counters(st);
+    const int64_t n_rows = ceil_div(seq_len, block_m), n_cols = ceil_div(seq_len, block_n), tiles = n_rows * n_cols;
+    const int32_t tile_bytes = static_cast<int32_t>(ceil_div(static_cast<int64_t>(block_m) * block_n, 8));
+    const int64_t total = out_bytes(n_rows, tiles, tiles, tiles, tiles * tile_bytes) + scratch1_bytes(tiles, n_rows) +
+                          scratch2_bytes(tiles, tiles);
+    char* blk = nullptr;
+    SF_CUDA_TRY(pool_malloc(reinterpret_cast<void**>(&blk), total, st));
+    char* p = blk;
+    carve_out(p, ws, n_rows, tiles, tiles, tiles, tiles * tile_bytes);
+    ws->_alloc = blk;
+    ws->seq_len = seq_len;
+    ws->block_m = block_m;
+    ws->block_n = block_n;
+    ws->n_rows = static_cast<int32_t>(n_rows);
+    ws->n_cols = static_cast<int32_t>(n_cols);
+    ws->n_full = ws->n_part = ws->n_load = ws->n_pool = static_cast<int32_t>(tiles);  // capacities
+    ws->tile_bytes = tile_bytes;
+    return SF_OK;
+}
+
+extern "C" sf_status sf_bsr_build_async(const uint32_t* d_bits, sf_bsr_dev* ws, int32_t* d_counts, void* stream) {
+    if (!ws || !ws->_alloc) return fail(SF_INVALID_PARAMETER, "BSR workspace not allocated (sf_bsr_workspace)");
+    sf_status bad = SF_OK;
+    if (!bsr_args_ok(d_bits, ws->seq_len, ws->block_m, ws->block_n, &bad)) return bad;
+    cudaStream_t st = as_stream(stream);
+    const Geo g{ws->seq_len, sf_mask_words(ws->seq_len), ws->block_m, ws->block_n, ws->n_rows, ws->n_cols};
+    const int64_t tiles = static_cast<int64_t>(g.n_rows) * g.n_cols;
+    char* p = static_cast<char*>(ws->_alloc);
+    sf_bsr_dev layout{};
+    carve_out(p, &layout, g.n_rows, tiles, tiles, tiles, tiles * ws->tile_bytes);  // skip the output block
+    const Scratch1 s1 = carve_scratch1(p, tiles, g.n_rows);
+    const Scratch2 s2 = carve_scratch2(p, tiles, tiles);
+    // the row pointers are scanned straight into the workspace's output arrays
+    SF_TRY(bsr_phase1(d_bits, g, s1, ws->full_row_ptr, ws->part_row_ptr, ws->load_row_ptr, st));
+    SF_TRY(bsr_phase2(d_bits, g, ws, ws->full_row_ptr, ws->part_row_ptr, ws->load_row_ptr, s1, s2, tiles, tiles,
+                      ws->tile_bytes, st));
+    if (d_counts) SF_CUDA_TRY(cudaMemcpyAsync(d_counts, s1.totals, 16, cudaMemcpyDeviceToDevice, st));
     return SF_OK;
 }
 

@@ -261,6 +261,34 @@ def to_dense(b: BsrMask, stream=None) -> DenseMask:
     return m
 
 
+class BsrWorkspace(BsrMask):
+    """A worst-case-sized BSR (sf_bsr_workspace) rebuilt in place by build_async() with no host
+    synchronisation — capturable in a CUDA graph next to the attention that reads it. The device
+    counts land in `counts` (int32 [4]: n_full, n_part, n_load, n_pool)."""
+
+    def __init__(self, seq_len: int, block_m: int, block_n: int, stream=None):
+        dev = BsrDev()
+        check(lib().sf_bsr_workspace(seq_len, block_m, block_n, C.byref(dev), _stream(stream)))
+        super().__init__(dev)
+        self.counts = torch.zeros(4, dtype=torch.int32, device="cuda")
+
+    def build_async(self, mask: DenseMask, stream=None) -> "BsrWorkspace":
+        if mask.seq_len != self.dev.seq_len:
+            raise _lib.ShapeError("mask seq_len differs from the workspace")
+        check(lib().sf_bsr_build_async(mask.bits.data_ptr(), C.byref(self.dev), self.counts.data_ptr(), _stream(stream)))
+        return self
+
+    def snapshot(self) -> BsrMask:
+        """A non-owning view with the built counts (reads `counts`: synchronises) for to_host / sfbr."""
+        n = self.counts.cpu().tolist()
+        d = BsrDev.from_buffer_copy(self.dev)
+        d.n_full, d.n_part, d.n_load, d.n_pool = n
+        d._alloc = None  # the workspace owns the memory
+        v = BsrMask(d)
+        v._owner = self
+        return v
+
+
 def build_bsr(mask: DenseMask, block_m: int, block_n: int, stream=None) -> BsrMask:
     dev = BsrDev()
     check(lib().sf_bsr_build(mask.bits.data_ptr(), mask.seq_len, block_m, block_n, C.byref(dev), _stream(stream)))

@@ -1,0 +1,40 @@
+"""The N > 1 bench path on one B200 (two ranks share cuda:0 over gloo, SF_BENCH_SHARED_GPU=1 —
+NCCL refuses two ranks on one device, and gpurun gives one GPU): the configured batch is sharded
+over the ranks, the gathered layer output equals the same layer on the whole batch, and the
+(b, h)-sharded cfg5 sweep runs. Launched exactly like the driver's N > 1 runs (torchrun)."""
+import json
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def _torchrun(args, port):
+    env = dict(os.environ, SF_BENCH_SHARED_GPU="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(ROOT / "bench.py")] + args
+    r = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-4000:]
+    return [json.loads(ln) for ln in r.stdout.splitlines() if ln.startswith("{")]
+
+
+def test_two_rank_layer_shards_the_batch_and_gathers_exactly():
+    lines = _torchrun(["--gpus", "2", "--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--check-gather"],
+                      29610 + os.getpid() % 200)
+    assert len(lines) == 1
+    ln = lines[0]
+    assert ln["n_gpus"] == 2 and ln["config"]["global_batch"] == 16 and ln["scaling"] == "strong"
+    gc = ln["gather_check"]
+    assert gc["world"] == 2 and gc["max_abs"] <= 2e-2, gc
+    assert gc["bit_exact"], gc  # 8 sequences per rank take the same kernel variants as 16
+
+
+def test_two_rank_sweep_shards_slices():
+    lines = _torchrun(["--sweep", "--patterns", "bigbird", "--seqs", "1024", "--steps", "5", "--no-cpu-baseline"],
+                      29810 + os.getpid() % 200)
+    assert len(lines) == 1 and lines[0]["n_gpus"] == 2 and lines[0]["slices_per_rank"] == 96

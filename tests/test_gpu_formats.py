@@ -222,3 +222,53 @@ def test_sfmk_errors(sf):
         sf.DenseMask.from_sfmk(data[:4] + np.array([2], np.uint32).tobytes() + data[8:])  # :82 version
     with pytest.raises(sf._lib.IoError):
         sf.DenseMask.from_sfmk(data[:-1])  # :88 truncated
+
+
+def test_async_build_equals_build_bsr(sf, oracle):
+    """sf_bsr_build_async on a worst-case workspace (no host sync) yields the same SFBR bytes as
+    sf_bsr_build, on random masks (test_bsr.cpp:65-84 shapes) and the BASELINE masks."""
+    rng = np.random.default_rng(77)
+    cases = []
+    for _ in range(100):
+        n = int(rng.integers(1, 97)); bm = int(rng.integers(1, 25)); bn = int(rng.integers(1, 25))
+        cases.append(((rng.random((n, n)) < rng.random()).astype(np.uint8), bm, bn))
+    for cfg in ("cfg2", "cfg3", "cfg4"):
+        m = oracle.mask(CONFIG_MASKS[cfg])
+        cases += [(m, 128, 16), (m, 16, 16)]
+    for m, bm, bn in cases:
+        dm = sf.DenseMask.from_numpy(m)
+        ws = sf.BsrWorkspace(dm.seq_len, bm, bn).build_async(dm)
+        assert ws.snapshot().sfbr() == sf.build_bsr(dm, bm, bn).sfbr(), (m.shape, bm, bn)
+
+
+def test_async_build_inside_a_cuda_graph(sf):
+    """Mask -> BSR -> attention captured as ONE graph; new mask bits written into the captured mask
+    buffer take effect at the next replay (per-request masks without host round trips)."""
+    import torch
+    n, bs, h, d = 1024, 2, 4, 64
+    masks = [sf.generate_mask([dict(pattern="bigbird", seq_len=n, global_width=32, band_width=32,
+                                    filling_rate=0.1, seed=s)]) for s in (1, 2)]
+    mbuf = sf.DenseMask(n, masks[0].bits.clone())
+    g = torch.Generator(device="cuda").manual_seed(3)
+    q, k, v = ((torch.rand(bs, h, n, d, device="cuda", generator=g) * 2 - 1).half() for _ in range(3))
+    ws = sf.BsrWorkspace(n, 128, 16)
+    out = torch.empty_like(q)
+    st = torch.cuda.Stream()
+    st.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(st):  # warm on the capture stream (attention work counter)
+        ws.build_async(mbuf, stream=st)
+        sf.block_sparse_sdpa(q, k, v, ws, out=out, stream=st)
+    torch.cuda.synchronize()
+    gr = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gr, stream=st):
+        ws.build_async(mbuf, stream=st)
+        sf.block_sparse_sdpa(q, k, v, ws, out=out, stream=st)
+    for m in masks + masks[:1]:
+        mbuf.bits.copy_(m.bits)
+        out.zero_()
+        gr.replay()
+        torch.cuda.synchronize()
+        ref = sf.block_sparse_sdpa(q, k, v, sf.build_bsr(m, 128, 16))
+        torch.cuda.synchronize()
+        assert torch.equal(out, ref)
+        assert ws.counts.cpu().tolist()[2] == sf.build_bsr(m, 128, 16).n_load
