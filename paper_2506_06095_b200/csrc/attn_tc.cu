@@ -45,12 +45,7 @@ constexpr int kStages = 4;                   // K/V ring depth (two CTAs per SM 
 constexpr int kSBuf = 2;
 constexpr uint32_t kPCol = 128, kOCol = 192;
 constexpr int kMaxRowBlocks = 128;           // n <= 8192 at block_m 64
-constexpr int kQBytes = kBM * kD * 2;
-constexpr int kKVBytes = kNS * kD * 2;       // one 64-key stage of K (or V)
-constexpr int kMaskBytes = kBM * 8;          // 64 bits per query row per stage
 constexpr float kRescaleLog2 = 8.0f;         // lazy-rescale threshold (P <= 2^8)
-constexpr int kSmem = 1024 + 2 * kQBytes + 2 * kStages * kKVBytes + kStages * kMaskBytes + kStages * 16 +
-                      kMaxRowBlocks * 4 + 512;
 
 // Geometry per query-block height. BM = 128: one (b, h) slice per work item, M = 128 MMAs.
 // BM = 64 ("head pair"): a work item is one 64-row block of TWO heads that share the block's load
@@ -68,7 +63,7 @@ struct AttnGeo {
     static constexpr int kKVB = kHeads * kNS * kD * 2;         // one stage of K (or V), all heads
     static constexpr int kMaskB = BM * 8;                      // 64 bits per query row per stage
     static constexpr int kSmemG = 1024 + 2 * kQB + 2 * kStagesG * kKVB + kStagesG * kMaskB + kStagesG * 16 +
-                                  kMaxRowBlocks * 4 + 512;
+                                  kMaxRowBlocks * 4 + (kMaxRowBlocks + 4) * 4 + 512;
 };
 
 struct AttnParams {
@@ -164,11 +159,6 @@ __device__ __forceinline__ uint32_t lds_u16(uint32_t addr) {
     asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(addr));
     return v;
 }
-__device__ __forceinline__ int4 lds_v4(uint32_t addr) {
-    int4 v;
-    asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
-    return v;
-}
 
 __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* m, uint64_t* bar, int32_t c0, int32_t c1,
                                             int32_t c2, int32_t c3) {
@@ -212,14 +202,6 @@ struct Items {
         const int g = static_cast<int>(gridDim.x);
         const int full = n_items / g, rem = n_items % g;
         return full + (rem > 0 && pos(full) < rem ? 1 : 0);
-    }
-    __device__ __forceinline__ void get(int k, int& rb, int& bh, int& l0, int& L, int& nsteps) const {
-        const int idx = k * static_cast<int>(gridDim.x) + pos(k);
-        rb = order[idx / bh_count];
-        bh = idx % bh_count;
-        l0 = lrp[rb];
-        L = lrp[rb + 1] - l0;
-        nsteps = (L + G - 1) / G;
     }
 };
 
@@ -279,7 +261,9 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
     unsigned char* sV = sK + kStages * kKVBytes;
     unsigned char* sMask = sV + kStages * kKVBytes;        // [kStages][BM * 8 B]: packed part-tile bits
     int32_t* s_order = reinterpret_cast<int32_t*>(sMask + kStages * kMaskBytes) + 4 * kStages;  // [kMaxRowBlocks]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(s_order + kMaxRowBlocks);
+    // load_row_ptr cached in smem: item decodes at item boundaries read no global memory
+    int32_t* s_lrp = s_order + kMaxRowBlocks;  // [n_rows + 1]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(s_lrp + kMaxRowBlocks + 4);
     uint64_t* q_full = bars;                  // [2]
     uint64_t* q_empty = q_full + 2;           // [2]
     // K (with the stage's bit rows) and V have separate barriers: a K slot is
@@ -312,6 +296,8 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
             rank += (Li > Lr) || (Li == Lr && i < r);
         }
         s_order[rank] = r;
+        s_lrp[r] = p.load_row_ptr[r];
+        if (r == p.n_rows - 1) s_lrp[p.n_rows] = p.load_row_ptr[p.n_rows];
     }
     if (warp == 0 && lane == 0) {
         tc::prefetch_tmap(&p.tq);
@@ -344,7 +330,7 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
     tc::fence_after_sync();
     const uint32_t tmem = *tmem_ptr;
     const uint32_t tO = tmem + kOCol;
-    const Items items{p.load_row_ptr, s_order, p.bh, p.n_items, G};
+    const Items items{s_lrp, s_order, p.bh, p.n_items, G};
     const ItemFeed feed{s_item, item_full, item_empty};
 
     if (warp == 0) {
@@ -523,6 +509,49 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
         const int my_head = kPair ? static_cast<int>(lane >> 4) : 0;
         const uint32_t trow = tmem + ((q * 32) << 16);
         const float sl2 = p.scale_log2;
+        // ---- epilogue of an item: out = O / l; rows without a valid column stay zero
+        // (attention.hpp:160-166). It is DEFERRED: the item's last P.V is still running when its
+        // last P is published, so the warps first compute the next item's step-0 probabilities and
+        // only then wait for that P.V and read O, just before publishing P_0 of the next item (whose
+        // P.V overwrites O). The wait for the last P.V hides behind a softmax step.
+        auto epilogue = [&](int rb_, int bh_, float l_, bool have_o, uint32_t g_last) {
+            const int slice = kPair ? 2 * bh_ + my_head : bh_;
+            const bool slice_ok = slice < p.bh_total;  // an odd last head pair has no head B
+            const int b = slice_ok ? slice / p.h : 0, hh = slice_ok ? slice % p.h : 0;
+            const int64_t i = static_cast<int64_t>(rb_) * BM + r;
+            if (have_o) {
+                tc::mbar_wait(&o_full[g_last & 1], (g_last >> 1) & 1);
+                tc::fence_after_sync();
+            }
+            const float inv = (have_o && l_ > 0.f) ? 1.f / l_ : 0.f;
+            uint4* dst = reinterpret_cast<uint4*>(static_cast<T*>(p.o) + b * p.o_sb + hh * p.o_sh + i * p.o_sn);
+#pragma unroll
+            for (int h2 = 0; h2 < 2; ++h2) {
+                uint32_t ov[32];
+                if (have_o) {
+                    tc::tmem_ld32(tO + ((q * 32) << 16) + 32 * h2, ov);
+                    tc::tmem_ld_wait();
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) ov[e] = 0u;
+                }
+                if (i < p.n && slice_ok) {
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        float v[8];
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) v[e] = __uint_as_float(ov[c * 8 + e]) * inv;
+                        dst[4 * h2 + c] = make_uint4(pack2<T>(v[0], v[1]), pack2<T>(v[2], v[3]), pack2<T>(v[4], v[5]),
+                                                     pack2<T>(v[6], v[7]));
+                    }
+                }
+            }
+            tc::fence_before_sync();  // O reads ordered before the next item's first P.V (p_full)
+        };
+        bool pend = false;  // an item whose epilogue is deferred into the next item's step 0
+        int pend_rb = 0, pend_bh = 0;
+        float pend_l = 0.f;
+        uint32_t pend_g = 0;
         uint32_t g = 0;
         for (uint32_t k = 0;; ++k) {
             const int idx = feed.read(k);
@@ -536,9 +565,9 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
                 const int st = g % kStages;
                 const int sb = g % kSBuf;
                 const bool tr = warp == 2 && lane == 0 && k == 0;
-                const bool trw = lane == 0 && k == 0;  // per-warp events 16 + 4 (warp - 2) + {0..3}
+                const bool trw = lane == 0;  // per-warp events 16 + 4 (warp - 2) + {0..3}, by CTA step g
                 if (tr) SF_TRACE(j, 0);
-                if (trw) SF_TRACE(j, 16 + 4 * (warp - 2));
+                if (trw) SF_TRACE(g, 16 + 4 * (warp - 2));
                 tc::mbar_wait(&k_full[st], (g / kStages) & 1);
                 if (tr) SF_TRACE(j, 1);
                 // this row's 64 mask bits (the producer staged every tile's rows: full -> ones,
@@ -560,7 +589,7 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
                 }
                 tc::mbar_wait(&s_full[sb], (g / kSBuf) & 1);
                 if (tr) SF_TRACE(j, 2);
-                if (trw) SF_TRACE(j, 17 + 4 * (warp - 2));
+                if (trw) SF_TRACE(g, 17 + 4 * (warp - 2));
                 tc::fence_after_sync();
                 uint32_t raw0[32], raw1[32];
                 tc::tmem_ld32(trow + 64 * sb, raw0);
@@ -598,7 +627,7 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
                 // max of the raw scores, then scaled: scale > 0 commutes with max (log2 domain)
                 const float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * sl2;
                 if (tr) SF_TRACE(j, 3);
-                if (trw) SF_TRACE(j, 18 + 4 * (warp - 2));
+                if (trw) SF_TRACE(g, 18 + 4 * (warp - 2));
                 // lazy max update: rescale O / l only when the max grows by > 2^8 (or first time).
                 // tcgen05.ld/st are warp-collective: the rescale is voted warp-uniformly and lanes
                 // that do not need it scale by 1.
@@ -646,48 +675,29 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
                     }
                 }
                 l += (rs2[0].x + rs2[0].y) + (rs2[1].x + rs2[1].y);
+                if (j == 0 && pend) {  // the previous item's O is read before P_0 lets P.V overwrite it
+                    epilogue(pend_rb, pend_bh, pend_l, true, pend_g);
+                    pend = false;
+                }
                 // P_g (64 keys = 32 packed columns) into P[sb] in TMEM
                 tc::tmem_st32(trow + kPCol + 32 * sb, pk);
                 tc::tmem_st_wait();
                 tc::fence_before_sync();
                 tc::mbar_arrive(&p_full[sb]);
                 if (tr) SF_TRACE(j, 6);
-                if (trw) SF_TRACE(j, 19 + 4 * (warp - 2));
+                if (trw) SF_TRACE(g, 19 + 4 * (warp - 2));
             }
-            // ---- epilogue: out = O / l; rows without a valid column stay zero
-            const int slice = kPair ? 2 * bh + my_head : bh;
-            const bool slice_ok = slice < p.bh_total;  // an odd last head pair has no head B
-            const int b = slice_ok ? slice / p.h : 0, hh = slice_ok ? slice % p.h : 0;
-            const int64_t i = static_cast<int64_t>(rb) * BM + r;
             if (nsteps > 0) {
-                tc::mbar_wait(&o_full[(g - 1) & 1], ((g - 1) >> 1) & 1);
-                tc::fence_after_sync();
+                pend = true;
+                pend_rb = rb;
+                pend_bh = bh;
+                pend_l = l;
+                pend_g = g - 1;
+            } else {
+                epilogue(rb, bh, 0.f, false, 0);  // an empty row block: zeros, no TMEM access
             }
-            const float inv = (nsteps > 0 && l > 0.f) ? 1.f / l : 0.f;
-            uint4* dst = reinterpret_cast<uint4*>(static_cast<T*>(p.o) + b * p.o_sb + hh * p.o_sh + i * p.o_sn);
-#pragma unroll
-            for (int h2 = 0; h2 < 2; ++h2) {
-                uint32_t ov[32];
-                if (nsteps > 0) {
-                    tc::tmem_ld32(tO + ((q * 32) << 16) + 32 * h2, ov);
-                    tc::tmem_ld_wait();
-                } else {
-#pragma unroll
-                    for (int e = 0; e < 32; ++e) ov[e] = 0u;
-                }
-                if (i < p.n && slice_ok) {
-#pragma unroll
-                    for (int c = 0; c < 4; ++c) {
-                        float v[8];
-#pragma unroll
-                        for (int e = 0; e < 8; ++e) v[e] = __uint_as_float(ov[c * 8 + e]) * inv;
-                        dst[4 * h2 + c] = make_uint4(pack2<T>(v[0], v[1]), pack2<T>(v[2], v[3]), pack2<T>(v[4], v[5]),
-                                                     pack2<T>(v[6], v[7]));
-                    }
-                }
-            }
-            tc::fence_before_sync();  // O reads ordered before the next item's first P.V (p_full)
         }
+        if (pend) epilogue(pend_rb, pend_bh, pend_l, true, pend_g);
     }
     tc::fence_before_sync();
     __syncthreads();

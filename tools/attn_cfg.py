@@ -27,11 +27,12 @@ def best_us(fn, reps=20):
         best = min(best, a.elapsed_time(b) / 5)
     return best * 1e3
 
-SHAPES = {"cfg2": (16, 1024), "cfg3": (8, 2048), "cfg4": (8, 4096)}
+SHAPES = {"cfg2": (16, 1024), "cfg3": (8, 2048), "cfg4": (8, 4096), "dense": (16, 1024)}
 TERMS = {"cfg2": [dict(pattern="bigbird", seq_len=1024, global_width=32, band_width=32, filling_rate=0.10, seed=0, block=16)],
          "cfg3": [dict(pattern="strided", seq_len=2048, band_width=45)],
          "cfg4": [dict(pattern="dilated", seq_len=4096, band_width=64, dilation_rate=1),
-                  dict(pattern="global", seq_len=4096, global_width=64)]}
+                  dict(pattern="global", seq_len=4096, global_width=64)],
+         "dense": [dict(pattern="sliding", seq_len=1024, band_width=1024)]}
 if __name__ == "__main__":
     for cfg in sys.argv[1:] or ["cfg2", "cfg3", "cfg4"]:
         bs, n = SHAPES[cfg]

@@ -27,8 +27,9 @@ for name, dm, bn in (("dense", sf.gen_sliding_window(n, n), 16), ("dense", sf.ge
         if t[j, 0] == 0: break
         r = t[j] - t0
         print(f"j={j:2d} " + " ".join(f"{e}:{r[e]:7d}" for e in (4, 5, 7, 11, 0, 1, 2, 3, 6, 8, 9, 13, 14, 10)))
-    print("per softmax warp (lane 0): top / S seen / max done / P arrived, warps 2..5 (SMSP 2,3,0,1)")
-    for j in range(16):
-        if t[j, 0] == 0: break
+    print("per softmax warp (lane 0), by CTA step g (across items): top / S seen / max done / P arrived, warps 2..5 (SMSP 2,3,0,1) | MMA P seen, PV issued, S(g+2) issued")
+    for j in range(64):
+        if t[j, 16] == 0: break
         r = t[j] - t0
-        print(f"j={j:2d} " + " | ".join(" ".join(f"{r[16 + 4 * w + e]:7d}" for e in range(4)) for w in range(4)))
+        print(f"g={j:2d} " + " | ".join(" ".join(f"{r[16 + 4 * w + e]:7d}" for e in range(4)) for w in range(4))
+              + f" | {r[8]:7d} {r[9]:7d} {r[10]:7d}")

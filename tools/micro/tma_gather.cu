@@ -72,8 +72,54 @@ __global__ void __launch_bounds__(64 + 32 * PW) gather(const __grid_constant__ C
     }
 }
 
+// HEADS heads per box ({64, BOX, HEADS, 1}): one TMA instruction fetches the same key block of
+// HEADS adjacent heads (items of one row block share the load list across heads); a stage holds
+// HEADS x 64 keys of K and of V.
+template <int BOX, int STAGES, int ISSUERS, int HEADS>
+__global__ void __launch_bounds__(96) gather_heads(const __grid_constant__ CUtensorMap tk, const __grid_constant__ CUtensorMap tv,
+                                                   int steps, int nblk, int h, int bs) {
+    extern __shared__ __align__(1024) unsigned char dsm[];
+    unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(dsm) + 1023) & ~uintptr_t(1023));
+    __shared__ uint64_t full[STAGES], empty[STAGES];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    constexpr int G = 64 / BOX;
+    constexpr int kStage = HEADS * 16384;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) { tc::mbar_init(&full[s], 1); tc::mbar_init(&empty[s], 1); }
+        tc::fence_barrier_init();
+    }
+    __syncthreads();
+    if (warp == 0) {
+        for (int g = 0; g < steps; ++g) {
+            const int st = g % STAGES;
+            const uint32_t ph = ((g / STAGES) & 1) ^ 1;
+            if (lane == 0) {
+                tc::mbar_wait(&empty[st], ph);
+                tc::mbar_expect_tx(&full[st], kStage);
+            }
+            __syncwarp();
+            const uint32_t hs = hash(blockIdx.x * 7919u + g);
+            const int hp = hs % (h / HEADS), b = (hs / 97) % bs;
+            if (lane < ISSUERS) {
+                for (int gg = lane; gg < G; gg += ISSUERS) {
+                    const int cb = hash(hs + gg) % nblk;
+                    unsigned char* k = base + st * kStage + gg * BOX * 128 * HEADS;
+                    tma4(k, &tk, &full[st], 0, cb * BOX, hp * HEADS, b);
+                    tma4(k + kStage / 2, &tv, &full[st], 0, cb * BOX, hp * HEADS, b);
+                }
+            }
+        }
+    } else if (warp == 1 && lane == 0) {
+        for (int g = 0; g < steps; ++g) {
+            const int st = g % STAGES;
+            tc::mbar_wait(&full[st], (g / STAGES) & 1);
+            tc::mbar_arrive(&empty[st]);
+        }
+    }
+}
+
 static PFN_cuTensorMapEncodeTiled_v12000 encode;
-static CUtensorMap map4(const void* base, int n, int h, int bs, long sn, long sh, long sb, int box);
+static CUtensorMap map4(const void* base, int n, int h, int bs, long sn, long sh, long sb, int box, int bh = 1);
 
 // The same gather with cp.async (LDGSTS, 16 B per thread) from PW producer warps; each thread
 // signals the stage barrier with cp.async.mbarrier.arrive.noinc once its copies land.
@@ -156,17 +202,42 @@ void run_lsu(const CUtensorMap& tk, const __half* kb, const __half* vb, int n, i
     if (cudaGetLastError() != cudaSuccess) { printf("error\n"); exit(1); }
 }
 
-static CUtensorMap map4(const void* base, int n, int h, int bs, long sn, long sh, long sb, int box) {
+static CUtensorMap map4(const void* base, int n, int h, int bs, long sn, long sh, long sb, int box, int bh) {
     CUtensorMap m;
     const cuuint64_t dims[4] = {64, (cuuint64_t)n, (cuuint64_t)h, (cuuint64_t)bs};
     const cuuint64_t strides[3] = {(cuuint64_t)sn * 2, (cuuint64_t)sh * 2, (cuuint64_t)sb * 2};
-    const cuuint32_t boxd[4] = {64, (cuuint32_t)box, 1, 1};
+    const cuuint32_t boxd[4] = {64, (cuuint32_t)box, (cuuint32_t)bh, 1};
     const cuuint32_t estr[4] = {1, 1, 1, 1};
     CUresult r = encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, const_cast<void*>(base), dims, strides, boxd, estr,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) { printf("encode failed %d\n", (int)r); exit(1); }
     return m;
+}
+
+template <int BOX, int STAGES, int ISSUERS, int HEADS>
+void run_heads(const CUtensorMap& tk, const CUtensorMap& tv, int n, int h, int bs, int sms, int cps) {
+    auto kern = gather_heads<BOX, STAGES, ISSUERS, HEADS>;
+    const int smem = STAGES * HEADS * 16384 + 1024;
+    if (cps * smem > 228 * 1024) return;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    const int steps = 2000, grid = sms * cps;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0); cudaEventCreate(&e1);
+    for (int it = 0; it < 2; ++it) kern<<<grid, 96, smem>>>(tk, tv, steps, n / BOX, h, bs);
+    cudaEventRecord(e0);
+    const int reps = 5;
+    for (int it = 0; it < reps; ++it) kern<<<grid, 96, smem>>>(tk, tv, steps, n / BOX, h, bs);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms; cudaEventElapsedTime(&ms, e0, e1);
+    const double bytes = double(reps) * grid * steps * 16384.0 * HEADS;
+    const double s = ms * 1e-3;
+    int clk; cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
+    printf("box %2dx%d heads stages %d issuers %d ctas/SM %d: %7.1f GB/s  %5.1f B/clk/SM  %6.0f clk per 64-key step (all heads) per CTA\n",
+           BOX, HEADS, STAGES, ISSUERS, cps, bytes / s / 1e9, bytes / s / (clk * 1e3) / sms,
+           s * clk * 1e3 / (double(reps) * steps));
+    if (cudaGetLastError() != cudaSuccess) { printf("error\n"); exit(1); }
 }
 
 template <int BOX, int STAGES, int ISSUERS, int PW = 1>
@@ -220,6 +291,19 @@ int main() {
             } else {
                 run<64, 4, 1>(tk, tv, n, h, bs, sms, cps);
                 run<64, 8, 1>(tk, tv, n, h, bs, sms, cps);
+            }
+        }
+    }
+    for (int hb : {2, 4}) {
+        CUtensorMap tk = map4(qkv + H, n, h, bs, 3 * H, 64, long(n) * 3 * H, 16, hb);
+        CUtensorMap tv = map4(qkv + 2 * H, n, h, bs, 3 * H, 64, long(n) * 3 * H, 16, hb);
+        for (int cps : {1, 2}) {
+            if (hb == 2) {
+                run_heads<16, 2, 4, 2>(tk, tv, n, h, bs, sms, cps);
+                run_heads<16, 3, 4, 2>(tk, tv, n, h, bs, sms, cps);
+                run_heads<16, 2, 1, 2>(tk, tv, n, h, bs, sms, cps);
+            } else {
+                run_heads<16, 2, 4, 4>(tk, tv, n, h, bs, sms, cps);
             }
         }
     }
