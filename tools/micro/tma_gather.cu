@@ -72,6 +72,116 @@ __global__ void __launch_bounds__(64 + 32 * PW) gather(const __grid_constant__ C
     }
 }
 
+// NB barriers per stage: box gg (K and V) completes on barrier gg % NB, the consumer waits all NB
+// (is the per-CTA box rate limited by complete_tx updates to ONE mbarrier?)
+template <int BOX, int STAGES, int NB>
+__global__ void __launch_bounds__(96) gather_nb(const __grid_constant__ CUtensorMap tk, const __grid_constant__ CUtensorMap tv,
+                                              int steps, int nblk, int h, int bs) {
+    extern __shared__ __align__(1024) unsigned char dsm[];
+    unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(dsm) + 1023) & ~uintptr_t(1023));
+    __shared__ uint64_t full[STAGES][NB], empty[STAGES];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    constexpr int G = 64 / BOX;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) { for (int b = 0; b < NB; ++b) tc::mbar_init(&full[s][b], 1); tc::mbar_init(&empty[s], 1); }
+        tc::fence_barrier_init();
+    }
+    __syncthreads();
+    if (warp == 0) {
+        for (int g = 0; g < steps; ++g) {
+            const int st = g % STAGES;
+            const uint32_t ph = ((g / STAGES) & 1) ^ 1;
+            if (lane == 0) {
+                tc::mbar_wait(&empty[st], ph);
+                for (int b = 0; b < NB; ++b) tc::mbar_expect_tx(&full[st][b], 2 * 64 * 128 / NB);
+            }
+            __syncwarp();
+            const uint32_t hs = hash(blockIdx.x * 7919u + g);
+            const int slice = hs % (h * bs);
+            if (lane < G) {
+                const int gg = lane;
+                const int cb = hash(hs + gg) % nblk;
+                unsigned char* k = base + st * 16384 + gg * BOX * 128;
+                tma4(k, &tk, &full[st][gg % NB], 0, cb * BOX, slice % h, slice / h);
+                tma4(k + 8192, &tv, &full[st][(gg + (NB > G ? G : 0)) % NB], 0, cb * BOX, slice % h, slice / h);
+            }
+        }
+    } else if (warp == 1 && lane == 0) {
+        for (int g = 0; g < steps; ++g) {
+            const int st = g % STAGES;
+            for (int b = 0; b < NB; ++b) tc::mbar_wait(&full[st][b], (g / STAGES) & 1);
+            tc::mbar_arrive(&empty[st]);
+        }
+    }
+}
+
+template <int BOX, int STAGES, int NB>
+void run_nb(const CUtensorMap& tk, const CUtensorMap& tv, int n, int h, int bs, int sms, int cps) {
+    auto kern = gather_nb<BOX, STAGES, NB>;
+    const int smem = STAGES * 16384 + 1024;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    const int steps = 2000, grid = sms * cps;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0); cudaEventCreate(&e1);
+    for (int it = 0; it < 2; ++it) kern<<<grid, 96, smem>>>(tk, tv, steps, n / BOX, h, bs);
+    cudaEventRecord(e0);
+    const int reps = 5;
+    for (int it = 0; it < reps; ++it) kern<<<grid, 96, smem>>>(tk, tv, steps, n / BOX, h, bs);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms; cudaEventElapsedTime(&ms, e0, e1);
+    const double bytes = double(reps) * grid * steps * 16384.0;
+    const double s = ms * 1e-3;
+    int clk; cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
+    printf("box %2d stages %d barriers/stage %d ctas/SM %d: %7.1f GB/s  %5.1f B/clk/SM  %6.0f clk per 64-key step per CTA\n",
+           BOX, STAGES, NB, cps, bytes / s / 1e9, bytes / s / (clk * 1e3) / sms, s * clk * 1e3 / (double(reps) * steps));
+    if (cudaGetLastError() != cudaSuccess) { printf("error\n"); exit(1); }
+}
+
+// the same 16-row boxes through a 2-D map (rows = b*n, cols = 3H): per-op cost vs dimensionality
+template <int BOX, int STAGES, int ISSUERS>
+__global__ void __launch_bounds__(96) gather_2d(const __grid_constant__ CUtensorMap t2, int steps, int nblk, int n, int h,
+                                              int bs, int H) {
+    extern __shared__ __align__(1024) unsigned char dsm[];
+    unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(dsm) + 1023) & ~uintptr_t(1023));
+    __shared__ uint64_t full[STAGES], empty[STAGES];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    constexpr int G = 64 / BOX;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) { tc::mbar_init(&full[s], 1); tc::mbar_init(&empty[s], 1); }
+        tc::fence_barrier_init();
+    }
+    __syncthreads();
+    if (warp == 0) {
+        for (int g = 0; g < steps; ++g) {
+            const int st = g % STAGES;
+            const uint32_t ph = ((g / STAGES) & 1) ^ 1;
+            if (lane == 0) {
+                tc::mbar_wait(&empty[st], ph);
+                tc::mbar_expect_tx(&full[st], 2 * 64 * 128);
+            }
+            __syncwarp();
+            const uint32_t hs = hash(blockIdx.x * 7919u + g);
+            const int slice = hs % (h * bs);
+            const int hh = slice % h, b = slice / h;
+            if (lane < ISSUERS) {
+                for (int gg = lane; gg < G; gg += ISSUERS) {
+                    const int cb = hash(hs + gg) % nblk;
+                    unsigned char* k = base + st * 16384 + gg * BOX * 128;
+                    tc::tma_load_2d(k, &t2, &full[st], H + hh * 64, b * n + cb * BOX);
+                    tc::tma_load_2d(k + 8192, &t2, &full[st], 2 * H + hh * 64, b * n + cb * BOX);
+                }
+            }
+        }
+    } else if (warp == 1 && lane == 0) {
+        for (int g = 0; g < steps; ++g) {
+            const int st = g % STAGES;
+            tc::mbar_wait(&full[st], (g / STAGES) & 1);
+            tc::mbar_arrive(&empty[st]);
+        }
+    }
+}
+
 // HEADS heads per box ({64, BOX, HEADS, 1}): one TMA instruction fetches the same key block of
 // HEADS adjacent heads (items of one row block share the load list across heads); a stage holds
 // HEADS x 64 keys of K and of V.
@@ -276,6 +386,43 @@ int main() {
     cudaMalloc(&qkv, size_t(bs) * n * 3 * H * 2);
     cudaMemset(qkv, 0x3c, size_t(bs) * n * 3 * H * 2);
     // (d, n, h, b) strides in elements: row 3H, head 64, batch n*3H
+    if (getenv("NB_ONLY")) {
+        CUtensorMap tk = map4(qkv + H, n, h, bs, 3 * H, 64, long(n) * 3 * H, 16);
+        CUtensorMap tv = map4(qkv + 2 * H, n, h, bs, 3 * H, 64, long(n) * 3 * H, 16);
+        for (int cps : {1, 2}) {
+            run_nb<16, 4, 1>(tk, tv, n, h, bs, sms, cps);
+            run_nb<16, 4, 2>(tk, tv, n, h, bs, sms, cps);
+            run_nb<16, 4, 4>(tk, tv, n, h, bs, sms, cps);
+            run_nb<16, 4, 8>(tk, tv, n, h, bs, sms, cps);
+        }
+        CUtensorMap t2;
+        {
+            const cuuint64_t dims[2] = {(cuuint64_t)3 * H, (cuuint64_t)bs * n};
+            const cuuint64_t strides[1] = {(cuuint64_t)3 * H * 2};
+            const cuuint32_t boxd[2] = {64, 16};
+            const cuuint32_t estr[2] = {1, 1};
+            encode(&t2, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, qkv, dims, strides, boxd, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        }
+        for (int cps : {1, 2}) {
+            auto kern = gather_2d<16, 4, 4>;
+            const int smem = 4 * 16384 + 1024;
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            const int steps = 2000, grid = sms * cps;
+            cudaEvent_t e0, e1;
+            cudaEventCreate(&e0); cudaEventCreate(&e1);
+            for (int it = 0; it < 2; ++it) kern<<<grid, 96, smem>>>(t2, steps, n / 16, n, h, bs, H);
+            cudaEventRecord(e0);
+            for (int it = 0; it < 5; ++it) kern<<<grid, 96, smem>>>(t2, steps, n / 16, n, h, bs, H);
+            cudaEventRecord(e1);
+            cudaEventSynchronize(e1);
+            float ms; cudaEventElapsedTime(&ms, e0, e1);
+            int clk; cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
+            printf("2-D map box 16 stages 4 issuers 4 ctas/SM %d: %6.0f clk per 64-key step per CTA (%s)\n", cps,
+                   ms * 1e-3 * clk * 1e3 / (5.0 * steps), cudaGetErrorString(cudaGetLastError()));
+        }
+        return 0;
+    }
     for (int box : {16, 64}) {
         CUtensorMap tk = map4(qkv + H, n, h, bs, 3 * H, 64, long(n) * 3 * H, box);
         CUtensorMap tv = map4(qkv + 2 * H, n, h, bs, 3 * H, 64, long(n) * 3 * H, box);
