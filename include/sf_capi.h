@@ -266,6 +266,13 @@ sf_status sf_mha_blockwise(const sf_attn_args* args, const sf_bsr_dev* bsr, cons
 /* Row-wise gather executor over a device CSR. Replaces rowwise_sdpa (attention.hpp:177-213). */
 sf_status sf_mha_rowwise(const sf_attn_args* args, const sf_csr_dev* csr, void* stream);
 
+/* Dense masked SDPA reference on the device (dense_sdpa_oracle, attention.hpp:15-56): reads the
+ * DENSE bit mask (sf_mask_generate's layout), accumulates in fp64 with the reference's exact
+ * two-pass softmax, and writes fp64 output (bs, h, n, head_size) contiguous to `o64`. Rows with no
+ * valid position are exactly zero. head_size even and <= 64. An executor independent of the
+ * storage formats, used by `sparsefuse attn verify`; not a hot path. */
+sf_status sf_mha_dense_oracle(const sf_attn_args* args, const uint32_t* d_bits, double* o64, void* stream);
+
 /* Kernel selection for sf_mha_blockwise: 0 = auto, 1 = force generic CUDA-core kernel,
  * 2 = force tcgen05 kernel (fails with SF_PLAN_ERROR if the shape is unsupported). */
 sf_status sf_set_attn_impl(int32_t impl);

@@ -485,4 +485,32 @@ inline Tensor4<double> rowwise_sdpa(const AttentionInput<double>& in, const Roww
     return detail::run_on_device<double, double>(in, [&](const sf_attn_args& a) { rowwise_sdpa(a, rw); });
 }
 
+// dense_sdpa_oracle (attention.hpp:15-56): the dense masked SDPA on the device from the DENSE
+// mask, fp64 accumulation and output. The inputs are rounded to fp16 on the way to the device,
+// exactly as the sparse executors' inputs are, so the three legs of `attn verify` see the same
+// values.
+inline Tensor4<double> dense_sdpa_oracle(const AttentionInput<double>& in, const DenseMask& mask) {
+    in.check();
+    if (mask.seq_len() != in.seq_len()) throw shape_error("mask seq_len differs from input");
+    const std::size_t cnt = in.q.v.size();
+    std::vector<__half> hq(cnt), hk(cnt), hv(cnt);
+    for (std::size_t i = 0; i < cnt; ++i) {
+        hq[i] = __float2half(static_cast<float>(in.q.v[i]));
+        hk[i] = __float2half(static_cast<float>(in.k.v[i]));
+        hv[i] = __float2half(static_cast<float>(in.v.v[i]));
+    }
+    DeviceBuffer<__half> q, k, v;
+    DeviceBuffer<double> o(cnt);
+    q.upload(hq.data(), cnt); k.upload(hk.data(), cnt); v.upload(hv.data(), cnt);
+    const int n = in.seq_len(), d = in.head_size();
+    sf_attn_args a{in.bs(), in.h(), n, d, SF_F16, q.data(), k.data(), v.data(), nullptr,
+                   static_cast<std::int64_t>(in.h()) * n * d, static_cast<std::int64_t>(n) * d, d,
+                   static_cast<std::int64_t>(in.h()) * n * d, static_cast<std::int64_t>(n) * d, d, 0.f};
+    a.o = o.data();  // not written (the fp64 output goes to o64); check_attn_args wants non-null
+    check(sf_mha_dense_oracle(&a, mask.device_bits(), o.data(), nullptr));
+    Tensor4<double> out(in.bs(), in.h(), n, d);
+    o.download(out.v.data(), cnt);
+    return out;
+}
+
 }  // namespace sparsefuse

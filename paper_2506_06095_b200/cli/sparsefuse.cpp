@@ -7,7 +7,8 @@
 //   sparsefuse plan select <mask flags> --hw NAME --heads H --bs B [--head-size D] [--mode reference|b200]
 //   sparsefuse fuse encode 0-1,1-3,3-4
 //   sparsefuse fuse decode 0110
-//   sparsefuse attn verify <mask flags> [--bs B] [--heads H] [--head-size D] [--seed S]
+//   sparsefuse attn verify <mask flags | --pattern none --seq-len N> [--bs B] [--heads H] [--head-size D]
+//                          [--seed S] [--tol A] [--tol-rel R] [--inject-fault tile]
 //   sparsefuse report show <report.jsonl> [--line K] [--output text|json]
 //   mask flags: --pattern P --seq-len N [--band W] [--global G] [--dilation R] [--fill F]
 //               [--block-rand B] [--seed S]   (or --sfmk file.sfmk)
@@ -165,29 +166,114 @@ int fuse(const Args& a, const std::string& op) {
     return 0;
 }
 
-// block-wise (tcgen05 at the B200 plan's tile) vs row-wise on the same seeded inputs; the loaded
-// tile count against block_stats (the executor visits exactly the valid tiles)
+// attn verify: the dense oracle (dense_sdpa_oracle on the device, fp64, from
+// the DENSE mask) vs the block-wise executor (tcgen05 at the B200 plan's tile, over the BSR) vs
+// the row-wise executor (over the CSR) on the same seeded inputs; max-abs and mean-rel errors of
+// each sparse executor against the oracle, and the loaded-tile count against block_stats.
+// --inject-fault flips one tile of the BSR before the block-wise run (a full tile dropped, a part
+// tile's bits inverted, or, for a mask with no valid tile, tile (0,0) made full): the run must
+// then fail (exit 1) with a diff report.
+namespace {
+struct Diff {
+    double max_abs = 0.0, sum_abs = 0.0, sum_ref = 0.0;
+    int64_t at = -1;
+    double got = 0.0, want = 0.0;
+    double mean_rel() const { return sum_ref > 0.0 ? sum_abs / sum_ref : sum_abs; }
+};
+template <typename T>
+Diff diff(const Tensor4<T>& got, const Tensor4<double>& want) {
+    Diff r;
+    for (size_t i = 0; i < want.v.size(); ++i) {
+        const double e = std::abs(static_cast<double>(got.v[i]) - want.v[i]);
+        r.sum_abs += e;
+        r.sum_ref += std::abs(want.v[i]);
+        if (e > r.max_abs) {
+            r.max_abs = e;
+            r.at = static_cast<int64_t>(i);
+            r.got = static_cast<double>(got.v[i]);
+            r.want = want.v[i];
+        }
+    }
+    return r;
+}
+
+// flip one tile of a host BsrMask (keeps the arrays structurally valid); returns what was done
+std::string flip_one_tile(BsrMask& b) {
+    const size_t tb = static_cast<size_t>(b.block_m) * b.block_n;
+    auto shift = [](std::vector<int32_t>& rp, int from, int by) {
+        for (size_t r = static_cast<size_t>(from); r < rp.size(); ++r) rp[r] += by;
+    };
+    for (int r = 0; r < b.n_rows; ++r) {
+        if (b.full_row_ptr[r + 1] > b.full_row_ptr[r]) {  // drop the row block's first full tile
+            const int c = b.full_col_idx[b.full_row_ptr[r]];
+            b.full_col_idx.erase(b.full_col_idx.begin() + b.full_row_ptr[r]);
+            shift(b.full_row_ptr, r + 1, -1);
+            for (int k = b.load_row_ptr[r]; k < b.load_row_ptr[r + 1]; ++k)
+                if (b.load_col_idx[k] == c) {
+                    b.load_col_idx.erase(b.load_col_idx.begin() + k);
+                    break;
+                }
+            shift(b.load_row_ptr, r + 1, -1);
+            return "full tile (" + std::to_string(r) + ", " + std::to_string(c) + ") dropped";
+        }
+        if (b.part_row_ptr[r + 1] > b.part_row_ptr[r]) {  // invert the bits of its first part tile
+            const int k = b.part_row_ptr[r];
+            std::vector<uint8_t> inv = b.part_mask_pool[b.part_tile_ids[k]];
+            for (auto& x : inv) x = x ? 0 : 1;
+            b.part_mask_pool.push_back(std::move(inv));
+            b.part_tile_ids[k] = static_cast<int32_t>(b.part_mask_pool.size() - 1);
+            (void)tb;
+            return "part tile (" + std::to_string(r) + ", " + std::to_string(b.part_col_idx[k]) + ") bits inverted";
+        }
+    }
+    // no valid tile at all: make tile (0, 0) full
+    b.full_col_idx.insert(b.full_col_idx.begin(), 0);
+    shift(b.full_row_ptr, 1, 1);
+    b.load_col_idx.insert(b.load_col_idx.begin(), 0);
+    shift(b.load_row_ptr, 1, 1);
+    return "empty tile (0, 0) made full";
+}
+}  // namespace
+
 int attn_verify(const Args& a) {
-    const DenseMask m = mask_of(a);
+    const DenseMask m = a.get("pattern") == "none" ? DenseMask(std::atoi(a.get("seq-len", "0").c_str()), false) : mask_of(a);
     const int bs = std::atoi(a.get("bs", "1").c_str()), h = std::atoi(a.get("heads", "2").c_str());
     const int d = std::atoi(a.get("head-size", "64").c_str());
     const auto in = random_attention_input<float>(bs, h, m.seq_len(), d, std::strtoull(a.get("seed", "1").c_str(), nullptr, 10));
+    const AttentionInput<double> ind{in.q.cast<double>(), in.k.cast<double>(), in.v.cast<double>()};
     const KernelPlan p = select_plan(m, hw_preset("b200"), m.seq_len(), h, bs, d, PlanMode::B200);
     const int bm = p.kind == KernelKind::BlockWise ? p.block_m : 128, bn = p.kind == KernelKind::BlockWise ? p.block_n : 16;
-    const BsrMask bsr = build_bsr(m, bm, bn);
-    BlockExecStats st;
-    const Tensor4<float> bw = block_sparse_sdpa(in, bsr, &st);
-    const AttentionInput<double> ind{in.q.cast<double>(), in.k.cast<double>(), in.v.cast<double>()};
-    const Tensor4<double> rw = rowwise_sdpa(ind, build_rowwise(m));
-    double mx = 0.0;
-    for (size_t i = 0; i < bw.v.size(); ++i) mx = std::max(mx, std::abs(static_cast<double>(bw.v[i]) - rw.v[i]));
+    BsrMask bsr = build_bsr(m, bm, bn);
     const BlockStats bs_ = block_stats(bsr);
+    std::string fault;
+    if (a.has("inject-fault")) {
+        fault = flip_one_tile(bsr);
+        bsr.device = upload_bsr(bsr);
+    }
+    const Tensor4<double> want = dense_sdpa_oracle(ind, m);
+    BlockExecStats st;
+    const Diff dbw = diff(block_sparse_sdpa(in, bsr, &st), want);
+    const Diff drw = diff(rowwise_sdpa(ind, build_rowwise(m)), want);
     const bool tiles_ok = st.tiles_loaded == bs_.full_count + bs_.part_count;
-    const double tol = std::atof(a.get("tol", "2e-2").c_str());
-    const bool pass = mx <= tol && tiles_ok;
-    std::cout << "{\"pass\": " << (pass ? "true" : "false") << ", \"max_abs_blockwise_vs_rowwise\": " << num(mx)
-              << ", \"tolerance\": " << num(tol) << ", \"block\": [" << bm << ", " << bn << "], \"tiles_loaded\": "
-              << st.tiles_loaded << ", \"valid_tiles\": " << bs_.full_count + bs_.part_count << "}" << std::endl;
+    const double tol = std::atof(a.get("tol", "2e-2").c_str()), tol_rel = std::atof(a.get("tol-rel", "1e-3").c_str());
+    const bool bw_ok = dbw.max_abs <= tol && dbw.mean_rel() <= tol_rel, rw_ok = drw.max_abs <= tol && drw.mean_rel() <= tol_rel;
+    const bool pass = bw_ok && rw_ok && tiles_ok;
+    std::cout << "{\"pass\": " << (pass ? "true" : "false") << ", \"oracle\": \"dense_sdpa_oracle (device, fp64)\""
+              << ", \"max_abs_blockwise\": " << num(dbw.max_abs) << ", \"mean_rel_blockwise\": " << num(dbw.mean_rel())
+              << ", \"max_abs_rowwise\": " << num(drw.max_abs) << ", \"mean_rel_rowwise\": " << num(drw.mean_rel())
+              << ", \"tolerance\": {\"max_abs\": " << num(tol) << ", \"mean_rel\": " << num(tol_rel) << "}"
+              << ", \"block\": [" << bm << ", " << bn << "], \"tiles_loaded\": " << st.tiles_loaded
+              << ", \"valid_tiles\": " << bs_.full_count + bs_.part_count << ", \"fault_injected\": "
+              << (fault.empty() ? "null" : "\"" + fault + "\"");
+    if (!pass) {  // diff report: the worst element of the failing executor
+        const bool bw_bad = !bw_ok || !tiles_ok;
+        const Diff& w = bw_bad ? dbw : drw;
+        const int64_t n = m.seq_len(), i = w.at < 0 ? 0 : w.at;
+        std::cout << ", \"diff\": {\"executor\": \"" << (bw_bad ? "block_wise" : "row_wise") << "\", \"b\": " << i / (int64_t(h) * n * d)
+                  << ", \"h\": " << (i / (n * d)) % h << ", \"row\": " << (i / d) % n << ", \"col\": " << i % d
+                  << ", \"got\": " << num(w.got) << ", \"want\": " << num(w.want) << "}";
+    }
+    std::cout << "}" << std::endl;
     return pass ? 0 : 1;
 }
 

@@ -63,6 +63,9 @@ def init_weights(model: str, s: LayerShape, dtype=torch.float16, device="cuda", 
     if not compat:
         W["wqkv"] = w(3 * H, H)
         W["bqkv"] = u(3 * H, -0.5, 0.5)
+    if model == "t5-decoder-layer":  # the cross-attention block (DecoderLayer)
+        W.update({"wqc": w(H, H), "bqc": u(H, -0.5, 0.5), "wkvc": w(2 * H, H), "bkvc": u(2 * H, -0.5, 0.5),
+                  "woc": w(H, H), "boc": u(H, -0.5, 0.5), "ln3_g": u(H, 0.5, 1.5), "ln3_b": u(H, -0.5, 0.5)})
     return W
 
 
@@ -190,3 +193,72 @@ class EncoderLayer:
     def replay(self, timed: bool = False):
         (self.graph_timed if timed else self.graph).replay()
         return self.out
+
+
+class DecoderLayer(EncoderLayer):
+    """T5-style decoder layer (pre-norm, ReLU): masked self-attention, encoder-decoder
+    cross-attention, feed-forward. The reference's t5-layer preset is the encoder block only
+    (fusion.hpp:379-392; the reference has no cross-attention); this adds the cross-attention
+    block between the self-attention and FFN blocks, built from the same templates:
+
+      h   = LN1(X)                                  [mi_chain]
+      qkv = h Wqkv + b                              [tcgen05]
+      A   = MHA(q, k, v; self mask, e.g. causal)    [attention]
+      X1  = A Wo + bo + X ;  h2 = LN2(X1)           [tcgen05, 2 outputs]
+      qc  = h2 Wqc + bqc                            [tcgen05]
+      kvc = E Wkvc + bkvc                           [tcgen05]   E: the encoder output
+      C   = MHA(qc, kc, vc; cross mask)             [attention]
+      X2  = C Woc + boc + X1 ;  h3 = LN3(X2)        [tcgen05, 2 outputs]
+      F   = relu(h3 W1 + b1)                        [tcgen05]
+      Y   = F W2 + b2 + X2                          [tcgen05]
+
+    Decoder and encoder sequences have the same length (the reference's masks are square); the
+    cross mask is any DenseMask of that length (all-ones for dense cross-attention)."""
+
+    def __init__(self, shape: LayerShape, weights: Dict[str, torch.Tensor], self_ctx: sf.MhaContext,
+                 cross_ctx: sf.MhaContext, dtype=torch.float16, ln_split: bool = False):
+        super().__init__("t5-layer", shape, weights, self_ctx, dtype=dtype, ln_split=ln_split)
+        if cross_ctx.mask.seq_len != shape.seq_len:
+            raise sf._lib.ShapeError("MHA mask seq_len mismatch")  # backend.hpp:333
+        self.model = "t5-decoder-layer"
+        self.cross_ctx = cross_ctx
+        M, H = shape.rows, shape.hidden
+        dev = weights["wo"].device
+        e = lambda *sz: torch.empty(*sz, dtype=dtype, device=dev)
+        # cross q | k | v in one (M, 3H) buffer (the two projections write column slices), so the
+        # three attention views share strides as the executor's argument block requires
+        self.qkvc, self.cattn, self.x2, self.h3 = e(M, 3 * H), e(M, H), e(M, H), e(M, H)
+        self.enc = None
+
+    def forward(self, x: torch.Tensor, enc: Optional[torch.Tensor] = None, stream=None, mark=None) -> torch.Tensor:
+        W = self.W
+        mark = mark or (lambda name: None)
+        enc = enc if enc is not None else self.enc
+        if enc is None or enc.shape != x.shape:
+            raise sf._lib.ShapeError("decoder layer needs the encoder output (bs*seq x hidden)")
+        H = self.s.hidden
+        fused.mi_chain(x, self.h, ln_gamma=W["ln1_g"], ln_beta=W["ln1_b"], stream=stream)
+        mark("ln1_mi_chain")
+        self._mha(self.h, stream, mark)
+        self._gemm_ln(self.attn, "wo", "bo", x, "ln2", self.h2, self.x1, "out_proj", stream, mark)
+        # cross-attention: queries from the decoder stream, keys / values from the encoder output
+        fused.gemm_fused(self.h2, W["wqc"], self.qkvc[:, :H], bias=W["bqc"], stream=stream)
+        mark("cross_q_gemm")
+        fused.gemm_fused(enc, W["wkvc"], self.qkvc[:, H:], bias=W["bkvc"], stream=stream)
+        mark("cross_kv_gemm")
+        sf.mha(self._heads(self.qkvc, 0), self._heads(self.qkvc, H), self._heads(self.qkvc, 2 * H), self.cross_ctx,
+               out=self._heads(self.cattn, 0), stream=stream)
+        mark("cross_mha")
+        self._gemm_ln(self.cattn, "woc", "boc", self.x1, "ln3", self.h3, self.x2, "cross_out", stream, mark)
+        fused.gemm_fused(self.h3, W["w1"], self.f, bias=W["b1"], act="relu", stream=stream)
+        mark("ffn1_gemm_act")
+        fused.gemm_fused(self.f, W["w2"], self.out, bias=W["b2"], aux=self.x2, stream=stream)
+        mark("ffn2_gemm")
+        return self.out
+
+    def kernels_per_step(self) -> int:
+        return 10 + (2 if self.ln_split else 0)
+
+    def capture(self, x: torch.Tensor, enc: Optional[torch.Tensor] = None, timed: bool = False) -> None:
+        self.enc = enc if enc is not None else self.enc
+        super().capture(x, timed)

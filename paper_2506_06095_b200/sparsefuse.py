@@ -450,6 +450,16 @@ def rowwise_sdpa(q, k, v, rw: RowwiseMask, out=None, stream=None):
     return o
 
 
+def dense_sdpa_oracle(q, k, v, mask: "DenseMask", stream=None) -> torch.Tensor:
+    """attention.hpp:15-56 on the device: dense masked SDPA from the DENSE mask, fp64 accumulation
+    and output (bs, h, n, d). Independent of the storage formats; `attn verify` checks the sparse
+    executors against it."""
+    o64 = torch.empty(q.shape, dtype=torch.float64, device=q.device)
+    a = attn_args(q, k, v, q)  # o (unused) must be non-null
+    check(lib().sf_mha_dense_oracle(C.byref(a), mask.bits.data_ptr(), o64.data_ptr(), _stream(stream)))
+    return o64
+
+
 class MhaContext:
     """Formats + plan for one session mask (backend.hpp:309-321 MhaContext), built on device."""
 

@@ -45,8 +45,32 @@ def test_mask_and_plan_commands(oracle, tmp_path):
 @pytest.mark.parametrize("pattern", [["--pattern", "sliding", "--band", 24], ["--pattern", "bigbird", "--band", 16,
                                                                                "--global", 16, "--fill", 0.1]])
 def test_attn_verify_passes(pattern):
+    """oracle vs block-wise vs row-wise on seeded inputs, errors and tile counts."""
     rc, j = run("attn", "verify", *pattern, "--seq-len", 512, "--bs", 1, "--heads", 2)
     assert rc == 0 and j["pass"] and j["tiles_loaded"] == j["valid_tiles"]
+    assert j["oracle"].startswith("dense_sdpa_oracle") and j["fault_injected"] is None
+    assert 0 < j["max_abs_blockwise"] <= 2e-2 and 0 < j["max_abs_rowwise"] <= 2e-2
+    assert j["mean_rel_blockwise"] <= 1e-3 and j["mean_rel_rowwise"] <= 1e-3
+
+
+@pytest.mark.gpu
+def test_attn_verify_all_false_mask_is_zero_and_passes():
+    """an all-false mask gives all-zero outputs (every executor and the oracle)."""
+    rc, j = run("attn", "verify", "--pattern", "none", "--seq-len", 256, "--bs", 1, "--heads", 2)
+    assert rc == 0 and j["pass"] and j["valid_tiles"] == 0
+    assert j["max_abs_blockwise"] == 0 and j["max_abs_rowwise"] == 0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("pattern", [["--pattern", "sliding", "--band", 24],
+                                     ["--pattern", "bigbird", "--band", 16, "--global", 16, "--fill", 0.1],
+                                     ["--pattern", "none"]])
+def test_attn_verify_injected_fault_fails(pattern):
+    """injected-fault mode (one tile flipped) exits 1 with a diff report."""
+    rc, j = run("attn", "verify", *pattern, "--seq-len", 512, "--bs", 1, "--heads", 2, "--inject-fault", "tile")
+    assert rc == 1 and not j["pass"] and j["fault_injected"]
+    assert j["diff"]["executor"] == "block_wise" and j["max_abs_blockwise"] > 2e-2
+    assert abs(j["diff"]["got"] - j["diff"]["want"]) == pytest.approx(j["max_abs_blockwise"], rel=1e-9, abs=1e-12)
 
 
 def test_report_show_renders_a_tuning_report():

@@ -233,3 +233,23 @@ def test_dynamic_schedule_graph_replay_and_streams(sf, oracle):
     be = sf.build_bsr(sf.DenseMask.from_numpy(mask_e), 128, 16)
     for _ in range(3):
         parity(sf.block_sparse_sdpa(qd, kd, vd, be), ref_e)
+
+
+@pytest.mark.parametrize("terms,n", [([dict(pattern="bigbird", seq_len=512, global_width=22, band_width=22,
+                                            filling_rate=0.1, seed=3)], 512),
+                                     ([dict(pattern="strided", seq_len=384, band_width=19)], 384),
+                                     ([dict(pattern="random", seq_len=256, block=16, filling_rate=0.05, seed=2)], 256)])
+def test_device_dense_oracle_matches_reference(sf, oracle, terms, n):
+    """sf_mha_dense_oracle (attention.hpp:15-56 on the device, fp64) equals the reference's
+    dense_sdpa_oracle restated in oracle/ on the same fp16-rounded inputs to fp64 rounding, and
+    keeps fully masked rows exactly zero."""
+    import torch
+    m = oracle.mask(terms)
+    q, k, v = fp16_inputs(oracle, 2, 3, n, 64, 11)
+    ref = oracle.dense_sdpa(q, k, v, m)
+    dm = sf.generate_mask(terms)
+    got = sf.dense_sdpa_oracle(to_dev(q, torch.float16), to_dev(k, torch.float16), to_dev(v, torch.float16), dm)
+    got = got.cpu().numpy()
+    assert np.abs(got - ref).max() <= 1e-9
+    empty = ~m.any(axis=1)
+    assert np.all(got[:, :, empty, :] == 0.0)

@@ -97,3 +97,64 @@ def test_layer_cuda_graph_replay(sf, oracle):
     out = L.replay()
     torch.cuda.synchronize()
     parity(out, ref)
+
+
+@pytest.mark.parametrize("cross", ["dense", "bigbird"])
+def test_t5_decoder_layer_cross_attention(sf, oracle, cross):
+    """T5 decoder layer (F3): causal self-attention, encoder-decoder cross-attention (dense or a
+    sparse cross mask), ReLU FFN, three pre-norm LayerNorms; vs the same chain composed from the
+    pinned per-op oracle functions in fp32 on the fp16-rounded weights and inputs."""
+    import torch
+    from paper_2506_06095_b200 import layer
+    bs, seq, hid, heads = 2, 256, 256, 4
+    hs, ff = hid // heads, 4 * hid
+    o = oracle
+    rng = np.random.default_rng(7)
+    a = lambda k: 1 / np.sqrt(k)
+    mat = lambda k, n: r16(rng.uniform(-a(k), a(k), (k, n)).astype(np.float32))  # reference layout inner x cols
+    vec = lambda n, lo, hi: rng.uniform(lo, hi, n).astype(np.float32)
+    P = {"wqkv": mat(hid, 3 * hid), "bqkv": vec(3 * hid, -.5, .5), "wo": mat(hid, hid), "bo": vec(hid, -.5, .5),
+         "wqc": mat(hid, hid), "bqc": vec(hid, -.5, .5), "wkvc": mat(hid, 2 * hid), "bkvc": vec(2 * hid, -.5, .5),
+         "woc": mat(hid, hid), "boc": vec(hid, -.5, .5), "w1": mat(hid, ff), "b1": vec(ff, -.5, .5),
+         "w2": mat(ff, hid), "b2": vec(hid, -.5, .5)}
+    for i in (1, 2, 3):
+        P[f"ln{i}_g"], P[f"ln{i}_b"] = vec(hid, .5, 1.5), vec(hid, -.5, .5)
+    x = r16(rng.uniform(-1, 1, (bs * seq, hid)).astype(np.float32))
+    enc = r16(rng.uniform(-1, 1, (bs * seq, hid)).astype(np.float32))
+    self_terms = [dict(pattern="causal", seq_len=seq)]
+    cross_terms = ([dict(pattern="sliding", seq_len=seq, band_width=seq)] if cross == "dense" else
+                   [dict(pattern="bigbird", seq_len=seq, global_width=16, band_width=16, filling_rate=0.1, seed=4)])
+
+    # oracle composition (fp32)
+    def split(t, c0):
+        return np.ascontiguousarray(t[:, c0:c0 + hid].reshape(bs, seq, heads, hs).transpose(0, 2, 1, 3))
+
+    def attn(q, k, v, terms):
+        out, _ = o.block_sparse_sdpa(q, k, v, o.mask(terms), 16, 16, 8)
+        return out.transpose(0, 2, 1, 3).reshape(bs * seq, hid)
+
+    h = o.layernorm(x, P["ln1_g"], P["ln1_b"])
+    qkv = o.bias(o.gemm(h, P["wqkv"], 8), P["bqkv"])
+    x1 = o.add(o.bias(o.gemm(attn(split(qkv, 0), split(qkv, hid), split(qkv, 2 * hid), self_terms), P["wo"], 8),
+                      P["bo"]), x)
+    h2 = o.layernorm(x1, P["ln2_g"], P["ln2_b"])
+    qc = o.bias(o.gemm(h2, P["wqc"], 8), P["bqc"])
+    kvc = o.bias(o.gemm(enc, P["wkvc"], 8), P["bkvc"])
+    x2 = o.add(o.bias(o.gemm(attn(split(qc, 0), split(kvc, 0), split(kvc, hid), cross_terms), P["woc"], 8), P["boc"]),
+               x1)
+    h3 = o.layernorm(x2, P["ln3_g"], P["ln3_b"])
+    ref = o.add(o.bias(o.gemm(o.relu(o.bias(o.gemm(h3, P["w1"], 8), P["b1"])), P["w2"], 8), P["b2"]), x2)
+
+    dev = lambda t, dt=torch.float16: torch.from_numpy(np.ascontiguousarray(t)).to("cuda", dt)
+    W = {k: (dev(v.T) if v.ndim == 2 else dev(v, torch.float32)) for k, v in P.items()}
+    ctx = lambda terms: sf.MhaContext(sf.generate_mask(terms), sf.select_plan(
+        sf.generate_mask(terms), sf.hw_preset("b200"), seq, heads, bs, hs, mode="b200"))
+    L = layer.DecoderLayer(layer.LayerShape(bs, seq, hid, heads, hs), W, ctx(self_terms), ctx(cross_terms))
+    xd, ed = dev(x), dev(enc)
+    parity(L.forward(xd, ed), ref)
+    # the same step replayed as one CUDA graph
+    L.capture(xd, ed)
+    L.out.zero_()
+    out = L.replay()
+    torch.cuda.synchronize()
+    parity(out, ref)
