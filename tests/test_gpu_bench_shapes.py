@@ -79,9 +79,10 @@ def _plan(sf, terms, bs, h):
     return dm, plan
 
 
-@pytest.mark.parametrize("schedule", ["dynamic", "static"])
+@pytest.mark.parametrize("schedule", ["dynamic", "static", "headgroup"])
 @pytest.mark.parametrize("name", list(ATTN_CASES))
 def test_mha_at_bench_plan(sf, attn_ref, monkeypatch, name, schedule):
+    """schedule "headgroup": the opt-in three-heads-per-item kernel (attn_tc3.cu), dynamic schedule."""
     import torch
     terms, bs, h = ATTN_CASES[name]
     _, q, k, v, ref = attn_ref(name, "f16")
@@ -90,6 +91,8 @@ def test_mha_at_bench_plan(sf, attn_ref, monkeypatch, name, schedule):
     b = sf.build_bsr(dm, plan.block_m, plan.block_n)
     if schedule == "static":
         monkeypatch.setenv("SF_ATTN_STATIC", "1")
+    if schedule == "headgroup":
+        monkeypatch.setenv("SF_ATTN_HEADGROUP", "1")
     sf.set_attn_impl("tcgen05")  # fail loudly if the plan is not the tcgen05 kernel's
     try:
         Q, K, V = (torch.from_numpy(x).to("cuda", torch.float16) for x in (q, k, v))
