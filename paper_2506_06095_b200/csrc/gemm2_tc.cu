@@ -547,7 +547,11 @@ bool gemm_pair_supported(const sf_gemm_args& a, bool ln) {
     return true;
 }
 
+bool gemm_ln_panel_supported(const sf_gemm_args& a);          // gemm2_ln.cu
+sf_status gemm_ln_panel(const sf_gemm_args& a, cudaStream_t st);
+
 sf_status gemm_pair_dispatch(const sf_gemm_args& a, bool ln, cudaStream_t st) {
+    if (ln && gemm_ln_panel_supported(a)) return gemm_ln_panel(a, st);  // one pair per 256-row panel
     if (!gemm_pair_supported(a, ln))
         return fail(SF_SHAPE_ERROR, ln ? "CTA-pair LayerNorm GEMM needs M > 128, N % 256 == 0 and N <= 1024"
                                        : "CTA-pair GEMM needs M > 128");
