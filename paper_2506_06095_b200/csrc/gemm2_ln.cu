@@ -292,10 +292,9 @@ __global__ void __launch_bounds__(kThreadsP, 1) gemm2_ln_kernel(const __grid_con
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
                     const float4 bb = b4[j];
-                    x[4 * j] += bb.x;
-                    x[4 * j + 1] += bb.y;
-                    x[4 * j + 2] += bb.z;
-                    x[4 * j + 3] += bb.w;
+                    const float2 lo = tc::fadd2(make_float2(x[4 * j], x[4 * j + 1]), make_float2(bb.x, bb.y));
+                    const float2 hi = tc::fadd2(make_float2(x[4 * j + 2], x[4 * j + 3]), make_float2(bb.z, bb.w));
+                    x[4 * j] = lo.x; x[4 * j + 1] = lo.y; x[4 * j + 2] = hi.x; x[4 * j + 3] = hi.y;
                 }
                 if (p.act) {
 #pragma unroll
@@ -319,18 +318,19 @@ __global__ void __launch_bounds__(kThreadsP, 1) gemm2_ln_kernel(const __grid_con
                     const int k2 = k + 2;  // chunk k + 2 of the warp's walk into the box just read
                     if (k2 < 4 * nsub) res_issue(b_, (k2 >> 2) * BNP + grp * 128 + (k2 & 3) * 32, row0);
                 }
-                float s4[4] = {0.f, 0.f, 0.f, 0.f};
+                float2 s2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
-                for (int j = 0; j < 32; ++j) s4[j & 3] += x[j];
-                const float mc = ((s4[0] + s4[1]) + (s4[2] + s4[3])) * (1.f / 32.f);
-                float q4[4] = {0.f, 0.f, 0.f, 0.f};
+                for (int j = 0; j < 32; j += 2) s2[(j >> 1) & 1] = tc::fadd2(s2[(j >> 1) & 1], make_float2(x[j], x[j + 1]));
+                const float mc = ((s2[0].x + s2[0].y) + (s2[1].x + s2[1].y)) * (1.f / 32.f);
+                float2 q2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+                const float2 nmc = make_float2(-mc, -mc);
 #pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    const float dd = x[j] - mc;
-                    q4[j & 3] = fmaf(dd, dd, q4[j & 3]);
+                for (int j = 0; j < 32; j += 2) {
+                    const float2 dd = tc::fadd2(make_float2(x[j], x[j + 1]), nmc);
+                    q2[(j >> 1) & 1] = tc::ffma2(dd, dd, q2[(j >> 1) & 1]);
                 }
                 {  // Chan: merge (32, mc, m2c) into the running statistics
-                    const float m2c = (q4[0] + q4[1]) + (q4[2] + q4[3]);
+                    const float m2c = (q2[0].x + q2[0].y) + (q2[1].x + q2[1].y);
                     const float n_new = run_n + 32.f;
                     const float dd = mc - run_mean;
                     run_mean += dd * (32.f / n_new);
@@ -389,16 +389,19 @@ __global__ void __launch_bounds__(kThreadsP, 1) gemm2_ln_kernel(const __grid_con
                     }
                 }
                 if (k + 1 < 4 * nsub) norm_load(k + 1);
+                // y = ((x - mean) inv) g + e as two packed FMAs per pair
                 float y[32];
                 const float4* g4 = reinterpret_cast<const float4*>(sprm + p.N + col);
                 const float4* e4 = reinterpret_cast<const float4*>(sprm + 2 * p.N + col);
+                const float2 inv2 = make_float2(inv, inv), nmi2 = make_float2(-mean * inv, -mean * inv);
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
                     const float4 g = g4[j], e = e4[j];
-                    y[4 * j] = (x[4 * j] - mean) * inv * g.x + e.x;
-                    y[4 * j + 1] = (x[4 * j + 1] - mean) * inv * g.y + e.y;
-                    y[4 * j + 2] = (x[4 * j + 2] - mean) * inv * g.z + e.z;
-                    y[4 * j + 3] = (x[4 * j + 3] - mean) * inv * g.w + e.w;
+                    const float2 t0 = tc::ffma2(make_float2(x[4 * j], x[4 * j + 1]), inv2, nmi2);
+                    const float2 t1 = tc::ffma2(make_float2(x[4 * j + 2], x[4 * j + 3]), inv2, nmi2);
+                    const float2 y0 = tc::ffma2(t0, make_float2(g.x, g.y), make_float2(e.x, e.y));
+                    const float2 y1 = tc::ffma2(t1, make_float2(g.z, g.w), make_float2(e.z, e.w));
+                    y[4 * j] = y0.x; y[4 * j + 1] = y0.y; y[4 * j + 2] = y1.x; y[4 * j + 3] = y1.y;
                 }
                 if (p.out_pre_ln) {  // two outputs: straight from registers
                     if (row_ok) {
