@@ -397,22 +397,27 @@ def run_band_sweep(args):
             ts.append(a.elapsed_time(b) * 1e3)
         return statistics.median(ts)
 
-    for pat in ("sliding", "causal_local"):
-        for w in (1, 2, 4, 8, 16, 24, 32, 48, 64):
-            dm = sf.generate_mask([dict(pattern=pat, seq_len=n, band_width=w)])
-            ref_plan = sf.select_plan(dm, sf.hw_preset("b200"), n, h, bs, d, mode="reference")
-            b200_plan = sf.select_plan(dm, sf.hw_preset("b200"), n, h, bs, d, mode="b200")
-            bsr = sf.build_bsr(dm, 128, 16)
-            rw = sf.build_rowwise(dm)
-            t_bw = timed(lambda s_: sf.block_sparse_sdpa(q, k, v, bsr, out=o, stream=s_))
-            t_rw = timed(lambda s_: sf.rowwise_sdpa(q, k, v, rw, out=o, stream=s_))
-            best = min(t_bw, t_rw)
-            chosen = lambda pl: t_bw if pl.kind == "block_wise" else t_rw
-            print(json.dumps({"band_sweep": pat, "seq_len": n, "band": w, "bs": bs, "heads": h, "nnz": dm.true_count(),
-                              "eq1_threshold": ref_plan.threshold, "reference_plan": ref_plan.kind,
-                              "b200_plan": b200_plan.kind, "blockwise_us": t_bw, "rowwise_us": t_rw,
-                              "regret_reference_mode": chosen(ref_plan) / best,
-                              "regret_b200_mode": chosen(b200_plan) / best}), flush=True)
+    # bands (Eq. 1's row-wise region), then unstructured cells (random blocks of 1 x 1 at density p:
+    # every (128,16) tile loaded, nearly empty — the masks the row-wise executor is for)
+    cases = [(pat, w, [dict(pattern=pat, seq_len=n, band_width=w)]) for pat in ("sliding", "causal_local")
+             for w in (1, 2, 4, 8, 16, 24, 32, 48, 64)]
+    cases += [("random_cells", p, [dict(pattern="random", seq_len=n, block=1, filling_rate=p, seed=7)])
+              for p in (0.002, 0.005, 0.01, 0.02, 0.05)]
+    for pat, w, terms in cases:
+        dm = sf.generate_mask(terms)
+        ref_plan = sf.select_plan(dm, sf.hw_preset("b200"), n, h, bs, d, mode="reference")
+        b200_plan = sf.select_plan(dm, sf.hw_preset("b200"), n, h, bs, d, mode="b200")
+        bsr = sf.build_bsr(dm, 128, 16)
+        rw = sf.build_rowwise(dm)
+        t_bw = timed(lambda s_: sf.block_sparse_sdpa(q, k, v, bsr, out=o, stream=s_))
+        t_rw = timed(lambda s_: sf.rowwise_sdpa(q, k, v, rw, out=o, stream=s_))
+        best = min(t_bw, t_rw)
+        chosen = lambda pl: t_bw if pl.kind == "block_wise" else t_rw
+        print(json.dumps({"band_sweep": pat, "seq_len": n, ("density" if pat == "random_cells" else "band"): w, "bs": bs, "heads": h, "nnz": dm.true_count(),
+                          "eq1_threshold": ref_plan.threshold, "reference_plan": ref_plan.kind,
+                          "b200_plan": b200_plan.kind, "blockwise_us": t_bw, "rowwise_us": t_rw,
+                          "regret_reference_mode": chosen(ref_plan) / best,
+                          "regret_b200_mode": chosen(b200_plan) / best}), flush=True)
 
 
 # ----------------------------------------------------------------------------------------------

@@ -214,9 +214,9 @@ typedef struct sf_plan {
 typedef enum sf_plan_mode {
     SF_PLAN_REFERENCE = 0,  /* reference grid {16,32,64,128}^2 x {1,2,4,8}, planner.hpp:115-161 */
     SF_PLAN_B200 = 1        /* same Eq. 1/2, grid restricted to tiles the tcgen05 kernel runs;
-                               a row-wise Eq. 1 verdict is overridden to block-wise (128, 16) when
-                               the B200-calibrated executor model predicts block-wise < 1/2 the
-                               row-wise time (sf_select_plan only: it needs the mask) */
+                               then (sf_select_plan only: it needs the mask, head_size 64) both
+                               executors are priced by the B200-calibrated cost model and the
+                               faster one is kept, overriding Eq. 1 in either direction */
 } sf_plan_mode;
 
 /* hw_preset (planner.hpp:36-40) plus "b200". */

@@ -201,13 +201,16 @@ extern "C" sf_status sf_select_plan(const uint32_t* d_bits, const sf_hw_spec* hw
     int64_t loads = 0;
     if (seq_len > 16) SF_TRY(loads16_of(d_bits, static_cast<int32_t>(seq_len), &loads, stream));
     SF_TRY(sf_select_plan_from_loads(loads, hw, seq_len, h, bs, head_size, mode, out));
-    if (mode == SF_PLAN_B200 && out->kind == SF_ROW_WISE && seq_len > 16 && head_size == 64) {
-        // B200 calibration of the Eq. 1 decision: Eq. 1 assumes a row-wise
-        // executor that is competitive per valid cell. On B200 the tcgen05 block executor runs
-        // ~30x more cells per second than the CUDA-core row-wise gather, so a row-wise plan is
-        // kept only while the fitted cost model above predicts it faster.
+    if (mode == SF_PLAN_B200 && seq_len > 16 && head_size == 64) {
+        // B200 calibration of the Eq. 1 decision: both executors are priced with the
+        // fitted cost model above and the faster one is kept, whichever way Eq. 1 routed. Eq. 1
+        // assumes a row-wise executor that is competitive per valid cell; on B200 the tcgen05
+        // block executor runs ~30x more cells per second than the CUDA-core row-wise gather, so
+        // most of Eq. 1's row-wise verdicts (narrow bands) flip to block-wise, while unstructured
+        // low-density masks (every (128,16) tile loaded, nearly empty) flip the other way.
+        const int bn = out->kind == SF_BLOCK_WISE ? out->block_n : 16;
         sf_bsr_dev b{};
-        SF_TRY(sf_bsr_build(d_bits, static_cast<int32_t>(seq_len), 128, 16, &b, stream));
+        SF_TRY(sf_bsr_build(d_bits, static_cast<int32_t>(seq_len), 128, bn, &b, stream));
         const int64_t n_load = b.n_load;
         SF_TRY(sf_bsr_free(&b, stream));
         int64_t nnz = 0;
@@ -215,14 +218,19 @@ extern "C" sf_status sf_select_plan(const uint32_t* d_bits, const sf_hw_spec* hw
         const double slices = static_cast<double>(bs) * h;
         const double rows = slices * static_cast<double>(seq_len);
         const double per_row_us = nnz <= 32 * seq_len ? 0.0002 : 0.00065;
-        const double t_bw = kBlockFloorUs + static_cast<double>(n_load) * 128.0 * 16.0 * slices / kBlockCellsPerUs;
+        const double t_bw = kBlockFloorUs + static_cast<double>(n_load) * 128.0 * bn * slices / kBlockCellsPerUs;
         const double t_rw = kRowFloorUs + rows * per_row_us + static_cast<double>(nnz) * slices / kRowNnzPerUs;
-        if (t_bw < t_rw) {
+        if (out->kind == SF_ROW_WISE && t_bw < t_rw) {
             out->kind = SF_BLOCK_WISE;
             out->block_m = 128;
             out->block_n = 16;
             out->num_warps = 8;
             out->score = plan_score(128, 16, 8, *hw, seq_len, h, bs, head_size);
+            out->fallback = 0;
+        } else if (out->kind == SF_BLOCK_WISE && t_rw < t_bw) {
+            out->kind = SF_ROW_WISE;
+            out->block_m = out->block_n = out->num_warps = 0;
+            out->score = 0.0;
             out->fallback = 0;
         }
     }

@@ -194,6 +194,12 @@ def test_b200_selector_calibration(sf):
     assert b200.threshold == ref.threshold
     small = sf.select_plan(sf.gen_sliding_window(2048, 4), sf.hw_preset("b200"), 2048, 2, 1, 64, mode="b200")
     assert small.kind == "row_wise"
+    # the other direction: an unstructured low-density mask loads nearly every (128,16) tile but
+    # leaves it nearly empty; Eq. 1 says block-wise, the B200 model keeps the row-wise gather
+    # (measured 60 vs 178 us at this shape, profiles/r02/band_sweep_v3.jsonl)
+    rnd = sf.gen_random_blocks(2048, 1, 0.002, 7)
+    assert sf.select_plan(rnd, sf.hw_preset("b200"), 2048, 12, 8, 64, mode="reference").kind == "block_wise"
+    assert sf.select_plan(rnd, sf.hw_preset("b200"), 2048, 12, 8, 64, mode="b200").kind == "row_wise"
 
 
 def test_dynamic_schedule_graph_replay_and_streams(sf, oracle):
