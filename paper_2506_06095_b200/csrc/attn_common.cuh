@@ -30,7 +30,7 @@ __device__ __forceinline__ uint32_t pack2<__nv_bfloat16>(float a, float b) {
 // < 5e-5, well under the fp16 spacing of P), and j added straight into the exponent field.
 // x is clamped at -125 so masked (-inf) cells give a tiny positive value that packs to 0.
 #ifndef SF_ATTN_EMU
-#define SF_ATTN_EMU 3
+#define SF_ATTN_EMU 1  // 1 of 8 pairs on the FMA pipe: the softmax is issue-bound (profiles/r02/attn_headgroup.txt)
 #endif
 constexpr int kEmuPairs = SF_ATTN_EMU;  // of the 8 pairs in each 16-column group
 __device__ __forceinline__ float2 ex2_emu2(float2 x) {

@@ -31,11 +31,11 @@ namespace {
 
 // B200 executor cost model, fitted to `bench.py --sweep --both` and `--band-sweep`
 // (profiles/r01/sweep_mha_both_v2.jsonl, band_sweep_v1.jsonl): the persistent tcgen05 block
-// executor has a ~25 us floor and retires ~1.8e12 executed cells/s (cells of the loaded 128x16
+// executor has a ~12 us floor (cfg1: 12.3 us measured, profiles/r01/bench_cfg1_v8.json) and retires ~1.8e12 executed cells/s (cells of the loaded 128x16
 // tiles); the row-wise gather has a ~10 us floor, a per-row cost (0.2 ns with one 8-lane group
 // per row when rows average <= 32 keys, 0.65 ns with a warp per row) and ~6e10 valid cells/s.
 constexpr double kBlockCellsPerUs = 1.8e6;
-constexpr double kBlockFloorUs = 25.0;
+constexpr double kBlockFloorUs = 12.0;
 constexpr double kRowNnzPerUs = 6.0e4;
 constexpr double kRowFloorUs = 10.0;
 

@@ -227,10 +227,12 @@ __global__ void __launch_bounds__(kThreadsP, 1) gemm2_ln_kernel(const __grid_con
                 tc::bulk_commit();
             }
         };
-        // y: this lane's row, 32 columns at `col`; half h of the warp's 64-column staging row. After
-        // the second half the 32 x 64 box goes out as 4-row groups of 128-byte lines.
-        auto coalesced_put = [&](void* base, const float (&yy)[32], int col, int row0_, int h) {
-            if (h == 0) __syncwarp();  // the previous box's reads are done
+        // Stores go through the warp's 4 KB staging box: a lane stages 32 values of its row into
+        // half h of its 128-byte staging row (16-byte piece j of row r at r * 128 + (j ^ (r & 7)) *
+        // 16, conflict-free), then the warp writes the box as 4-row groups, eight lanes per row:
+        // half 0 to (base0, col0), half 1 to (base1, col1) — two column chunks of one output, or
+        // one chunk of the output and of out_pre_ln.
+        auto stage = [&](const float (&yy)[32], int h) {
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 const uint32_t pc = static_cast<uint32_t>(4 * h + j);
@@ -240,9 +242,9 @@ __global__ void __launch_bounds__(kThreadsP, 1) gemm2_ln_kernel(const __grid_con
                              "r"(pack2<T>(yy[8 * j + 6], yy[8 * j + 7]))
                              : "memory");
             }
-            if (h == 0) return;
+        };
+        auto flush = [&](void* base0, int col0, void* base1, int col1, int row0_) {
             __syncwarp();
-            const int c64 = col - 32;  // the box's first column
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
                 const uint32_t rr = 4u * k + (lane >> 3), pc = lane & 7u;
@@ -251,9 +253,11 @@ __global__ void __launch_bounds__(kThreadsP, 1) gemm2_ln_kernel(const __grid_con
                              : "=r"(u.x), "=r"(u.y), "=r"(u.z), "=r"(u.w)
                              : "r"(box + rr * 128u + ((pc ^ (rr & 7u)) << 4)));
                 const int64_t grow = static_cast<int64_t>(row0_) + rr;
-                if (grow < p.M)
-                    *reinterpret_cast<uint4*>(static_cast<T*>(base) + grow * p.ldout + c64 + 8 * pc) = u;
+                void* base = pc < 4 ? base0 : base1;
+                const int c = (pc < 4 ? col0 : col1) + 8 * static_cast<int>(pc & 3u);
+                if (grow < p.M) *reinterpret_cast<uint4*>(static_cast<T*>(base) + grow * p.ldout + c) = u;
             }
+            __syncwarp();  // the box's reads are done before the next staging
         };
         uint32_t i = 0;
         uint32_t bph = 0;  // bit b: phase of residual box b
@@ -262,8 +266,6 @@ __global__ void __launch_bounds__(kThreadsP, 1) gemm2_ln_kernel(const __grid_con
         // chunk of instruction-fetch stalls).
         for (int mp = static_cast<int>(blockIdx.y); mp < mp_tiles; mp += static_cast<int>(gridDim.y), ++i) {
             const int row0 = (2 * mp + static_cast<int>(px)) * BM + static_cast<int>(q) * 32;
-            const int64_t row = static_cast<int64_t>(row0) + lane;
-            const bool row_ok = row < p.M;
             float run_n = 0.f, run_mean = 0.f, run_m2 = 0.f;  // Chan's running (count, mean, M2)
             uint32_t r[32];
             float x[32];
@@ -403,13 +405,13 @@ __global__ void __launch_bounds__(kThreadsP, 1) gemm2_ln_kernel(const __grid_con
                     const float2 y1 = tc::ffma2(t1, make_float2(g.z, g.w), make_float2(e.z, e.w));
                     y[4 * j] = y0.x; y[4 * j + 1] = y0.y; y[4 * j + 2] = y1.x; y[4 * j + 3] = y1.y;
                 }
-                if (p.out_pre_ln) {  // two outputs: straight from registers
-                    if (row_ok) {
-                        store_chunk<T>(p.out, p.ldout, row, col, y);
-                        store_chunk<T>(p.out_pre_ln, p.ldout, row, col, x);
-                    }
-                } else {
-                    coalesced_put(p.out, y, col, row0, cc & 1);
+                if (p.out_pre_ln) {  // the chunk of both outputs per box
+                    stage(y, 0);
+                    stage(x, 1);
+                    flush(p.out, col, p.out_pre_ln, col, row0);
+                } else {             // two chunks of the output per box
+                    stage(y, cc & 1);
+                    if (cc & 1) flush(p.out, col - 32, p.out, col, row0);
                 }
             }
             if (warp == 4 && lane == 0) LTRACE(25);
@@ -489,7 +491,10 @@ bool gemm_ln_panel_supported(const sf_gemm_args& a) {
     // the panel form reads the X panel once per sub-tile: from L2 when K is short (the out-projection,
     // K = 768: 41 vs 43 us cold); at K = 3072 the re-reads come from HBM and the cluster form, whose
     // three pairs read one panel together, is faster (70 vs 84 us; tools/ln_time.py)
-    return a.M > BM && (a.N == 512 || a.N == 768) && a.K <= 1024 && a.epi.ln_gamma && a.epi.ln_beta;
+    // and the pairs run one panel each: a second panel per pair cannot overlap the first one's
+    // normalise pass (T5 cfg4, M = 32768: 87 vs 82 us), so longer M keeps the cluster form
+    return a.M > BM && (a.N == 512 || a.N == 768) && a.K <= 1024 && a.epi.ln_gamma && a.epi.ln_beta &&
+           ceil_div(a.M, 2 * BM) <= max_pairs_ln();
 }
 
 sf_status gemm_ln_panel(const sf_gemm_args& a, cudaStream_t st) {

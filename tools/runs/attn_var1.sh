@@ -1,0 +1,7 @@
+D=paper_2506_06095_b200
+for v in "" e1 e1s; do echo "== ${v:-default}"; if [ -n "$v" ]; then export SF_B200_LIB=$D/_lib_$v/libsf_b200.so; else unset SF_B200_LIB; fi
+timeout 300 python tools/attn_cfg.py cfg2 cfg3 cfg4 dense
+timeout 600 python bench.py --no-cpu-baseline --steps 200 2>/dev/null | python -c "
+import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); k=d['kernels_ms']
+print('bench', round(d['value']/1e6,2), {a: round(b*1e3,1) for a,b in k.items()})"
+done
