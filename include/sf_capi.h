@@ -315,6 +315,28 @@ typedef struct sf_gemm_args {
                                 256 x 256 tiles, tcgen05 cta_group::2) */
 } sf_gemm_args;
 
+/* CiCi template (backend.hpp:270-306), chained on chip: out = post(mid(X . W1^T) . W2^T) with
+ * mid = bias + activation (N1) and post = bias + aux residual + LayerNorm (N2) or any subset.
+ * Each CTA computes a 128 x 128 block of the intermediate with tcgen05, applies mid in registers,
+ * keeps it in shared memory as the next MMA's operand, multiplies it by its slice of W2 and
+ * reduces into an fp32 accumulator (split-K over the intermediate); a row pass applies post. Meant
+ * for the short activations where the reference's search forms CiCi segments (bs*seq <= 4096,
+ * search.hpp:228). SF_BACKEND_ERROR when the shape is outside the kernel (K1 % 64, N1 % 128,
+ * N2 % 64, N2 <= 2048) or mid carries more than bias + activation. Measured slower than two
+ * sf_gemm_fused launches at the BERT FFN shapes (the split-K reduction), so only the
+ * C++ GpuBackend offers it to the search, which times it against the split forms. */
+typedef struct sf_gemm_chain_args {
+    int32_t M, K1, N1, N2;
+    int32_t dtype;                   /* sf_dtype of X, W1, W2, out, aux */
+    const void* x; int64_t ldx;      /* M x K1 */
+    const void* w1; int64_t ldw1;    /* N1 x K1 row-major */
+    const void* w2; int64_t ldw2;    /* N2 x N1 row-major */
+    void* out; int64_t ldout;        /* M x N2 */
+    sf_gemm_epilogue mid;            /* bias (N1) and act only */
+    sf_gemm_epilogue post;           /* bias (N2), aux, LayerNorm, out_pre_ln */
+} sf_gemm_chain_args;
+sf_status sf_gemm_chain(const sf_gemm_chain_args* args, void* stream);
+
 /* Programmatic dependent launch for the hot-path kernels (default on; env SF_PDL=0 disables):
  * each kernel is scheduled while its stream predecessor drains and waits for it on device
  * (griddepcontrol) before touching global data. Not part of the reference API. */

@@ -202,9 +202,14 @@ public:
         }
         if (gemms.size() == 1) {  // CiMi
             gemm(gemms[0], s, group_mi(gemms[0] + 1, seg.end), src, y);
-        } else {  // CiCi: GEMM -> mid MI -> GEMM (intermediate in HBM)
-            gemm(gemms[0], s, group_mi(gemms[0] + 1, gemms[1]), src, mid_.data());
-            gemm(gemms[1], s, group_mi(gemms[1] + 1, seg.end), mid_.data(), y);
+        } else {  // CiCi: GEMM -> mid MI -> GEMM
+            const auto mid = group_mi(gemms[0] + 1, gemms[1]);
+            const auto post = group_mi(gemms[1] + 1, seg.end);
+            // chained on chip (sf_gemm_chain) where the reference forms CiCi segments (bs*seq <= 4096,
+            // search.hpp:228) and the kernel covers the shape; else two CiMi launches through HBM
+            if (rows_ <= 4096 && chain(gemms[0], gemms[1], mid, post, src, y)) return;
+            gemm(gemms[0], s, mid, src, mid_.data());
+            gemm(gemms[1], s, post, mid_.data(), y);
         }
     }
 
@@ -267,6 +272,31 @@ private:
             src = y;
         }
         if (src != y) cuda_check(cudaMemcpyAsync(y, x, static_cast<std::size_t>(rows_ * cols) * 2, cudaMemcpyDeviceToDevice, st_), "copy");
+    }
+
+    // sf_gemm_chain: mid must be one epilogue group of bias / activation, post one group (no
+    // Softmax); returns false (nothing launched) when the kernel does not cover the segment
+    bool chain(int g0, int g1, const std::vector<Group>& mid, const std::vector<Group>& post, const __half* x,
+               __half* y) {
+        if (mid.size() > 1 || post.size() > 1) return false;
+        if (!mid.empty() && (mid[0].e.aux || mid[0].e.ln_gamma || mid[0].e.softmax)) return false;
+        if (!post.empty() && post[0].e.softmax) return false;
+        const OpNode& n0 = g_.nodes[static_cast<std::size_t>(g0)];
+        const OpNode& n1 = g_.nodes[static_cast<std::size_t>(g1)];
+        sf_gemm_chain_args a{};
+        a.M = static_cast<int32_t>(rows_); a.K1 = static_cast<int32_t>(n0.inner);
+        a.N1 = static_cast<int32_t>(n0.cols); a.N2 = static_cast<int32_t>(n1.cols);
+        a.dtype = SF_F16;
+        a.x = x; a.ldx = n0.inner;
+        a.w1 = nodes_[static_cast<std::size_t>(g0)].w_nk.data(); a.ldw1 = n0.inner;
+        a.w2 = nodes_[static_cast<std::size_t>(g1)].w_nk.data(); a.ldw2 = n1.inner;
+        a.out = y; a.ldout = n1.cols;
+        if (!mid.empty()) a.mid = mid[0].e;
+        if (!post.empty()) a.post = post[0].e;
+        const sf_status st = sf_gemm_chain(&a, st_);
+        if (st == SF_BACKEND_ERROR) return false;
+        check(st);
+        return true;
     }
 
     void gemm(int node, const Setting& s, const std::vector<Group>& post, const __half* x, __half* y) {

@@ -92,6 +92,13 @@ class GemmArgs(C.Structure):
                 ("out", C.c_void_p), ("ldout", C.c_int64), ("epi", GemmEpilogue), ("tile_n", C.c_int32)]
 
 
+class GemmChainArgs(C.Structure):
+    _fields_ = [("M", C.c_int32), ("K1", C.c_int32), ("N1", C.c_int32), ("N2", C.c_int32), ("dtype", C.c_int32),
+                ("x", C.c_void_p), ("ldx", C.c_int64), ("w1", C.c_void_p), ("ldw1", C.c_int64),
+                ("w2", C.c_void_p), ("ldw2", C.c_int64), ("out", C.c_void_p), ("ldout", C.c_int64),
+                ("mid", GemmEpilogue), ("post", GemmEpilogue)]
+
+
 LAUNCH_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p)
 
 # Every symbol include/sf_capi.h declares, with its ctypes signature.
@@ -131,6 +138,7 @@ SIGNATURES = {
     "sf_set_pdl": (C.c_int, [_I32]),
     "sf_get_attn_impl": (_I32, []),
     "sf_gemm_fused": (C.c_int, [C.POINTER(GemmArgs), _P]),
+    "sf_gemm_chain": (C.c_int, [C.POINTER(GemmChainArgs), _P]),
     "sf_mi_chain": (C.c_int, [_I32, _I32, _I32, _P, _I64, C.POINTER(GemmEpilogue), _P, _I64, _P]),
     "sf_time_best": (C.c_int, [LAUNCH_FN, _P, _I32, _I32, C.POINTER(C.c_float), _P]),
     "sf_launch_count": (_I64, []),

@@ -12,7 +12,7 @@ from typing import Optional
 import torch
 
 from . import _lib
-from ._lib import GemmArgs, GemmEpilogue, SF_ACT, check, lib
+from ._lib import GemmArgs, GemmChainArgs, GemmEpilogue, SF_ACT, check, lib
 from .sparsefuse import _dtype_code, _stream
 
 
@@ -63,4 +63,26 @@ def mi_chain(x: torch.Tensor, out: Optional[torch.Tensor] = None, *, bias=None, 
     e = epilogue(bias, act, aux, ln_gamma, ln_beta, out_pre_ln, softmax)
     check(lib().sf_mi_chain(M, N, _dtype_code(x), x.data_ptr(), x.stride(0), C.byref(e), out.data_ptr(),
                             out.stride(0), _stream(stream)))
+    return out
+
+
+def gemm_chain(x: torch.Tensor, w1_nk: torch.Tensor, w2_nk: torch.Tensor, out: Optional[torch.Tensor] = None, *,
+               bias1=None, act: str = "none", bias2=None, aux=None, ln_gamma=None, ln_beta=None, out_pre_ln=None,
+               stream=None) -> torch.Tensor:
+    """The CiCi template chained on chip (backend.hpp:270-306): out = LN(act(x @ w1.T + bias1) @ w2.T
+    + bias2 + aux); the intermediate stays in shared memory (sf_gemm_chain)."""
+    M, K1 = x.shape
+    N1, K1b = w1_nk.shape
+    N2, N1b = w2_nk.shape
+    if K1 != K1b or N1 != N1b:
+        raise _lib.ShapeError("gemm chain width mismatch")  # backend.hpp:278
+    if out is None:
+        out = torch.empty((M, N2), dtype=x.dtype, device=x.device)
+    for t in (x, w1_nk, w2_nk, out):
+        if t.stride(1) != 1:
+            raise _lib.ShapeError("GEMM operands must be row-major")
+    a = GemmChainArgs(M, K1, N1, N2, _dtype_code(x), x.data_ptr(), x.stride(0), w1_nk.data_ptr(), w1_nk.stride(0),
+                      w2_nk.data_ptr(), w2_nk.stride(0), out.data_ptr(), out.stride(0), epilogue(bias1, act),
+                      epilogue(bias2, "none", aux, ln_gamma, ln_beta, out_pre_ln))
+    check(lib().sf_gemm_chain(C.byref(a), _stream(stream)))
     return out

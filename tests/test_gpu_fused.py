@@ -181,3 +181,44 @@ def test_gemm_ln_split_auto(fz, M, N, K, pre):
     assert err.max().item() <= 2e-2 and err.sum().item() / ref.abs().sum().item() <= 1e-3
     if pre:
         assert (pre_t.float().cpu() - s).abs().max().item() <= 2e-2
+
+
+@pytest.mark.parametrize("M,K1,N1,N2", [(512, 768, 3072, 768), (300, 256, 384, 384), (128, 128, 128, 192),
+                                        (4096, 768, 3072, 768), (512, 256, 1024, 256), (200, 128, 256, 64)])
+@pytest.mark.parametrize("post", ["ln", "bias_aux", "none"])
+def test_gemm_chain(fz, oracle, M, K1, N1, N2, post):
+    """The CiCi template chained on chip (sf_gemm_chain, backend.hpp:270-306): X -> GEMM1 -> bias ->
+    GELU -> GEMM2 -> bias -> +aux -> LayerNorm, vs the per-op oracle with the intermediate rounded
+    to fp16 (the activation dtype both the chained and the two-launch forms carry it in)."""
+    import torch
+    x = r16(oracle.random_matrix(M, K1, 21))
+    w1 = r16(oracle.random_matrix(K1, N1, 22, -1 / np.sqrt(K1), 1 / np.sqrt(K1)))
+    w2 = r16(oracle.random_matrix(N1, N2, 23, -1 / np.sqrt(N1), 1 / np.sqrt(N1)))
+    b1 = oracle.random_matrix(1, N1, 24, -0.5, 0.5)[0]
+    b2 = oracle.random_matrix(1, N2, 25, -0.5, 0.5)[0]
+    aux = r16(oracle.random_matrix(M, N2, 26))
+    g = 0.5 + oracle.random_matrix(1, N2, 27, 0, 1)[0]
+    be = oracle.random_matrix(1, N2, 28, -0.5, 0.5)[0]
+    h = r16(oracle.gelu(oracle.bias(oracle.gemm(x, w1, 8), b1)))
+    y = oracle.gemm(h, w2, 8)
+    kw = {}
+    if post != "none":
+        y = oracle.add(oracle.bias(y, b2), aux)
+        kw = dict(bias2=dev(b2, torch.float32), aux=dev(aux))
+    if post == "ln":
+        y = oracle.layernorm(y, g, be)
+        kw.update(ln_gamma=dev(g, torch.float32), ln_beta=dev(be, torch.float32))
+    out = fz.gemm_chain(dev(x), dev(w1.T), dev(w2.T), bias1=dev(b1, torch.float32), act="gelu", **kw)
+    parity(out, y)
+
+
+def test_gemm_chain_shape_errors(fz):
+    import torch
+    from paper_2506_06095_b200 import _lib
+    x = torch.zeros(256, 768, dtype=torch.float16, device="cuda")
+    with pytest.raises(_lib.BackendError):  # N2 % 64 != 0
+        fz.gemm_chain(x, torch.zeros(3072, 768, dtype=torch.float16, device="cuda"),
+                      torch.zeros(96, 3072, dtype=torch.float16, device="cuda"))
+    with pytest.raises(_lib.ShapeError):
+        fz.gemm_chain(x, torch.zeros(3072, 512, dtype=torch.float16, device="cuda"),
+                      torch.zeros(768, 3072, dtype=torch.float16, device="cuda"))
