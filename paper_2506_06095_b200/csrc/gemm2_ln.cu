@@ -34,14 +34,20 @@ namespace {
 
 constexpr int BNP = 256;              // N per sub-tile (one pair MMA tile)
 constexpr int kMaxSub = 3;            // N <= 768
-constexpr int kStagesP = 5;
-constexpr int kEpiWarpsP = 8;
+#ifndef SF_LNP_EPI
+#define SF_LNP_EPI 8
+#endif
+constexpr int kEpiWarpsP = SF_LNP_EPI;          // 8 or 16: 2 or 4 warps per TMEM lane quarter
+constexpr int kGroups = kEpiWarpsP / 4;         // column groups of a sub-tile
+constexpr int kGW = BNP / kGroups;              // columns of a sub-tile per group (128 / 64)
+constexpr int kCPG = kGW / 32;                  // 32-column chunks per group and sub-tile
+constexpr int kStagesP = kEpiWarpsP == 8 ? 5 : 4;
 constexpr int kThreadsP = 128 + 32 * kEpiWarpsP;
 constexpr int kABytes = BM * BK * 2;          // 16 KB
 constexpr int kBBytes = (BNP / 2) * BK * 2;   // 16 KB
 constexpr int kStgBytesP = kEpiWarpsP * 2 * 2048;
 constexpr int kPrmFloats = 3 * kMaxSub * BNP;  // bias, gamma, beta over N
-constexpr int kPartFloats = 2 * 2 * BM * 2;    // [parity][grp][row] float2
+constexpr int kPartFloats = 2 * kGroups * BM * 2;  // [parity][grp][row] float2
 constexpr int kSmemP = 1024 + kStagesP * (kABytes + kBBytes) + kStgBytesP + 512 + (kPrmFloats + kPartFloats) * 4;
 constexpr uint32_t kColB = 256;
 
@@ -270,26 +276,26 @@ __global__ void __launch_bounds__(kThreadsP, 1) gemm2_ln_kernel(const __grid_con
             uint32_t r[32];
             float x[32];
             if (p.aux) {  // the residual ring runs two chunks ahead, across sub-tiles
-                res_issue(0, grp * 128, row0);
-                res_issue(1, grp * 128 + 32, row0);
+                res_issue(0, grp * kGW, row0);
+                res_issue(1, grp * kGW + 32, row0);
             }
             // ---- E_sub: bias (+act) + residual, chunk statistics, pre-LN values parked in TMEM
 #pragma unroll 1
-            for (int k = 0; k < 4 * nsub; ++k) {
-                const int sub = k >> 2, cc = k & 3;
+            for (int k = 0; k < kCPG * nsub; ++k) {
+                const int sub = k / kCPG, cc = k % kCPG;
                 const bool last = sub == nsub - 1;
-                const uint32_t src = (sub == 0 && !last ? 0u : kColB) + 128u * grp;
+                const uint32_t src = (sub == 0 && !last ? 0u : kColB) + kGW * grp;
                 if (cc == 0) {
                     tc::mbar_wait(&tfull[sub], i & 1);
                     if (warp == 4 && lane == 0) LTRACE(8 * sub + 2);
                     tc::fence_after_sync();
                 }
-                const int col = sub * BNP + grp * 128 + cc * 32;
+                const int col = sub * BNP + grp * kGW + cc * 32;
                 if (cc == 0) tc::tmem_ld32(tl + src, r);  // later chunks were issued one chunk ahead
                 tc::tmem_ld_wait();
 #pragma unroll
                 for (int j = 0; j < 32; ++j) x[j] = __uint_as_float(r[j]);
-                if (cc < 3) tc::tmem_ld32(tl + src + 32 * (cc + 1), r);
+                if (cc + 1 < kCPG) tc::tmem_ld32(tl + src + 32 * (cc + 1), r);
                 const float4* b4 = reinterpret_cast<const float4*>(sprm + col);
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
@@ -318,7 +324,7 @@ __global__ void __launch_bounds__(kThreadsP, 1) gemm2_ln_kernel(const __grid_con
                         for (int e = 0; e < 8; ++e) x[8 * j + e] += DT<T>::to_f(h[e]);
                     }
                     const int k2 = k + 2;  // chunk k + 2 of the warp's walk into the box just read
-                    if (k2 < 4 * nsub) res_issue(b_, (k2 >> 2) * BNP + grp * 128 + (k2 & 3) * 32, row0);
+                    if (k2 < kCPG * nsub) res_issue(b_, (k2 / kCPG) * BNP + grp * kGW + (k2 % kCPG) * 32, row0);
                 }
                 float2 s2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
@@ -348,36 +354,47 @@ __global__ void __launch_bounds__(kThreadsP, 1) gemm2_ln_kernel(const __grid_con
                     uint32_t pk[16];
 #pragma unroll
                     for (int j = 0; j < 16; ++j) pk[j] = pack2<T>(x[2 * j], x[2 * j + 1]);
-                    tc::tmem_st16(tl + 128u * grp + 64u * sub + 16u * cc, pk);
+                    tc::tmem_st16(tl + kGW * grp + (kGW / 2) * sub + 16u * cc, pk);
                 }
-                if (cc == 3) {
+                if (cc == kCPG - 1) {
                     tc::tmem_st_wait();
                     if (warp == 4 && lane == 0) LTRACE(8 * sub + 3);
                     if (sub == 1 && !last) arrive_leader(bfree1);  // B may take sub-tile 2
                 }
             }
             // ---- the row's (mean, M2): this thread's columns, then the other column half's warp
-            float2* slot = part + (i & 1) * (2 * BM);
+            float2* slot = part + (i & 1) * (kGroups * BM);
             slot[grp * BM + r_local] = make_float2(run_mean, run_m2);
             asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarpsP) : "memory");
             if (warp == 4 && lane == 0) LTRACE(24);
-            const float2 o = slot[(grp ^ 1) * BM + r_local];
-            const float mean = 0.5f * (run_mean + o.x);
-            const float half_cols = static_cast<float>(p.N / 2);
-            const float m2 = run_m2 + o.y + half_cols * ((run_mean - mean) * (run_mean - mean) + (o.x - mean) * (o.x - mean));
+            float2 part_g[kGroups];  // every group's (mean, M2) over an equal share of the row
+            float mean = 0.f;
+#pragma unroll
+            for (int g2 = 0; g2 < kGroups; ++g2) {
+                part_g[g2] = slot[g2 * BM + r_local];
+                mean += part_g[g2].x;
+            }
+            mean *= 1.f / kGroups;
+            const float group_cols = static_cast<float>(p.N / kGroups);
+            float m2 = 0.f;
+#pragma unroll
+            for (int g2 = 0; g2 < kGroups; ++g2) {
+                const float dd = part_g[g2].x - mean;
+                m2 += part_g[g2].y + group_cols * dd * dd;
+            }
             const float inv = 1.0f / sqrtf(m2 / static_cast<float>(p.N) + kLnEps);
             // ---- normalise and store; chunk k + 1's TMEM load flies while chunk k is normalised
             auto norm_load = [&](int k) {
-                const int sub = k >> 2, cc = k & 3;
-                if (sub == nsub - 1) tc::tmem_ld32(tl + kColB + 128u * grp + 32u * cc, r);
-                else tc::tmem_ld16(tl + 128u * grp + 64u * sub + 16u * cc, *reinterpret_cast<uint32_t(*)[16]>(r));
+                const int sub = k / kCPG, cc = k % kCPG;
+                if (sub == nsub - 1) tc::tmem_ld32(tl + kColB + kGW * grp + 32u * cc, r);
+                else tc::tmem_ld16(tl + kGW * grp + (kGW / 2) * sub + 16u * cc, *reinterpret_cast<uint32_t(*)[16]>(r));
             };
             norm_load(0);
 #pragma unroll 1
-            for (int k = 0; k < 4 * nsub; ++k) {
-                const int sub = k >> 2, cc = k & 3;
+            for (int k = 0; k < kCPG * nsub; ++k) {
+                const int sub = k / kCPG, cc = k % kCPG;
                 const bool last = sub == nsub - 1;
-                const int col = sub * BNP + grp * 128 + cc * 32;
+                const int col = sub * BNP + grp * kGW + cc * 32;
                 tc::tmem_ld_wait();
                 if (last) {
 #pragma unroll
@@ -390,7 +407,7 @@ __global__ void __launch_bounds__(kThreadsP, 1) gemm2_ln_kernel(const __grid_con
                         x[2 * j + 1] = DT<T>::to_f(h[1]);
                     }
                 }
-                if (k + 1 < 4 * nsub) norm_load(k + 1);
+                if (k + 1 < kCPG * nsub) norm_load(k + 1);
                 // y = ((x - mean) inv) g + e as two packed FMAs per pair
                 float y[32];
                 const float4* g4 = reinterpret_cast<const float4*>(sprm + p.N + col);
