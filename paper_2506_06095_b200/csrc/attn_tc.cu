@@ -132,7 +132,6 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
     int32_t* s_item = reinterpret_cast<int32_t*>(item_empty + kItemRing);  // [kItemRing]
     uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(s_item + kItemRing);
 
-    pdl_enter();
     const uint32_t warp = tc::warp_id();
     const uint32_t lane = threadIdx.x & 31;
 
@@ -179,6 +178,9 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
     __syncthreads();
     tc::fence_after_sync();
     const uint32_t tmem = *tmem_ptr;
+    // the prologue above reads only the BSR (not written by the stream predecessor): it overlaps the
+    // predecessor's tail under PDL; Q/K/V and O are touched only after this wait
+    pdl_enter();
     const uint32_t tO = tmem + kOCol;
     const Items items{s_lrp, s_order, p.bh, p.n_items, G};
     const ItemFeed feed{s_item, item_full, item_empty};

@@ -93,7 +93,6 @@ __global__ void __launch_bounds__(kThreadsP, 1) gemm2_ln_kernel(const __grid_con
     float* sprm = reinterpret_cast<float*>(sStg + kStgBytesP + 512);  // [3][N]: bias, gamma, beta
     float2* part = reinterpret_cast<float2*>(sprm + kPrmFloats);       // [2][2][BM]
 
-    pdl_enter();
     LSPAN(1);
     const uint32_t warp = tc::warp_id();
     const uint32_t lane = threadIdx.x & 31;
@@ -135,6 +134,9 @@ __global__ void __launch_bounds__(kThreadsP, 1) gemm2_ln_kernel(const __grid_con
     tc::cluster_sync_all();
     tc::fence_after_sync();
     const uint32_t tmem = *tmem_ptr;
+    // the prologue above reads only parameters (bias / LayerNorm vectors): it overlaps the stream
+    // predecessor's tail under PDL; activations are read and outputs written only after this wait
+    pdl_enter();
 
     if (warp == 0) {
         // ------------------------------------------------------------------ TMA producer (both CTAs)

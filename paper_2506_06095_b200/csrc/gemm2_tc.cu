@@ -92,7 +92,6 @@ __global__ void __launch_bounds__(Cfg2<LN>::THREADS, 1) gemm2_kernel(const __gri
 #ifdef SF_GEMM_TRACE
     const long long c_entry = clock64();
 #endif
-    pdl_enter();
     GSPAN(1);
     const uint32_t warp = tc::warp_id();
     const uint32_t lane = threadIdx.x & 31;
@@ -152,6 +151,9 @@ __global__ void __launch_bounds__(Cfg2<LN>::THREADS, 1) gemm2_kernel(const __gri
     tc::cluster_sync_all();
     tc::fence_after_sync();
     const uint32_t tmem = *tmem_ptr;
+    // the prologue above reads only parameters (bias / LayerNorm vectors): it overlaps the stream
+    // predecessor's tail under PDL; activations are read and outputs written only after this wait
+    pdl_enter();
 
     if (warp == 0) {
         // ------------------------------------------------------------------ TMA producer (both CTAs)

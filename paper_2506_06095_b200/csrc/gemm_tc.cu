@@ -40,7 +40,6 @@ struct Cfg {
 template <typename T, int BN, bool LN>
 __global__ void __launch_bounds__(Cfg<BN, LN>::THREADS, 1) gemm_fused_kernel(const __grid_constant__ GemmParams p) {
     using C = Cfg<BN, LN>;
-    pdl_enter();
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     unsigned char* sA = smem;
@@ -102,6 +101,7 @@ __global__ void __launch_bounds__(Cfg<BN, LN>::THREADS, 1) gemm_fused_kernel(con
     if (csz > 1) tc::cluster_sync_all();  // peers' barriers are initialised before any remote traffic
     tc::fence_after_sync();
     const uint32_t tmem = *tmem_ptr;
+    pdl_enter();  // the prologue above overlaps the stream predecessor's tail under PDL
 
     if (warp == 0) {
         // ------------------------------------------------------------------ TMA producer

@@ -161,7 +161,6 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, V >= 4 ? 2 : 3) mi_chain_ro
                                                                           const T* __restrict__ x, int64_t ldx,
                                                                           sf_gemm_epilogue e, T* __restrict__ out,
                                                                           int64_t ldout) {
-    pdl_enter();
     __shared__ float4 sprm[3][2 * V * 32];  // bias, gamma, beta
     const int lane = threadIdx.x & 31;
     const T* aux = static_cast<const T*>(e.aux);
@@ -176,6 +175,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, V >= 4 ? 2 : 3) mi_chain_ro
             sprm[j][t] = (src[j] && c < N) ? *reinterpret_cast<const float4*>(src[j] + c) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
     __syncthreads();
+    pdl_enter();  // the parameter staging above overlaps the stream predecessor's tail
     const int64_t stride = static_cast<int64_t>(gridDim.x) * kWarpsPerCta;
     int64_t row = static_cast<int64_t>(blockIdx.x) * kWarpsPerCta + (threadIdx.x >> 5);
     bool ok[V];
