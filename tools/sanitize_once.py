@@ -1,5 +1,6 @@
-"""Small multi-item launches of the tcgen05 attention (both schedules) and the CTA-pair GEMM
-for compute-sanitizer (racecheck / synccheck / memcheck). The attention grid is capped at 8
+"""Small multi-item launches of the tcgen05 attention (both schedules, and the head-group kernel),
+the CTA-pair GEMM, the row-panel LayerNorm GEMM and the chained CiCi kernel for compute-sanitizer
+(racecheck / synccheck / memcheck). The attention grid is capped at 8
 CTAs (SF_ATTN_MAX_CTAS) so every CTA walks ~24 items: Q double-buffering, the item ring, the
 O-barrier phases across items and the counter reset all run. Checks the results too.
 usage: compute-sanitizer --tool racecheck python tools/sanitize_once.py"""
@@ -31,10 +32,40 @@ for static in ("0", "1"):
         err = np.abs(out.float().cpu().numpy() - ref).max()
         assert err < 2e-2, err
         print(f"attn static={static} max_abs {err:.2e}")
+os.environ["SF_ATTN_STATIC"] = "0"
+os.environ["SF_ATTN_HEADGROUP"] = "1"  # attn_tc3.cu: three heads per item, ~16 items per CTA here
+for _ in range(2):
+    out = sf.block_sparse_sdpa(Q, K, V, b)
+    torch.cuda.synchronize()
+    err = np.abs(out.float().cpu().numpy() - ref).max()
+    assert err < 2e-2, err
+    print(f"attn head groups max_abs {err:.2e}")
+os.environ["SF_ATTN_HEADGROUP"] = "0"
 x = torch.randn(512, 768, device="cuda").half()
 w = torch.randn(768, 768, device="cuda").half() * 0.03
 y = fused.gemm_fused(x, w, tile_n=1)
 err = (y.float() - x.float() @ w.float().t()).abs().max().item()
 print(f"gemm pair max_abs {err:.2e}")
 assert err < 2e-2
+# row-panel LayerNorm GEMM (gemm2_ln.cu): 512 rows = two panels, N 768 = three sub-tiles
+g, be = torch.rand(768, device="cuda") + 0.5, torch.rand(768, device="cuda") - 0.5
+aux = torch.randn(512, 768, device="cuda").half()
+pre = torch.empty(512, 768, device="cuda").half()
+y = fused.gemm_fused(x, w, aux=aux, ln_gamma=g, ln_beta=be, out_pre_ln=pre, tile_n=1)
+r = x.float() @ w.float().t() + aux.float()
+r = (r - r.mean(1, keepdim=True)) / torch.sqrt(r.var(1, unbiased=False, keepdim=True) + 1e-5) * g + be
+err = (y.float() - r).abs().max().item()
+print(f"gemm row-panel LN max_abs {err:.2e}")
+assert err < 5e-2
+# chained CiCi (cici.cu): 256 rows, 768 -> 1024 -> 768, GELU, LayerNorm
+w1 = torch.randn(1024, 768, device="cuda").half() * 0.03
+w2 = torch.randn(768, 1024, device="cuda").half() * 0.03
+xc = x[:256].contiguous()
+y = fused.gemm_chain(xc, w1, w2, act="gelu", aux=aux[:256].contiguous(), ln_gamma=g, ln_beta=be)
+hmid = torch.nn.functional.gelu(xc.float() @ w1.float().t()).half().float()
+r = hmid @ w2.float().t() + aux[:256].float()
+r = (r - r.mean(1, keepdim=True)) / torch.sqrt(r.var(1, unbiased=False, keepdim=True) + 1e-5) * g + be
+err = (y.float() - r).abs().max().item()
+print(f"gemm chain max_abs {err:.2e}")
+assert err < 5e-2
 print("sanitize_once ok")
