@@ -512,8 +512,11 @@ bool gemm_ln_panel_supported(const sf_gemm_args& a) {
     // three pairs read one panel together, is faster (70 vs 84 us; tools/ln_time.py)
     // and the pairs run one panel each: a second panel per pair cannot overlap the first one's
     // normalise pass (T5 cfg4, M = 32768: 87 vs 82 us), so longer M keeps the cluster form
+    // Fewer panels than ~3/4 of the pairs would leave SMs idle that the cluster form (one pair per
+    // 256 x 256 tile) keeps busy.
+    const int64_t panels = ceil_div(a.M, 2 * BM);
     return a.M > BM && (a.N == 512 || a.N == 768) && a.K <= 1024 && a.epi.ln_gamma && a.epi.ln_beta &&
-           ceil_div(a.M, 2 * BM) <= max_pairs_ln();
+           panels <= max_pairs_ln() && 4 * panels >= 3 * max_pairs_ln();
 }
 
 sf_status gemm_ln_panel(const sf_gemm_args& a, cudaStream_t st) {
