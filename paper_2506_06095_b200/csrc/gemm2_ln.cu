@@ -507,6 +507,8 @@ sf_status launch_ln_panel(const sf_gemm_args& a, cudaStream_t st) {
 bool gemm_ln_panel_supported(const sf_gemm_args& a) {
     const char* e = std::getenv("SF_GEMM_LN_CLUSTER");
     if (e && *e == '1') return false;
+    const char* f = std::getenv("SF_GEMM_LN_PANEL");  // test aid: the panel form whenever the shape fits
+    const bool force = f && *f == '1';
     // the panel form reads the X panel once per sub-tile: from L2 when K is short (the out-projection,
     // K = 768: 41 vs 43 us cold); at K = 3072 the re-reads come from HBM and the cluster form, whose
     // three pairs read one panel together, is faster (70 vs 84 us; tools/ln_time.py)
@@ -516,7 +518,7 @@ bool gemm_ln_panel_supported(const sf_gemm_args& a) {
     // 256 x 256 tile) keeps busy.
     const int64_t panels = ceil_div(a.M, 2 * BM);
     return a.M > BM && (a.N == 512 || a.N == 768) && a.K <= 1024 && a.epi.ln_gamma && a.epi.ln_beta &&
-           panels <= max_pairs_ln() && 4 * panels >= 3 * max_pairs_ln();
+           panels <= max_pairs_ln() && (force || 4 * panels >= 3 * max_pairs_ln());
 }
 
 sf_status gemm_ln_panel(const sf_gemm_args& a, cudaStream_t st) {

@@ -61,8 +61,13 @@ def test_gemm_bias_act(fz, oracle, act, tile):
 
 
 @pytest.mark.parametrize("N,K", [(768, 768), (768, 3072), (512, 256), (256, 128), (1024, 256)])
-@pytest.mark.parametrize("tile", [0, 128, 256, PAIR])
-def test_gemm_bias_add_layernorm(fz, oracle, N, K, tile):
+@pytest.mark.parametrize("tile", [0, 128, 256, PAIR, "panel"])
+def test_gemm_bias_add_layernorm(fz, oracle, N, K, tile, monkeypatch):
+    """tile "panel": the row-panel LayerNorm GEMM (gemm2_ln.cu) forced at this short M (it is the
+    automatic choice only when the panels fill most of the pairs, e.g. 16384 rows)."""
+    if tile == "panel":
+        monkeypatch.setenv("SF_GEMM_LN_PANEL", "1")
+        tile = PAIR
     import torch
     M = 384
     x = r16(oracle.random_matrix(M, K, 6))

@@ -48,6 +48,7 @@ err = (y.float() - x.float() @ w.float().t()).abs().max().item()
 print(f"gemm pair max_abs {err:.2e}")
 assert err < 2e-2
 # row-panel LayerNorm GEMM (gemm2_ln.cu): 512 rows = two panels, N 768 = three sub-tiles
+os.environ["SF_GEMM_LN_PANEL"] = "1"
 g, be = torch.rand(768, device="cuda") + 0.5, torch.rand(768, device="cuda") - 0.5
 aux = torch.randn(512, 768, device="cuda").half()
 pre = torch.empty(512, 768, device="cuda").half()
