@@ -272,7 +272,7 @@ def run_sweep(args):
             dm = sf.generate_mask(sweep_terms(pat, n))
             nnz = dm.true_count()
             plan = sf.select_plan(dm, sf.hw_preset("b200"), n, h, bs, d, mode="b200")  # the job's plan
-            ctx = sf.MhaContext(dm, plan)
+            ctx = sf.MhaContext(dm, plan, strided_band=sf.strided_band(sweep_terms(pat, n)))
             run = lambda: sf.mha(q, k, v, ctx, out=o)
             for _ in range(3):
                 run()
@@ -302,7 +302,7 @@ def run_sweep(args):
             line = {"sweep": "masked_mha", "pattern": pat, "seq_len": n, "bs": bs, "heads": h, "head_size": d,
                     "n_gpus": world, "slices_per_rank": s1 - s0, "scaling": "strong",
                     "nnz_per_slice": nnz, "density": nnz / float(n * n),
-                    "plan": [plan.kind, plan.block_m, plan.block_n], "latency_us": us,
+                    "plan": sf.executor_label(ctx), "latency_us": us,
                     "useful_tflops": flops / us / 1e6, "compulsory_gbs": comp / us / 1e3,  # whole job
                     "roofline": {"bound": binds, "bound_us": bound_us, "t_tensor_us": t_tc, "t_mufu_us": t_exp,
                                  "t_hbm_us": t_hbm, "frac": bound_us / us},
@@ -567,7 +567,7 @@ def main():
     dm = sf.generate_mask(cfg["mask"])
     nnz = dm.true_count()
     plan = sf.select_plan(dm, sf.hw_preset("b200"), s.seq_len, s.heads, s.bs, s.head_size, mode="b200")
-    ctx = sf.MhaContext(dm, plan)
+    ctx = sf.MhaContext(dm, plan, strided_band=sf.strided_band(cfg["mask"]))
     W = layer.init_weights(cfg["model"], s, seed=1)  # one model: the same weights on every rank
     L = layer.EncoderLayer(cfg["model"], s, W, ctx, ln_split=args.ln_split)
     g = torch.Generator(device="cuda").manual_seed(7)
@@ -735,7 +735,7 @@ def main():
     if traffic_file.exists():
         roof["traffic"] = json.loads(traffic_file.read_text()).get(args.config, {}).get(dom)
     mha_ms = parts["masked_mha"]
-    mha = {"latency_us": mha_ms * 1e3, "plan": [plan.kind, plan.block_m, plan.block_n],
+    mha = {"latency_us": mha_ms * 1e3, "plan": sf.executor_label(ctx),
            "nnz_per_slice": nnz, "useful_tflops": mha_flops / (mha_ms / 1e3) / 1e12,
            "compulsory_gbs": wm["masked_mha"][1] / (mha_ms / 1e3) / 1e9,
            "hbm_frac": wm["masked_mha"][1] / (mha_ms / 1e3) / 1e9 / pk["hbm_gbs"]}

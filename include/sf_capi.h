@@ -266,6 +266,16 @@ sf_status sf_mha_blockwise(const sf_attn_args* args, const sf_bsr_dev* bsr, cons
 /* Row-wise gather executor over a device CSR. Replaces rowwise_sdpa (attention.hpp:177-213). */
 sf_status sf_mha_rowwise(const sf_attn_args* args, const sf_csr_dev* csr, void* stream);
 
+/* Masked MHA for the strided pattern (sf_pattern SF_PATTERN_STRIDED, band w) by mask decomposition:
+ * strided(w) = causal-local(w) (disjoint-)union the diagonals i - j = k w, k >= 1. The band runs on
+ * the tcgen05 block kernel over `band_bsr` (the block_m 128 BSR of the causal-local(w) mask, e.g.
+ * sf_mask_generate of {SF_PATTERN_CAUSAL_LOCAL, w} then sf_bsr_build), emitting per-row
+ * log-sum-exp; the diagonals are exact dense causal attention inside each residue class i % w
+ * (warp-level tensor-core MMAs) merged into the band's output. Same result semantics as
+ * sf_mha_blockwise over the strided mask (attention.hpp:71-172). Needs head_size 64 and
+ * ceil(seq_len / w) <= 128, else SF_PLAN_ERROR. */
+sf_status sf_mha_strided(const sf_attn_args* args, int32_t band_width, const sf_bsr_dev* band_bsr, void* stream);
+
 /* Dense masked SDPA reference on the device (dense_sdpa_oracle, attention.hpp:15-56): reads the
  * DENSE bit mask (sf_mask_generate's layout), accumulates in fp64 with the reference's exact
  * two-pass softmax, and writes fp64 output (bs, h, n, head_size) contiguous to `o64`. Rows with no

@@ -133,6 +133,7 @@ SIGNATURES = {
     "sf_select_plan_from_loads": (C.c_int, [_I64, C.POINTER(HwSpec), _I64, _I32, _I64, _I32, _I32, C.POINTER(Plan)]),
     "sf_mha_blockwise": (C.c_int, [C.POINTER(AttnArgs), C.POINTER(BsrDev), C.POINTER(Plan), C.POINTER(AttnStats), _P]),
     "sf_mha_rowwise": (C.c_int, [C.POINTER(AttnArgs), C.POINTER(CsrDev), _P]),
+    "sf_mha_strided": (C.c_int, [C.POINTER(AttnArgs), _I32, C.POINTER(BsrDev), _P]),
     "sf_mha_dense_oracle": (C.c_int, [C.POINTER(AttnArgs), _P, _P, _P]),
     "sf_set_attn_impl": (C.c_int, [_I32]),
     "sf_set_pdl": (C.c_int, [_I32]),

@@ -78,6 +78,7 @@ struct AttnParams {
     int64_t o_sb, o_sh, o_sn;
     float scale_log2;
     unsigned* work;  // [2]: next item, CTAs done (dynamic schedule), or null (static deal)
+    float* lse;      // optional [b*h][n] log2-sum-exp2 per row (null: not written)
     unsigned long long* trace;  // optional clock64 trace of CTA 0 (sf_debug_attn_trace)
 };
 
@@ -366,11 +367,15 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
         // last P is published, so the warps first compute the next item's step-0 probabilities and
         // only then wait for that P.V and read O, just before publishing P_0 of the next item (whose
         // P.V overwrites O). The wait for the last P.V hides behind a softmax step.
-        auto epilogue = [&](int rb_, int bh_, float l_, bool have_o, uint32_t g_last) {
+        auto epilogue = [&](int rb_, int bh_, float l_, float m_, bool have_o, uint32_t g_last) {
             const int slice = kPair ? 2 * bh_ + my_head : bh_;
             const bool slice_ok = slice < p.bh_total;  // an odd last head pair has no head B
             const int b = slice_ok ? slice / p.h : 0, hh = slice_ok ? slice % p.h : 0;
             const int64_t i = static_cast<int64_t>(rb_) * BM + r;
+            // optional per-row log2-sum-exp2 of the scaled scores (m + log2 l), for merging partial
+            // attentions over disjoint key sets (sf_mha_strided); -inf for rows without a valid key
+            if (p.lse && slice_ok && i < p.n)
+                p.lse[static_cast<int64_t>(slice) * p.n + i] = (have_o && l_ > 0.f) ? m_ + __log2f(l_) : -INFINITY;
             if (have_o) {
                 tc::mbar_wait(&o_full[g_last & 1], (g_last >> 1) & 1);
                 tc::fence_after_sync();
@@ -402,7 +407,7 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
         };
         bool pend = false;  // an item whose epilogue is deferred into the next item's step 0
         int pend_rb = 0, pend_bh = 0;
-        float pend_l = 0.f;
+        float pend_l = 0.f, pend_m = 0.f;
         uint32_t pend_g = 0;
         uint32_t g = 0;
         for (uint32_t k = 0;; ++k) {
@@ -528,7 +533,7 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
                 }
                 l += (rs2[0].x + rs2[0].y) + (rs2[1].x + rs2[1].y);
                 if (j == 0 && pend) {  // the previous item's O is read before P_0 lets P.V overwrite it
-                    epilogue(pend_rb, pend_bh, pend_l, true, pend_g);
+                    epilogue(pend_rb, pend_bh, pend_l, pend_m, true, pend_g);
                     pend = false;
                 }
                 // P_g (64 keys = 32 packed columns) into P[sb] in TMEM
@@ -544,12 +549,13 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
                 pend_rb = rb;
                 pend_bh = bh;
                 pend_l = l;
+                pend_m = m;
                 pend_g = g - 1;
             } else {
-                epilogue(rb, bh, 0.f, false, 0);  // an empty row block: zeros, no TMEM access
+                epilogue(rb, bh, 0.f, 0.f, false, 0);  // an empty row block: zeros, no TMEM access
             }
         }
-        if (pend) epilogue(pend_rb, pend_bh, pend_l, true, pend_g);
+        if (pend) epilogue(pend_rb, pend_bh, pend_l, pend_m, true, pend_g);
     }
     tc::fence_before_sync();
     __syncthreads();
@@ -660,7 +666,7 @@ void attn_reserve_counters(cudaStream_t st) {
     reserve_pool_locked(dev, st);
 }
 
-sf_status attn_tc(const sf_attn_args& a, const sf_bsr_dev& b, cudaStream_t st, bool probe_only) {
+sf_status attn_tc(const sf_attn_args& a, const sf_bsr_dev& b, cudaStream_t st, bool probe_only, float* lse) {
     const bool shape_ok = (b.block_m == 128 || b.block_m == 64) && (b.block_n == 16 || b.block_n == 32 || b.block_n == 64) &&
                           a.head_size == kD && b.n_rows <= kMaxRowBlocks;
     const bool layout_ok = a.q_sn % 8 == 0 && a.q_sh % 8 == 0 && a.q_sb % 8 == 0 && a.o_sn % 8 == 0 &&
@@ -673,7 +679,7 @@ sf_status attn_tc(const sf_attn_args& a, const sf_bsr_dev& b, cudaStream_t st, b
     if (probe_only) return SF_OK;
     if (b.tile_bytes != b.block_m * b.block_n / 8) return fail(SF_PLAN_ERROR, "BSR tile_bytes does not match block shape");
     // head groups sharing one mask per work item (attn_tc3.cu) where the slice has >= 3 heads
-    if (attn_tc3_eligible(a, b)) return attn_tc3(a, b, st);
+    if (!lse && attn_tc3_eligible(a, b)) return attn_tc3(a, b, st);
     AttnParams p{};
     const bool bf = a.dtype == SF_BF16;
     SF_TRY(make_tmap_4d(&p.tq, a.q, a.seq_len, a.h, a.bs, a.q_sn, a.q_sh, a.q_sb, b.block_m, bf));
@@ -696,6 +702,7 @@ sf_status attn_tc(const sf_attn_args& a, const sf_bsr_dev& b, cudaStream_t st, b
     p.scale_log2 = a.scale * 1.4426950408889634f;
     p.trace = g_attn_trace;
     p.work = attn_work_counter(st);
+    p.lse = lse;
     void (*kern)(AttnParams) = nullptr;
     int smem = AttnGeo<128>::kSmemG;
     if (b.block_m == 128) {

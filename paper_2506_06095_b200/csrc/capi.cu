@@ -25,7 +25,7 @@ void note_launch(int64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed)
 sf_status check_attn_args(const sf_attn_args& a);
 sf_status attn_generic(const sf_attn_args& a, const sf_bsr_dev& b, cudaStream_t st);
 // attn_tc.cu: returns SF_PLAN_ERROR (without launching) when the shape is not supported.
-sf_status attn_tc(const sf_attn_args& a, const sf_bsr_dev& b, cudaStream_t st, bool probe_only);
+sf_status attn_tc(const sf_attn_args& a, const sf_bsr_dev& b, cudaStream_t st, bool probe_only, float* lse = nullptr);
 
 namespace {
 

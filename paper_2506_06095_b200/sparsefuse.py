@@ -460,12 +460,52 @@ def dense_sdpa_oracle(q, k, v, mask: "DenseMask", stream=None) -> torch.Tensor:
     return o64
 
 
-class MhaContext:
-    """Formats + plan for one session mask (backend.hpp:309-321 MhaContext), built on device."""
+def strided_sdpa(q, k, v, band_width: int, band_bsr: BsrMask, out=None, stream=None):
+    """Masked MHA over the strided(w) mask by decomposition (sf_mha_strided): the causal-local(w)
+    band on the tcgen05 block kernel (band_bsr: its block_m 128 BSR) plus the i - j = k w diagonals
+    as dense causal attention inside each residue class, merged by log-sum-exp. Same semantics as
+    block_sparse_sdpa over the strided mask (attention.hpp:71-172)."""
+    o = out if out is not None else torch.empty_like(q)
+    a = attn_args(q, k, v, o)
+    check(lib().sf_mha_strided(C.byref(a), int(band_width), C.byref(band_bsr.dev), _stream(stream)))
+    return o
 
-    def __init__(self, mask: DenseMask, plan: KernelPlan, stream=None):
+
+def strided_band(terms) -> Optional[int]:
+    """The band w when the mask descriptor is exactly one strided(w) term with n >= 2048 that the
+    decomposed executor covers (ceil(n / w) <= 128), else None."""
+    ts = terms if isinstance(terms, (list, tuple)) else [terms]
+    if len(ts) != 1:
+        return None
+    t = ts[0] if isinstance(ts[0], MaskDescriptor) else MaskDescriptor(**ts[0])
+    # below n = 2048 the block-wise executor over the whole strided mask is as fast or faster
+    # (bs16 x 12 heads, n 1024, w 32: 59 vs 67 us; n 2048, w 45: 196 vs 137 us; tools/strided_time.py)
+    if t.pattern != "strided" or t.band_width < 1 or -(-t.seq_len // t.band_width) > 128 or t.seq_len < 2048:
+        return None
+    return int(t.band_width)
+
+
+def executor_label(ctx) -> list:
+    """The executor a context runs, as reported by the bench: [kind, block_m, block_n] or
+    ["strided_decomposed", band_width, 0]."""
+    if getattr(ctx, "strided_band", None):
+        return ["strided_decomposed", int(ctx.strided_band), 0]
+    return [ctx.plan.kind, ctx.plan.block_m, ctx.plan.block_n]
+
+
+class MhaContext:
+    """Formats + plan for one session mask (backend.hpp:309-321 MhaContext), built on device.
+    strided_band=w (a mask that is one strided(w) descriptor, see strided_band()): the unified MHA
+    runs the decomposed strided executor (band BSR built here) instead of the plan's executor."""
+
+    def __init__(self, mask: DenseMask, plan: KernelPlan, stream=None, strided_band: Optional[int] = None):
         self.mask = mask
         self.plan = plan
+        self.strided_band = strided_band
+        self.band_bsr = None
+        if strided_band:
+            band = generate_mask([dict(pattern="causal_local", seq_len=mask.seq_len, band_width=strided_band)], stream)
+            self.band_bsr = build_bsr(band, 128, 16, stream)
         if plan.kind == "block_wise":
             self.bsr = build_bsr(mask, plan.block_m, plan.block_n, stream)
             self.csr = None
@@ -475,7 +515,10 @@ class MhaContext:
 
 
 def mha(q, k, v, ctx: MhaContext, out=None, stream=None):
-    """Unified MHA entry: dispatches the row-wise or block-wise executor from the plan."""
+    """Unified MHA entry: dispatches the row-wise or block-wise executor from the plan (or the
+    decomposed strided executor when the context carries a strided band)."""
+    if ctx.strided_band:
+        return strided_sdpa(q, k, v, ctx.strided_band, ctx.band_bsr, out=out, stream=stream)
     if ctx.plan.kind == "block_wise":
         return block_sparse_sdpa(q, k, v, ctx.bsr, ctx.plan, out=out, stream=stream)
     return rowwise_sdpa(q, k, v, ctx.csr, out=out, stream=stream)

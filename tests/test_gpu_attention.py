@@ -1,6 +1,7 @@
 """Masked MHA on the GPU vs the reference executors (north-star bar: fp16 outputs within
 max-abs 2e-2 and mean-rel (sum|d| / sum|ref|) 1e-3 of the reference's fp32 results on the same
 fp16-rounded inputs). Cases follow test_attention.cpp."""
+import os
 from pathlib import Path
 
 import numpy as np
@@ -259,3 +260,29 @@ def test_device_dense_oracle_matches_reference(sf, oracle, terms, n):
     assert np.abs(got - ref).max() <= 1e-9
     empty = ~m.any(axis=1)
     assert np.all(got[:, :, empty, :] == 0.0)
+
+
+@pytest.mark.parametrize("n,w,bs,h", [(2048, 45, 8, 12), (2048, 45, 2, 12), (512, 22, 2, 3), (1000, 31, 1, 4),
+                                     (8192, 90, 1, 2)])
+def test_strided_decomposition_matches_oracle(sf, oracle, n, w, bs, h):
+    """sf_mha_strided (causal-local band on the tcgen05 kernel + per-residue-class dense causal
+    attention, merged by log-sum-exp) against the oracle's block_sparse_sdpa over the strided mask
+    (attention.hpp:71-172): the decomposition changes the executor, not the result."""
+    import torch
+    terms = [dict(pattern="strided", seq_len=n, band_width=w)]
+    m = oracle.mask(terms)
+    q, k, v = (x.astype(np.float16).astype(np.float32) for x in oracle.random_attention_input(bs, h, n, 64, 3))
+    ref, _ = oracle.block_sparse_sdpa(q, k, v, m, 128, 16, threads=os.cpu_count() or 8)
+    assert sf.strided_band(terms) == (w if n >= 2048 else None)
+    band = sf.generate_mask([dict(pattern="causal_local", seq_len=n, band_width=w)])
+    bb = sf.build_bsr(band, 128, 16)
+    dev = lambda x: torch.from_numpy(x).to("cuda", torch.float16)
+    out = sf.strided_sdpa(dev(q), dev(k), dev(v), w, bb).float().cpu().numpy()
+    d = np.abs(out - ref)
+    assert d.max() <= 2e-2 and d.sum() / np.abs(ref).sum() <= 1e-3, (d.max(), d.sum() / np.abs(ref).sum())
+    # through the unified MHA entry with a context that carries the band
+    dm = sf.generate_mask(terms)
+    plan = sf.select_plan(dm, sf.hw_preset("b200"), n, h, bs, 64, mode="b200")
+    ctx = sf.MhaContext(dm, plan, strided_band=w)
+    out2 = sf.mha(dev(q), dev(k), dev(v), ctx).float().cpu().numpy()
+    assert np.abs(out2 - out).max() == 0.0
