@@ -99,14 +99,36 @@ struct MhaContext {
     KernelPlan plan;
     std::optional<BsrMask> bsr;
     std::optional<RowwiseMask> rw;
+    // strided(w) masks executed by decomposition (sf_mha_strided): the causal-local(w) band's BSR
+    int32_t strided_band = 0;
+    std::optional<BsrMask> band_bsr;
 
     static MhaContext make(const DenseMask& mask, const KernelPlan& plan) {
-        MhaContext ctx{mask, plan, {}, {}};
+        MhaContext ctx{mask, plan, {}, {}, 0, {}};
         if (plan.kind == KernelKind::BlockWise) ctx.bsr = build_bsr(mask, plan.block_m, plan.block_n);
         else ctx.rw = build_rowwise(mask);
         return ctx;
     }
+    // `mask` must be the strided(band) mask (generate_mask of one "strided" descriptor): exec_mha
+    // then runs the decomposed executor instead of the plan's
+    static MhaContext make_strided(const DenseMask& mask, const KernelPlan& plan, int32_t band) {
+        MhaContext ctx = make(mask, plan);
+        MaskDescriptor d{"causal_local", mask.seq_len(), {}};
+        d.params.band_width = band;
+        ctx.band_bsr = build_bsr(generate_mask(d), 128, 16);
+        ctx.strided_band = band;
+        return ctx;
+    }
 };
+
+namespace detail {
+// the executor a context runs (exec_mha's dispatch): decomposed strided, block-wise or row-wise
+inline void run_mha(const MhaContext& ctx, const sf_attn_args& a, cudaStream_t st) {
+    if (ctx.strided_band > 0) check(sf_mha_strided(&a, ctx.strided_band, &ctx.band_bsr->device->d, st));
+    else if (ctx.plan.kind == KernelKind::BlockWise) check(sf_mha_blockwise(&a, &ctx.bsr->device->d, nullptr, nullptr, st));
+    else check(sf_mha_rowwise(&a, &ctx.rw->device->d, st));
+}
+}  // namespace detail
 
 namespace detail {
 inline DeviceBuffer<__half> to_dev_half(const std::vector<float>& v, cudaStream_t st = nullptr) {
@@ -222,8 +244,7 @@ public:
         if (mha_->mask.seq_len() != hy.seq_len) throw shape_error("MHA mask seq_len mismatch");
         sf_attn_args a{static_cast<int32_t>(hy.bs), hy.heads, static_cast<int32_t>(hy.seq_len), hy.head_size, SF_F16,
                        x, x, x, y, hy.seq_len * H, hy.head_size, H, hy.seq_len * H, hy.head_size, H, 0.f};
-        if (mha_->plan.kind == KernelKind::BlockWise) check(sf_mha_blockwise(&a, &mha_->bsr->device->d, nullptr, nullptr, st_));
-        else check(sf_mha_rowwise(&a, &mha_->rw->device->d, st_));
+        detail::run_mha(*mha_, a, st_);
     }
 
 private:
@@ -344,8 +365,7 @@ inline Matrix exec_mha(const OpNode& node, const GraphHyper& hyper, const MhaCon
     sf_attn_args a{static_cast<int32_t>(hyper.bs), hyper.heads, static_cast<int32_t>(hyper.seq_len), hyper.head_size, SF_F16,
                    x.data(), x.data(), x.data(), y.data(), hyper.seq_len * H, hyper.head_size, H, hyper.seq_len * H,
                    hyper.head_size, H, 0.f};
-    if (ctx.plan.kind == KernelKind::BlockWise) check(sf_mha_blockwise(&a, &ctx.bsr->device->d, nullptr, nullptr, st));
-    else check(sf_mha_rowwise(&a, &ctx.rw->device->d, st));
+    detail::run_mha(ctx, a, st);
     return detail::to_host(y.data(), in.rows, in.cols, st);
 }
 

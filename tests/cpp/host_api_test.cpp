@@ -273,7 +273,7 @@ static std::vector<char> read_file(const std::string& path) {
 }
 
 // exec-segment <model> <bs> <seq> <hidden> <heads> <head_size> <seed> <seg_begin> <seg_end> <in.f32>
-//              <out.f32> [<mask.u8> <bm> <bn>]
+//              <out.f32> [<mask.u8> <bm> <bn> [<strided band>]]
 // The reference-signature free functions (exec_segment / exec_mha with host Matrix in / out and an
 // MhaContext) on GraphData(seed); the Python test compares the output with the reference's own
 // exec_segment (oracle/_ref).
@@ -301,7 +301,8 @@ static int cmd_exec_segment(int argc, char** argv) {
         plan.kind = KernelKind::BlockWise;
         plan.block_m = std::atoi(argv[14]);
         plan.block_n = std::atoi(argv[15]);
-        ctx = MhaContext::make(m, plan);
+        // a strided(band) mask may be run by the decomposed executor (MhaContext::make_strided)
+        ctx = argc >= 17 ? MhaContext::make_strided(m, plan, std::atoi(argv[16])) : MhaContext::make(m, plan);
     }
     const Matrix y = exec_segment(g, gd, ctx ? &*ctx : nullptr, seg, default_setting(classify_segment(seg, g)), x);
     std::FILE* f = std::fopen(argv[12], "wb");
