@@ -69,4 +69,18 @@ r = (r - r.mean(1, keepdim=True)) / torch.sqrt(r.var(1, unbiased=False, keepdim=
 err = (y.float() - r).abs().max().item()
 print(f"gemm chain max_abs {err:.2e}")
 assert err < 5e-2
+# decomposed strided executor (strided.cu): band part on tcgen05 with LSE, class part on mma.sync, merge
+ts = [dict(pattern="strided", seq_len=2048, band_width=32)]
+ms = o.mask(ts)
+qs, ks, vs = (x.astype(np.float16).astype(np.float32) for x in o.random_attention_input(1, 2, 2048, d, 2))
+refs, _ = o.block_sparse_sdpa(qs, ks, vs, ms, 128, 16, threads=8)
+Qs, Ks, Vs = (torch.from_numpy(x).cuda().half() for x in (qs, ks, vs))
+w_band = sf.strided_band(ts)
+assert w_band == 32, w_band
+bb = sf.build_bsr(sf.generate_mask([dict(pattern="causal_local", seq_len=2048, band_width=32)]), 128, 16)
+out = sf.strided_sdpa(Qs, Ks, Vs, 32, bb)
+torch.cuda.synchronize()
+err = np.abs(out.float().cpu().numpy() - refs).max()
+print(f"strided max_abs {err:.2e}")
+assert err < 2e-2
 print("sanitize_once ok")
