@@ -272,7 +272,7 @@ def run_sweep(args):
             dm = sf.generate_mask(sweep_terms(pat, n))
             nnz = dm.true_count()
             plan = sf.select_plan(dm, sf.hw_preset("b200"), n, h, bs, d, mode="b200")  # the job's plan
-            ctx = sf.MhaContext(dm, plan, strided_band=sf.strided_band(sweep_terms(pat, n)))
+            ctx = sf.context_for(sweep_terms(pat, n), dm, plan)
             run = lambda: sf.mha(q, k, v, ctx, out=o)
             for _ in range(3):
                 run()
@@ -567,7 +567,7 @@ def main():
     dm = sf.generate_mask(cfg["mask"])
     nnz = dm.true_count()
     plan = sf.select_plan(dm, sf.hw_preset("b200"), s.seq_len, s.heads, s.bs, s.head_size, mode="b200")
-    ctx = sf.MhaContext(dm, plan, strided_band=sf.strided_band(cfg["mask"]))
+    ctx = sf.context_for(cfg["mask"], dm, plan)
     W = layer.init_weights(cfg["model"], s, seed=1)  # one model: the same weights on every rank
     L = layer.EncoderLayer(cfg["model"], s, W, ctx, ln_split=args.ln_split)
     g = torch.Generator(device="cuda").manual_seed(7)

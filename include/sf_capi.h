@@ -108,6 +108,10 @@ sf_status sf_mask_deserialize(const uint8_t* buf, int64_t nbytes, int32_t* seq_l
  * (mask.hpp:146-166) when they are not all descriptor-generated. */
 sf_status sf_mask_or(const uint32_t* d_src, uint32_t* d_acc, int32_t seq_len, void* stream);
 
+/* d_acc &= ~d_src over n rows: the cells of one mask not covered by another (mask decomposition,
+ * sf_mha_dilated's rest). No reference counterpart. */
+sf_status sf_mask_andnot(const uint32_t* d_src, uint32_t* d_acc, int32_t seq_len, void* stream);
+
 /* Valid-cell count of a device bit mask (DenseMask::true_count, mask.hpp:39-43). Synchronizes. */
 sf_status sf_mask_count(const uint32_t* d_bits, int32_t seq_len, int64_t* count, void* stream);
 
@@ -275,6 +279,16 @@ sf_status sf_mha_rowwise(const sf_attn_args* args, const sf_csr_dev* csr, void* 
  * sf_mha_blockwise over the strided mask (attention.hpp:71-172). Needs head_size 64 and
  * ceil(seq_len / w) <= 128, else SF_PLAN_ERROR. */
 sf_status sf_mha_strided(const sf_attn_args* args, int32_t band_width, const sf_bsr_dev* band_bsr, void* stream);
+
+/* block_sparse_sdpa (attention.hpp:71-172) over a mask containing dilated(w, r) (mask.hpp:89-103),
+ * by decomposition: dilated(w, r) pairs only rows and keys of one residue class mod s = r + 1, and
+ * inside a class it is sliding(w) (mask.hpp:74-84) over n / s rows. Each class runs the tcgen05
+ * block executor on the tensors' rows p, p + s, ... with class_bsr = build_bsr(sliding(w) over
+ * n / s rows, 128, bn); rest_bsr (NULL or empty: none) = build_bsr(mask AND NOT dilated(w, r), 128, bn)
+ * runs over the full rows, and the two parts are merged per row by log-sum-exp. Needs n % s == 0,
+ * head_size 64, block_m 128 BSRs. SF_PLAN_ERROR otherwise (no launch). */
+sf_status sf_mha_dilated(const sf_attn_args* args, int32_t stride, const sf_bsr_dev* class_bsr,
+                         const sf_bsr_dev* rest_bsr, void* stream);
 
 /* Dense masked SDPA reference on the device (dense_sdpa_oracle, attention.hpp:15-56): reads the
  * DENSE bit mask (sf_mask_generate's layout), accumulates in fp64 with the reference's exact

@@ -102,6 +102,10 @@ struct MhaContext {
     // strided(w) masks executed by decomposition (sf_mha_strided): the causal-local(w) band's BSR
     int32_t strided_band = 0;
     std::optional<BsrMask> band_bsr;
+    // dilated(w, r) masks executed by class decomposition (sf_mha_dilated): the sliding(w) BSR of
+    // n / (r + 1) rows, and the BSR of the rest of the mask (empty when the mask is the dilated term)
+    int32_t dilated_stride = 0;
+    std::optional<BsrMask> class_bsr, rest_bsr;
 
     static MhaContext make(const DenseMask& mask, const KernelPlan& plan) {
         MhaContext ctx{mask, plan, {}, {}, 0, {}};
@@ -119,12 +123,34 @@ struct MhaContext {
         ctx.strided_band = band;
         return ctx;
     }
+    // `mask` holds the dilated(band, rate) term (generate_mask of it, possibly OR-ed with others):
+    // exec_mha runs the class decomposition, the rest of the mask merged by log-sum-exp
+    static MhaContext make_dilated(const DenseMask& mask, const KernelPlan& plan, int32_t band, int32_t rate) {
+        const int n = mask.seq_len(), s = rate + 1;
+        if (rate < 1 || band < 1 || n % s) throw invalid_parameter("make_dilated: rate >= 1, band >= 1, seq_len % (rate + 1) == 0");
+        MhaContext ctx = make(mask, plan);
+        MaskDescriptor cd{"sliding", n / s, {}};
+        cd.params.band_width = std::min(band, n / s);
+        ctx.class_bsr = build_bsr(generate_mask(cd), 128, 16);
+        MaskDescriptor dd{"dilated", n, {}};
+        dd.params.band_width = band;
+        dd.params.dilation_rate = rate;
+        DenseMask rest(mask);
+        check(sf_mask_andnot(generate_mask(dd).device_bits(), rest.mutable_device_bits(), n, nullptr));
+        BsrMask rb = build_bsr(rest, 128, 16);
+        if (rb.device->d.n_load > 0) ctx.rest_bsr = std::move(rb);
+        ctx.dilated_stride = s;
+        return ctx;
+    }
 };
 
 namespace detail {
-// the executor a context runs (exec_mha's dispatch): decomposed strided, block-wise or row-wise
+// the executor a context runs (exec_mha's dispatch): decomposed strided / dilated, block-wise or row-wise
 inline void run_mha(const MhaContext& ctx, const sf_attn_args& a, cudaStream_t st) {
     if (ctx.strided_band > 0) check(sf_mha_strided(&a, ctx.strided_band, &ctx.band_bsr->device->d, st));
+    else if (ctx.dilated_stride > 0)
+        check(sf_mha_dilated(&a, ctx.dilated_stride, &ctx.class_bsr->device->d,
+                             ctx.rest_bsr ? &ctx.rest_bsr->device->d : nullptr, st));
     else if (ctx.plan.kind == KernelKind::BlockWise) check(sf_mha_blockwise(&a, &ctx.bsr->device->d, nullptr, nullptr, st));
     else check(sf_mha_rowwise(&a, &ctx.rw->device->d, st));
 }

@@ -112,6 +112,7 @@ SIGNATURES = {
     "sf_mask_pack_u8": (C.c_int, [_P, _I32, _P, _P]),
     "sf_mask_count": (C.c_int, [_P, _I32, C.POINTER(_I64), _P]),
     "sf_mask_or": (C.c_int, [_P, _P, _I32, _P]),
+    "sf_mask_andnot": (C.c_int, [_P, _P, _I32, _P]),
     "sf_bsr_build": (C.c_int, [_P, _I32, _I32, _I32, C.POINTER(BsrDev), _P]),
     "sf_bsr_free": (C.c_int, [C.POINTER(BsrDev), _P]),
     "sf_bsr_to_host": (C.c_int, [C.POINTER(BsrDev)] + [_P] * 8 + [_P]),
@@ -134,6 +135,7 @@ SIGNATURES = {
     "sf_mha_blockwise": (C.c_int, [C.POINTER(AttnArgs), C.POINTER(BsrDev), C.POINTER(Plan), C.POINTER(AttnStats), _P]),
     "sf_mha_rowwise": (C.c_int, [C.POINTER(AttnArgs), C.POINTER(CsrDev), _P]),
     "sf_mha_strided": (C.c_int, [C.POINTER(AttnArgs), _I32, C.POINTER(BsrDev), _P]),
+    "sf_mha_dilated": (C.c_int, [C.POINTER(AttnArgs), _I32, C.POINTER(BsrDev), C.POINTER(BsrDev), _P]),
     "sf_mha_dense_oracle": (C.c_int, [C.POINTER(AttnArgs), _P, _P, _P]),
     "sf_set_attn_impl": (C.c_int, [_I32]),
     "sf_set_pdl": (C.c_int, [_I32]),

@@ -253,6 +253,10 @@ __global__ void or_kernel(const uint32_t* __restrict__ src, uint32_t* __restrict
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i < total) acc[i] |= src[i];
 }
+__global__ void andnot_kernel(const uint32_t* __restrict__ src, uint32_t* __restrict__ acc, int64_t total) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < total) acc[i] &= ~src[i];
+}
 }  // namespace
 }  // namespace sf
 
@@ -260,6 +264,14 @@ extern "C" sf_status sf_mask_or(const uint32_t* d_src, uint32_t* d_acc, int32_t 
     if (seq_len <= 0) return fail(SF_INVALID_PARAMETER, "seq_len must be positive");
     const int64_t total = static_cast<int64_t>(seq_len) * sf_mask_words(seq_len);
     or_kernel<<<static_cast<unsigned>(ceil_div(total, 256)), 256, 0, as_stream(stream)>>>(d_src, d_acc, total);
+    SF_LAUNCH_CHECK();
+    return SF_OK;
+}
+
+extern "C" sf_status sf_mask_andnot(const uint32_t* d_src, uint32_t* d_acc, int32_t seq_len, void* stream) {
+    if (seq_len <= 0) return fail(SF_INVALID_PARAMETER, "seq_len must be positive");
+    const int64_t total = static_cast<int64_t>(seq_len) * sf_mask_words(seq_len);
+    andnot_kernel<<<static_cast<unsigned>(ceil_div(total, 256)), 256, 0, as_stream(stream)>>>(d_src, d_acc, total);
     SF_LAUNCH_CHECK();
     return SF_OK;
 }

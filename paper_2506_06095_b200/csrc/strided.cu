@@ -262,6 +262,7 @@ extern "C" sf_status sf_mha_strided(const sf_attn_args* args, int32_t band_width
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * kMaxClassRows * 128);
         if (e == cudaSuccess) e = launch_pdl(kern, grid, dim3(32 * warps), smem, st, nullptr, p);
         if (e != cudaSuccess) status = fail(SF_CUDA_ERROR, std::string("strided class kernel: ") + cudaGetErrorString(e));
+        else note_launch();
     }
     cudaFreeAsync(lse, st);
     return status;

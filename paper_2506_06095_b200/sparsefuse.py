@@ -460,6 +460,11 @@ def dense_sdpa_oracle(q, k, v, mask: "DenseMask", stream=None) -> torch.Tensor:
     return o64
 
 
+# below this length the block executor over the whole dilated mask is as fast (bs16 x 12 heads,
+# dilated(sqrt n, 1): n 2048 66 vs 68 us, n 4096 144 vs 120 us, n 8192 363 vs 265 us; tools/dilated_time.py)
+DILATED_MIN_SEQ = 4096
+
+
 def strided_sdpa(q, k, v, band_width: int, band_bsr: BsrMask, out=None, stream=None):
     """Masked MHA over the strided(w) mask by decomposition (sf_mha_strided): the causal-local(w)
     band on the tcgen05 block kernel (band_bsr: its block_m 128 BSR) plus the i - j = k w diagonals
@@ -485,11 +490,53 @@ def strided_band(terms) -> Optional[int]:
     return int(t.band_width)
 
 
+def mask_andnot(mask: DenseMask, minus: DenseMask, stream=None) -> DenseMask:
+    """The cells of `mask` not in `minus` (sf_mask_andnot), as a new device mask."""
+    if mask.seq_len != minus.seq_len:
+        raise _lib.ShapeError("mask_andnot: seq_len differs")
+    out = DenseMask(mask.seq_len, mask.bits.clone())
+    check(lib().sf_mask_andnot(minus.bits.data_ptr(), out.bits.data_ptr(), mask.seq_len, _stream(stream)))
+    return out
+
+
+def dilated_sdpa(q, k, v, stride: int, class_bsr: BsrMask, rest_bsr: Optional[BsrMask] = None, out=None,
+                 stream=None):
+    """Masked MHA over a mask holding dilated(w, r) by decomposition (sf_mha_dilated): each residue
+    class mod stride = r + 1 is a sliding(w) band over n / stride rows (class_bsr: its block_m 128
+    BSR, shared by the classes) on the tcgen05 block kernel; rest_bsr (the mask minus the dilated
+    cells, or None) runs over the full rows and the parts merge per row by log-sum-exp. Same
+    semantics as block_sparse_sdpa over the whole mask (attention.hpp:71-172)."""
+    o = out if out is not None else torch.empty_like(q)
+    a = attn_args(q, k, v, o)
+    rest = C.byref(rest_bsr.dev) if rest_bsr is not None else None
+    check(lib().sf_mha_dilated(C.byref(a), int(stride), C.byref(class_bsr.dev), rest, _stream(stream)))
+    return o
+
+
+def dilated_split(terms, min_seq_len: int = DILATED_MIN_SEQ, allow_rest: bool = False) -> Optional[tuple]:
+    """(stride, band_width) when the descriptor holds one dilated(w, r >= 1) term, seq_len % (r + 1)
+    == 0 and seq_len >= min_seq_len; else None. Other terms (the decomposition's rest) only with
+    allow_rest: a rest with global rows is slower than the block executor over the whole mask (its
+    global row blocks are single 64-step items; T5 cfg4: 170 vs 115 us, tools/dilated_time.py)."""
+    ts = terms if isinstance(terms, (list, tuple)) else [terms]
+    ds = [t if isinstance(t, MaskDescriptor) else MaskDescriptor(**t) for t in ts]
+    dil = [t for t in ds if t.pattern == "dilated"]
+    if len(dil) != 1 or (len(ds) > 1 and not allow_rest):
+        return None
+    t = dil[0]
+    s = int(t.dilation_rate) + 1
+    if s < 2 or t.band_width < 1 or t.seq_len % s or t.seq_len < min_seq_len:
+        return None
+    return s, int(t.band_width)
+
+
 def executor_label(ctx) -> list:
-    """The executor a context runs, as reported by the bench: [kind, block_m, block_n] or
-    ["strided_decomposed", band_width, 0]."""
+    """The executor a context runs, as reported by the bench: [kind, block_m, block_n],
+    ["strided_decomposed", band_width, 0] or ["dilated_decomposed", stride, band_width]."""
     if getattr(ctx, "strided_band", None):
         return ["strided_decomposed", int(ctx.strided_band), 0]
+    if getattr(ctx, "dilated", None):
+        return ["dilated_decomposed", int(ctx.dilated[0]), int(ctx.dilated[1])]
     return [ctx.plan.kind, ctx.plan.block_m, ctx.plan.block_n]
 
 
@@ -498,14 +545,25 @@ class MhaContext:
     strided_band=w (a mask that is one strided(w) descriptor, see strided_band()): the unified MHA
     runs the decomposed strided executor (band BSR built here) instead of the plan's executor."""
 
-    def __init__(self, mask: DenseMask, plan: KernelPlan, stream=None, strided_band: Optional[int] = None):
+    def __init__(self, mask: DenseMask, plan: KernelPlan, stream=None, strided_band: Optional[int] = None,
+                 dilated: Optional[tuple] = None):
         self.mask = mask
         self.plan = plan
         self.strided_band = strided_band
+        self.dilated = tuple(dilated) if dilated else None
         self.band_bsr = None
+        self.class_bsr = self.rest_bsr = None
         if strided_band:
             band = generate_mask([dict(pattern="causal_local", seq_len=mask.seq_len, band_width=strided_band)], stream)
             self.band_bsr = build_bsr(band, 128, 16, stream)
+        elif self.dilated:  # (stride, w) from dilated_split(): class band + the rest of the mask
+            s, w = self.dilated
+            n = mask.seq_len
+            band = generate_mask([dict(pattern="sliding", seq_len=n // s, band_width=min(w, n // s))], stream)
+            self.class_bsr = build_bsr(band, 128, 16, stream)
+            dil = generate_mask([dict(pattern="dilated", seq_len=n, band_width=w, dilation_rate=s - 1)], stream)
+            rest = build_bsr(mask_andnot(mask, dil, stream), 128, 16, stream)
+            self.rest_bsr = rest if rest.dev.n_load > 0 else None
         if plan.kind == "block_wise":
             self.bsr = build_bsr(mask, plan.block_m, plan.block_n, stream)
             self.csr = None
@@ -514,11 +572,23 @@ class MhaContext:
             self.csr = build_rowwise(mask, stream)
 
 
+def context_for(terms, mask: DenseMask, plan: KernelPlan, stream=None) -> MhaContext:
+    """The MhaContext the unified MHA should run for a session mask given by its descriptor terms:
+    the decomposed strided executor for one strided(w) term, the class decomposition for one
+    dilated(w, r) term, else the plan's executor (strided_band(), dilated_split())."""
+    sb = strided_band(terms)
+    if sb:
+        return MhaContext(mask, plan, stream, strided_band=sb)
+    return MhaContext(mask, plan, stream, dilated=dilated_split(terms))
+
+
 def mha(q, k, v, ctx: MhaContext, out=None, stream=None):
     """Unified MHA entry: dispatches the row-wise or block-wise executor from the plan (or the
     decomposed strided executor when the context carries a strided band)."""
     if ctx.strided_band:
         return strided_sdpa(q, k, v, ctx.strided_band, ctx.band_bsr, out=out, stream=stream)
+    if ctx.dilated:
+        return dilated_sdpa(q, k, v, ctx.dilated[0], ctx.class_bsr, ctx.rest_bsr, out=out, stream=stream)
     if ctx.plan.kind == "block_wise":
         return block_sparse_sdpa(q, k, v, ctx.bsr, ctx.plan, out=out, stream=stream)
     return rowwise_sdpa(q, k, v, ctx.csr, out=out, stream=stream)

@@ -301,8 +301,15 @@ static int cmd_exec_segment(int argc, char** argv) {
         plan.kind = KernelKind::BlockWise;
         plan.block_m = std::atoi(argv[14]);
         plan.block_n = std::atoi(argv[15]);
-        // a strided(band) mask may be run by the decomposed executor (MhaContext::make_strided)
-        ctx = argc >= 17 ? MhaContext::make_strided(m, plan, std::atoi(argv[16])) : MhaContext::make(m, plan);
+        // a strided(band) mask may be run by the decomposed executor (MhaContext::make_strided), a
+        // mask holding dilated(band, rate) by the class decomposition ("dil:<band>:<rate>", make_dilated)
+        if (argc >= 17 && std::strncmp(argv[16], "dil:", 4) == 0) {
+            int band = 0, rate = 0;
+            REQUIRE(std::sscanf(argv[16], "dil:%d:%d", &band, &rate) == 2);
+            ctx = MhaContext::make_dilated(m, plan, band, rate);
+        } else {
+            ctx = argc >= 17 ? MhaContext::make_strided(m, plan, std::atoi(argv[16])) : MhaContext::make(m, plan);
+        }
     }
     const Matrix y = exec_segment(g, gd, ctx ? &*ctx : nullptr, seg, default_setting(classify_segment(seg, g)), x);
     std::FILE* f = std::fopen(argv[12], "wb");

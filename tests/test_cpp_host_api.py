@@ -80,6 +80,7 @@ SEGMENT_CASES = [  # (graph, segment, template) at bs 2, seq 256, hidden 256, 4 
     ("spec:l,g256,b,r", (0, 4), "CiMi with a LayerNorm prologue"),
     ("bert-layer", (0, 1), "MhaFused unit (exec_mha), BigBird mask, BSR 128x16"),
     ("bert-layer", (0, 1), "MhaFused unit (exec_mha), strided(16) mask, decomposed executor"),
+    ("t5-layer", (1, 2), "MhaFused unit (exec_mha), dilated(16,1)+global(16) mask, class decomposition"),
 ]
 
 
@@ -99,11 +100,18 @@ def test_exec_segment_matches_reference(reference, tmp_path, model, seg, what):
     extra = []
     if "Mha" in what:
         from oracle.oracle import Oracle
-        terms = ([dict(pattern="strided", seq_len=seq, band_width=16)] if "strided" in what else
-                 [dict(pattern="bigbird", seq_len=seq, global_width=16, band_width=16, filling_rate=0.1, seed=2)])
+        if "strided" in what:
+            terms, tail = [dict(pattern="strided", seq_len=seq, band_width=16)], ["16"]
+        elif "dilated" in what:
+            terms = [dict(pattern="dilated", seq_len=seq, band_width=16, dilation_rate=1),
+                     dict(pattern="global", seq_len=seq, global_width=16)]
+            tail = ["dil:16:1"]
+        else:
+            terms = [dict(pattern="bigbird", seq_len=seq, global_width=16, band_width=16, filling_rate=0.1, seed=2)]
+            tail = []
         mask = Oracle().mask(terms)
         (tmp_path / "m.u8").write_bytes(mask.astype(np.uint8).tobytes())
-        extra = [str(tmp_path / "m.u8"), "128", "16"] + (["16"] if "strided" in what else [])
+        extra = [str(tmp_path / "m.u8"), "128", "16"] + tail
     (tmp_path / "x.f32").write_bytes(x.tobytes())
     r = subprocess.run([_bin(), "exec-segment", model, str(bs), str(seq), str(hid), str(heads), str(hs), str(seed),
                         str(seg[0]), str(seg[1]), str(tmp_path / "x.f32"), str(tmp_path / "y.f32")] + extra,
