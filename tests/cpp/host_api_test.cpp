@@ -168,7 +168,7 @@ static int cmd_gpu_basics() {
     REQUIRE(p.kind == KernelKind::BlockWise && p.block_m == 16 && p.block_n == 16 && p.num_warps == 4);
     REQUIRE(std::isnan(select_plan(DenseMask(16, true), hw_preset("a100"), 16, 12, 8, 64).threshold));
     const auto pb = select_plan(gen_bigbird(1024, 32, 32, 0.1, 0), hw_preset("b200"), 1024, 12, 16, 64, PlanMode::B200);
-    REQUIRE(pb.kind == KernelKind::BlockWise && pb.block_m == 128);
+    REQUIRE(pb.kind == KernelKind::BlockWise && pb.block_m == 64 && pb.block_n == 16);  // head pairs for BigBird
     // test_attention.cpp-style, through the host-tensor signatures
     {
         const auto in = random_attention_input<float>(2, 2, 16, 8, 1);

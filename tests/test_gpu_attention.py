@@ -180,7 +180,10 @@ def test_unified_mha_dispatch(sf, oracle):
     wide = sf.generate_mask([dict(pattern="bigbird", seq_len=1024, global_width=32, band_width=32,
                                   filling_rate=0.1, seed=0)])
     plan = sf.select_plan(wide, sf.hw_preset("b200"), 1024, 12, 16, 64, mode="b200")
-    assert plan.kind == "block_wise" and plan.block_m == 128
+    # BigBird's 16-row random blocks: 64-row blocks (head pairs) execute 0.67x the cells
+    assert plan.kind == "block_wise" and (plan.block_m, plan.block_n) == (64, 16), plan
+    band = sf.select_plan(sf.gen_sliding_window(4096, 64), sf.hw_preset("b200"), 4096, 12, 16, 64, mode="b200")
+    assert band.kind == "block_wise" and band.block_m == 128, band  # wide band: 0.75x cells, slower as pairs
 
 
 def test_b200_selector_calibration(sf):
@@ -191,7 +194,8 @@ def test_b200_selector_calibration(sf):
     ref = sf.select_plan(dm, sf.hw_preset("b200"), 2048, 12, 16, 64, mode="reference")
     assert ref.kind == "row_wise" and ref.threshold < 0
     b200 = sf.select_plan(dm, sf.hw_preset("b200"), 2048, 12, 16, 64, mode="b200")
-    assert b200.kind == "block_wise" and (b200.block_m, b200.block_n) == (128, 16)
+    # block_m 64 (head pairs): a 16-wide band executes 0.60x the cells of 128-row blocks
+    assert b200.kind == "block_wise" and (b200.block_m, b200.block_n) == (64, 16)
     assert b200.threshold == ref.threshold
     small = sf.select_plan(sf.gen_sliding_window(2048, 4), sf.hw_preset("b200"), 2048, 2, 1, 64, mode="b200")
     assert small.kind == "row_wise"
