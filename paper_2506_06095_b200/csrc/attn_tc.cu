@@ -68,6 +68,11 @@ struct AttnGeo {
 
 struct AttnParams {
     CUtensorMap tq, tk, tv;  // 4-D (d, n, h, b) maps; boxes {64,128,1,1} / {64,bn,1,1}
+    // head pairs (BM 64) with pair5: 5-D K / V maps (d, row % 8, h, row / 8, b), box {64, 8, 2, bn / 8, 1}:
+    // ONE box per column block carries both heads' rows as [row / 8][head][8 rows][128 B], so head
+    // t's swizzle atoms sit at t * 1 KB + a 2 KB stride (half the boxes of one box per head)
+    CUtensorMap tk2, tv2;
+    int32_t pair5;
     int32_t n, h, bh, n_rows, n_items;  // bh: work units per row block (slices, or head pairs at BM 64)
     int32_t bh_total;                   // b * h slices
     const int32_t* load_row_ptr;
@@ -153,6 +158,10 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
         tc::prefetch_tmap(&p.tq);
         tc::prefetch_tmap(&p.tk);
         tc::prefetch_tmap(&p.tv);
+        if (kPair && p.pair5) {
+            tc::prefetch_tmap(&p.tk2);
+            tc::prefetch_tmap(&p.tv2);
+        }
         for (int i = 0; i < 2; ++i) {
             tc::mbar_init(&q_full[i], 1);
             tc::mbar_init(&q_empty[i], 1);
@@ -268,10 +277,15 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
                     __syncwarp();
                     if (lane < G) {
                         const int gg = static_cast<int>(lane);
+                        if (kPair && p.pair5) {
+                            tma_load_5d(sK + st * kKVBytes + gg * BN * kD * 2 * 2, &p.tk2, &k_full[st], 0, 0, hh2[0],
+                                        gcol * (BN / 8), hb[0]);
+                        } else {
 #pragma unroll
-                        for (int t = 0; t < Geo::kHeads; ++t)  // head t's 64 keys at t * 8 KB
-                            tma_load_4d(sK + st * kKVBytes + t * (kNS * kD * 2) + gg * BN * kD * 2, &p.tk, &k_full[st], 0,
-                                        gcol * BN, hh2[t], hb[t]);
+                            for (int t = 0; t < Geo::kHeads; ++t)  // head t's 64 keys at t * 8 KB
+                                tma_load_4d(sK + st * kKVBytes + t * (kNS * kD * 2) + gg * BN * kD * 2, &p.tk, &k_full[st],
+                                            0, gcol * BN, hh2[t], hb[t]);
+                        }
                         if (gtile >= 0)
                             tc::bulk_load(sMask + st * kMaskBytes + gg * TB, p.pool + static_cast<int64_t>(gtile) * TB, TB,
                                           &k_full[st]);
@@ -285,10 +299,15 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
                     __syncwarp();
                     if (lane < G) {
                         const int gg = static_cast<int>(lane);
+                        if (kPair && p.pair5) {
+                            tma_load_5d(sV + st * kKVBytes + gg * BN * kD * 2 * 2, &p.tv2, &v_full[st], 0, 0, hh2[0],
+                                        gcol * (BN / 8), hb[0]);
+                        } else {
 #pragma unroll
-                        for (int t = 0; t < Geo::kHeads; ++t)
-                            tma_load_4d(sV + st * kKVBytes + t * (kNS * kD * 2) + gg * BN * kD * 2, &p.tv, &v_full[st], 0,
-                                        gcol * BN, hh2[t], hb[t]);
+                            for (int t = 0; t < Geo::kHeads; ++t)
+                                tma_load_4d(sV + st * kKVBytes + t * (kNS * kD * 2) + gg * BN * kD * 2, &p.tv, &v_full[st],
+                                            0, gcol * BN, hh2[t], hb[t]);
+                        }
                     }
                 }
             }
@@ -316,11 +335,13 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
 #pragma unroll
                 for (int t = 0; t < Geo::kHeads; ++t) {  // head t: M = BM rows at TMEM lane offset 16t
                     const uint32_t q0 = tc::smem_u32(sQ + (cs.qi & 1) * kQBytes + t * (BM * kD * 2));
-                    const uint32_t k0 = tc::smem_u32(sK + s * kKVBytes + t * (kNS * kD * 2));
+                    const bool p5 = kPair && p.pair5;
+                    const uint32_t k0 = tc::smem_u32(sK + s * kKVBytes) + (p5 ? 1024u * t : static_cast<uint32_t>(t * (kNS * kD * 2)));
+                    const uint32_t kv_sbo = p5 ? 2048u : 1024u;
 #pragma unroll
                     for (int k = 0; k < kD / 16; ++k)
                         tc::mma_f16_ss(tmem + ((16u * t) << 16) + 64 * (gS % kSBuf), tc::sdesc_sw128(q0 + 32 * k),
-                                       tc::sdesc_sw128(k0 + 32 * k), idesc_s, k != 0);
+                                       sdesc_sw128_sbo(k0 + 32 * k, kv_sbo), idesc_s, k != 0);
                 }
                 tc::mma_commit(&s_full[gS % kSBuf]);
                 if (cs.j == cs.ns - 1) tc::mma_commit(&q_empty[cs.qi & 1]);  // last S of the item: Q free
@@ -337,11 +358,13 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
                 tc::fence_after_sync();
 #pragma unroll
                 for (int t = 0; t < Geo::kHeads; ++t) {
-                    const uint32_t v0 = tc::smem_u32(sV + s * kKVBytes + t * (kNS * kD * 2));
+                    const bool p5 = kPair && p.pair5;
+                    const uint32_t v0 = tc::smem_u32(sV + s * kKVBytes) + (p5 ? 1024u * t : static_cast<uint32_t>(t * (kNS * kD * 2)));
+                    const uint32_t kv_sbo = p5 ? 2048u : 1024u;
                     const uint32_t lo = (16u * t) << 16;
 #pragma unroll
                     for (int k = 0; k < kNS / 16; ++k)  // P_g: 64 keys = 32 packed columns, 8 per K=16
-                        tc::mma_f16_ts(tO + lo, tmem + lo + kPCol + 32 * sb + 8 * k, tc::sdesc_sw128_mn(v0 + 2048 * k),
+                        tc::mma_f16_ts(tO + lo, tmem + lo + kPCol + 32 * sb + 8 * k, sdesc_sw128_sbo(v0 + 2 * kv_sbo * k, kv_sbo),
                                        idesc_o, (cp.j | k) != 0);
                 }
                 tc::mma_commit(&o_full[g & 1]);
@@ -592,6 +615,31 @@ sf_status make_tmap_4d(CUtensorMap* map, const void* base, int n, int h, int bs,
     return SF_OK;
 }
 
+// Head-pair K / V map: 5-D (d, row % 8, h, row / 8, b) with byte strides (sn, sh, 8 sn, sb) (x 2 B),
+// box {64, 8, 2, bn / 8, 1}, SW128 (n % 8 == 0).
+sf_status make_tmap_pair5(CUtensorMap* map, const void* base, int n, int h, int bs, int64_t sn, int64_t sh, int64_t sb,
+                          uint32_t bn, bool bf16) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+        cudaDriverEntryPointQueryResult q{};
+        void* fn = nullptr;
+        SF_CUDA_TRY(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+        if (!fn || q != cudaDriverEntryPointSuccess) return fail(SF_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
+        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    const cuuint64_t dims[5] = {static_cast<cuuint64_t>(kD), 8, static_cast<cuuint64_t>(h), static_cast<cuuint64_t>(n / 8),
+                                static_cast<cuuint64_t>(bs)};
+    const cuuint64_t strides[4] = {static_cast<cuuint64_t>(sn * 2), static_cast<cuuint64_t>(sh * 2),
+                                   static_cast<cuuint64_t>(sn * 16), static_cast<cuuint64_t>(sb * 2)};
+    const cuuint32_t box[5] = {static_cast<cuuint32_t>(kD), 8, 2, bn / 8, 1};
+    const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+    CUresult r = encode(map, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 5,
+                        const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(SF_CUDA_ERROR, "cuTensorMapEncodeTiled (head pair) failed: " + std::to_string(int(r)));
+    return SF_OK;
+}
+
 }  // namespace
 
 unsigned long long* g_attn_trace = nullptr;
@@ -685,6 +733,16 @@ sf_status attn_tc(const sf_attn_args& a, const sf_bsr_dev& b, cudaStream_t st, b
     SF_TRY(make_tmap_4d(&p.tq, a.q, a.seq_len, a.h, a.bs, a.q_sn, a.q_sh, a.q_sb, b.block_m, bf));
     SF_TRY(make_tmap_4d(&p.tk, a.k, a.seq_len, a.h, a.bs, a.q_sn, a.q_sh, a.q_sb, b.block_n, bf));
     SF_TRY(make_tmap_4d(&p.tv, a.v, a.seq_len, a.h, a.bs, a.q_sn, a.q_sh, a.q_sb, b.block_n, bf));
+    // head pairs with an even head count (a pair never straddles two sequences) and rows a multiple
+    // of 8: both heads of a column block in one 5-D box
+    if (b.block_m == 64 && a.h % 2 == 0 && a.seq_len % 8 == 0) {
+        const char* e = std::getenv("SF_ATTN_PAIR5");
+        if (!(e && *e == '0')) {
+            SF_TRY(make_tmap_pair5(&p.tk2, a.k, a.seq_len, a.h, a.bs, a.q_sn, a.q_sh, a.q_sb, b.block_n, bf));
+            SF_TRY(make_tmap_pair5(&p.tv2, a.v, a.seq_len, a.h, a.bs, a.q_sn, a.q_sh, a.q_sb, b.block_n, bf));
+            p.pair5 = 1;
+        }
+    }
     p.n = a.seq_len;
     p.h = a.h;
     p.bh_total = a.bs * a.h;

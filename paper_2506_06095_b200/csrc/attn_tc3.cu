@@ -78,16 +78,6 @@ struct Attn3Params {
     } while (0)
 #endif
 
-__device__ __forceinline__ uint64_t sdesc_sw128_sbo(uint32_t smem_addr, uint32_t sbo) {
-    uint64_t d = 0;
-    d |= static_cast<uint64_t>((smem_addr >> 4) & 0x3FFFu);
-    d |= static_cast<uint64_t>(1u) << 16;
-    d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32;
-    d |= static_cast<uint64_t>(1u) << 46;
-    d |= static_cast<uint64_t>(2u) << 61;
-    return d;
-}
-
 // exp2 on the FMA pipe for 1 of every 8 pairs: this kernel is issue-bound (three softmax warps per
 // sub-partition), and the polynomial costs ~6.5 issue slots per element against MUFU's 2.5
 constexpr int kEmuPairs3 = 1;
@@ -102,15 +92,6 @@ __device__ __forceinline__ void wait3(uint64_t* bar, uint32_t parity) {
         "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
         "@!P1 bra WAIT_%=;\n\t}" ::"r"(tc::smem_u32(bar)),
         "r"(parity), "n"(200)
-        : "memory");
-}
-
-__device__ __forceinline__ void tma_load_5d(void* dst, const CUtensorMap* m, uint64_t* bar, int32_t c0, int32_t c1,
-                                            int32_t c2, int32_t c3, int32_t c4) {
-    asm volatile(
-        "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6, "
-        "%7}], [%2];" ::"r"(tc::smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(m)), "r"(tc::smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
         : "memory");
 }
 
