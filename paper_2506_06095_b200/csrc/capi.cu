@@ -36,7 +36,7 @@ namespace {
 // per row when rows average <= 32 keys, 0.65 ns with a warp per row) and ~6e10 valid cells/s.
 constexpr double kBlockCellsPerUs = 1.8e6;
 constexpr double kBlockFloorUs = 12.0;
-constexpr double kPairCellRatio = 0.68;  // block_m 64 when its executed cells < 0.68x block_m 128's
+constexpr double kPairCellRatio = 0.73;  // block_m 64 when its executed cells < 0.73x block_m 128's
 constexpr double kRowNnzPerUs = 6.0e4;
 constexpr double kRowFloorUs = 10.0;
 
@@ -234,10 +234,11 @@ extern "C" sf_status sf_select_plan(const uint32_t* d_bits, const sf_hw_spec* hw
             out->score = 0.0;
             out->fallback = 0;
         }
-        // block_m 64 (the tcgen05 kernel's head-pair mode: M = 64 tiles of two heads per work item)
-        // retires executed cells at 0.64-0.87x the rate of block_m 128, so it wins only where
-        // 64-row blocks execute clearly fewer cells: BigBird-like random blocks (cfg2: 0.67x the
-        // cells, 0.90x the time; n 8192: 0.64x / 0.82x), never causal or wide bands
+        // block_m 64 (the tcgen05 kernel's head-pair mode: M = 64 tiles of two heads per work item,
+        // one 5-D TMA box per column block for both heads) retires executed cells at 0.7-0.9x the
+        // rate of block_m 128, so it wins only where 64-row blocks execute clearly fewer cells:
+        // BigBird-like random blocks (cfg2: 0.67x the cells, 0.83x the time), narrow bands,
+        // longformer; never causal or wide bands (0.75-0.98x the cells, 1.04-1.08x the time)
         // (tools/bm_sweep.py, profiles/r02/bm_sweep.txt). SF_PLAN_PAIR=0 keeps block_m 128.
         const char* pe = std::getenv("SF_PLAN_PAIR");
         if (out->kind == SF_BLOCK_WISE && out->block_m == 128 && !(pe && *pe == '0')) {
