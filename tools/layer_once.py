@@ -12,7 +12,7 @@ iters = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 s = layer.LayerShape(cfg["bs"], cfg["seq"], cfg["hidden"], cfg["heads"], cfg["hidden"] // cfg["heads"])
 dm = sf.generate_mask(cfg["mask"])
 plan = sf.select_plan(dm, sf.hw_preset("b200"), s.seq_len, s.heads, s.bs, s.head_size, mode="b200")
-L = layer.EncoderLayer(cfg["model"], s, layer.init_weights(cfg["model"], s, seed=1), sf.MhaContext(dm, plan, strided_band=sf.strided_band(cfg["mask"])))
+L = layer.EncoderLayer(cfg["model"], s, layer.init_weights(cfg["model"], s, seed=1), sf.context_for(cfg["mask"], dm, plan))
 x = (torch.rand(s.rows, s.hidden, device="cuda") * 2 - 1).half()
 for _ in range(iters):
     L.forward(x)
