@@ -231,9 +231,9 @@ extern "C" sf_status sf_mha_strided(const sf_attn_args* args, int32_t band_width
     const sf_attn_args& a0 = *args;
     if (band_width < 1 || band_width > a0.seq_len) return fail(SF_INVALID_PARAMETER, "band_width must be in [1, seq_len]");
     if (band_bsr->seq_len != a0.seq_len) return fail(SF_SHAPE_ERROR, "band BSR seq_len differs from input");
-    if (a0.head_size != kDs || band_bsr->block_m != 128 ||
+    if (a0.head_size != kDs || (band_bsr->block_m != 128 && band_bsr->block_m != 64) ||
         (a0.seq_len + band_width - 1) / band_width > kMaxClassRows || static_cast<int64_t>(a0.bs) * a0.h > 65535)
-        return fail(SF_PLAN_ERROR, "strided decomposition needs head_size 64, a block_m 128 band BSR, "
+        return fail(SF_PLAN_ERROR, "strided decomposition needs head_size 64, a block_m 128 (or 64: head pairs) band BSR, "
                                    "ceil(seq_len / band_width) <= 128 and bs * h <= 65535");
     if ((a0.q_sn | a0.q_sh | a0.q_sb | a0.o_sn | a0.o_sh | a0.o_sb) % 8 ||
         ((reinterpret_cast<uintptr_t>(a0.q) | reinterpret_cast<uintptr_t>(a0.k) | reinterpret_cast<uintptr_t>(a0.v) |

@@ -290,3 +290,7 @@ def test_strided_decomposition_matches_oracle(sf, oracle, n, w, bs, h):
     ctx = sf.MhaContext(dm, plan, strided_band=w)
     out2 = sf.mha(dev(q), dev(k), dev(v), ctx).float().cpu().numpy()
     assert np.abs(out2 - out).max() == 0.0
+    if h % 2 == 0:  # the band part on head pairs (block_m 64 band BSR)
+        out3 = sf.strided_sdpa(dev(q), dev(k), dev(v), w, sf.build_bsr(band, 64, 16)).float().cpu().numpy()
+        d3 = np.abs(out3 - ref)
+        assert d3.max() <= 2e-2 and d3.sum() / np.abs(ref).sum() <= 1e-3, (d3.max(), d3.sum() / np.abs(ref).sum())

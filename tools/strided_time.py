@@ -18,8 +18,11 @@ for bs, n, w in ((8, 2048, 45), (16, 1024, 32), (16, 2048, 45), (16, 4096, 64), 
     b = sf.build_bsr(dm, 128, 16)
     band = sf.generate_mask([dict(pattern="causal_local", seq_len=n, band_width=w)])
     bb = sf.build_bsr(band, 128, 16)
+    bb64 = sf.build_bsr(band, 64, 16)  # the band part on head pairs
     t_bw = best_us(lambda: sf.block_sparse_sdpa(q, k, v, b, out=o))
     t_dec = best_us(lambda: sf.strided_sdpa(q, k, v, w, bb, out=o))
+    t_dec64 = best_us(lambda: sf.strided_sdpa(q, k, v, w, bb64, out=o))
     t_band = best_us(lambda: sf.block_sparse_sdpa(q, k, v, bb, out=o))
-    print(f"bs{bs} n{n} w{w}: block-wise {t_bw:8.1f} us  decomposed {t_dec:8.1f} us (band part alone {t_band:6.1f} us)"
-          f"  x{t_bw / t_dec:.2f}")
+    t_band64 = best_us(lambda: sf.block_sparse_sdpa(q, k, v, bb64, out=o))
+    print(f"bs{bs} n{n} w{w}: block-wise {t_bw:8.1f} us  decomposed {t_dec:8.1f} us / band on head pairs {t_dec64:8.1f} us"
+          f" (band part alone {t_band:6.1f} / {t_band64:6.1f} us)  x{t_bw / t_dec:.2f}", flush=True)
