@@ -294,3 +294,29 @@ def test_strided_decomposition_matches_oracle(sf, oracle, n, w, bs, h):
         out3 = sf.strided_sdpa(dev(q), dev(k), dev(v), w, sf.build_bsr(band, 64, 16)).float().cpu().numpy()
         d3 = np.abs(out3 - ref)
         assert d3.max() <= 2e-2 and d3.sum() / np.abs(ref).sum() <= 1e-3, (d3.max(), d3.sum() / np.abs(ref).sum())
+
+
+@pytest.mark.parametrize("n,bs,h,dtype", [(1000, 3, 4, "f16"), (1000, 1, 6, "bf16"), (776, 2, 2, "f16")])
+def test_head_pair_boxes_ragged(sf, oracle, monkeypatch, n, bs, h, dtype):
+    """Head pairs (block_m 64) with the two-head 5-D K/V boxes (even head count, n % 8 == 0) at row
+    counts that are not a multiple of the 64-row block, f16 and bf16, against the oracle; the
+    one-box-per-head path (SF_ATTN_PAIR5=0) gives the same bits."""
+    import torch
+    terms = [dict(pattern="bigbird", seq_len=n, global_width=20, band_width=20, filling_rate=0.1, seed=3)]
+    m = oracle.mask(terms)
+    q, k, v = fp16_inputs(oracle, bs, h, n, 64, 9)
+    ref, _ = oracle.block_sparse_sdpa(q, k, v, m, 64, 16, threads=8)
+    b = sf.build_bsr(sf.generate_mask(terms), 64, 16)
+    dt = torch.float16 if dtype == "f16" else torch.bfloat16
+    sf.set_attn_impl("tcgen05")
+    try:
+        out = sf.block_sparse_sdpa(to_dev(q, dt), to_dev(k, dt), to_dev(v, dt), b)
+        if dtype == "f16":
+            parity(out, ref)
+        else:
+            parity(out, ref, max_abs=6e-2, mean_rel=6e-3)
+        monkeypatch.setenv("SF_ATTN_PAIR5", "0")
+        out1 = sf.block_sparse_sdpa(to_dev(q, dt), to_dev(k, dt), to_dev(v, dt), b)
+        assert torch.equal(out, out1)
+    finally:
+        sf.set_attn_impl("auto")
