@@ -41,6 +41,15 @@ for _ in range(2):
     assert err < 2e-2, err
     print(f"attn head groups max_abs {err:.2e}")
 os.environ["SF_ATTN_HEADGROUP"] = "0"
+# head pairs (block_m 64) with the two-head 5-D K/V boxes: ~24 items per CTA here too
+ref64, _ = o.block_sparse_sdpa(q, k, v, m, 64, 16, threads=8)
+b64 = sf.build_bsr(sf.generate_mask(terms), 64, 16)
+for _ in range(2):
+    out = sf.block_sparse_sdpa(Q, K, V, b64)
+    torch.cuda.synchronize()
+    err = np.abs(out.float().cpu().numpy() - ref64).max()
+    assert err < 2e-2, err
+    print(f"attn head pairs max_abs {err:.2e}")
 x = torch.randn(512, 768, device="cuda").half()
 w = torch.randn(768, 768, device="cuda").half() * 0.03
 y = fused.gemm_fused(x, w, tile_n=1)
@@ -82,5 +91,15 @@ out = sf.strided_sdpa(Qs, Ks, Vs, 32, bb)
 torch.cuda.synchronize()
 err = np.abs(out.float().cpu().numpy() - refs).max()
 print(f"strided max_abs {err:.2e}")
+assert err < 2e-2
+# dilated class decomposition with a rest (dilated(16,1) + global(16), n 1024): classes, rest, merge
+td = [dict(pattern="dilated", seq_len=1024, band_width=16, dilation_rate=1), dict(pattern="global", seq_len=1024, global_width=16)]
+qd, kd, vd = (x.astype(np.float16).astype(np.float32) for x in o.random_attention_input(1, 2, 1024, d, 4))
+refd, _ = o.block_sparse_sdpa(qd, kd, vd, o.mask(td), 128, 16, threads=8)
+ctxd = sf.MhaContext(sf.generate_mask(td), sf.KernelPlan("block_wise", 128, 16), dilated=sf.dilated_split(td, 0, True))
+out = sf.mha(*(torch.from_numpy(x).cuda().half() for x in (qd, kd, vd)), ctxd)
+torch.cuda.synchronize()
+err = np.abs(out.float().cpu().numpy() - refd).max()
+print(f"dilated max_abs {err:.2e}")
 assert err < 2e-2
 print("sanitize_once ok")
