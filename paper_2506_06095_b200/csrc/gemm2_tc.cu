@@ -309,7 +309,7 @@ __global__ void __launch_bounds__(Cfg2<LN>::THREADS, 1) gemm2_kernel(const __gri
                 // no second TMEM pass is needed for the variance. The residual boxes are double-
                 // buffered: chunk c+1's load flies while c is added.
                 constexpr int CPT = CHUNKS / GROUPS;
-                uint32_t bph[2] = {0u, 0u};
+                uint32_t bph = 0u;  // bit b: phase of residual box b
                 auto res_issue = [&](int b_, int col) {
                     __syncwarp();  // every lane's reads of the box are done
                     if (lane == 0) {
@@ -319,8 +319,10 @@ __global__ void __launch_bounds__(Cfg2<LN>::THREADS, 1) gemm2_kernel(const __gri
                     }
                 };
                 if (p.aux) res_issue(0, n0 + c_begin * 32);
-                float cmean[CPT], cm2[CPT];
-#pragma unroll
+                // the chunk loops stay rolled: the epilogue runs a handful of times per CTA, so an
+                // unrolled body is fetched cold each time (no_instructions stalls)
+                float run_n = 0.f, run_mean = 0.f, run_m2 = 0.f;  // Chan's running (count, mean, M2)
+#pragma unroll 1
                 for (int cc = 0; cc < CPT; ++cc) {
                     const int c = c_begin + cc;
                     if (p.aux && cc + 1 < CPT) res_issue((cc + 1) & 1, n0 + (c + 1) * 32);
@@ -341,8 +343,8 @@ __global__ void __launch_bounds__(Cfg2<LN>::THREADS, 1) gemm2_kernel(const __gri
                     }
                     if (p.aux) {
                         const int b_ = cc & 1;
-                        tc::mbar_wait(&my_abar[b_], bph[b_]);
-                        bph[b_] ^= 1u;
+                        tc::mbar_wait(&my_abar[b_], (bph >> b_) & 1u);
+                        bph ^= 1u << b_;
                         const uint32_t bx = box + b_ * 2048u;
 #pragma unroll
                         for (int j = 0; j < 4; ++j) {
@@ -369,20 +371,17 @@ __global__ void __launch_bounds__(Cfg2<LN>::THREADS, 1) gemm2_kernel(const __gri
                         const float d = x[j] - mc;
                         q4[j & 3] = fmaf(d, d, q4[j & 3]);
                     }
-                    cmean[cc] = mc;
-                    cm2[cc] = (q4[0] + q4[1]) + (q4[2] + q4[3]);
+                    {  // Chan: merge (32, mc, m2c) into the running statistics
+                        const float m2c = (q4[0] + q4[1]) + (q4[2] + q4[3]);
+                        const float n_new = run_n + 32.f;
+                        const float dd = mc - run_mean;
+                        run_mean += dd * (32.f / n_new);
+                        run_m2 += m2c + dd * dd * (run_n * 32.f / n_new);
+                        run_n = n_new;
+                    }
                 }
                 tc::tmem_st_wait();
-                float lmean = 0.f;
-#pragma unroll
-                for (int cc = 0; cc < CPT; ++cc) lmean += cmean[cc];
-                lmean *= 1.f / CPT;
-                float lm2 = 0.f;
-#pragma unroll
-                for (int cc = 0; cc < CPT; ++cc) {
-                    const float d = cmean[cc] - lmean;
-                    lm2 += cm2[cc] + 32.f * d * d;
-                }
+                const float lmean = run_mean, lm2 = run_m2;
                 constexpr float kCols = 32.f * CPT;
                 const float2 mine = make_float2(lmean, lm2);
                 // exchange: every lane writes its row's partial into each row-sharing CTA, then one
@@ -416,7 +415,7 @@ __global__ void __launch_bounds__(Cfg2<LN>::THREADS, 1) gemm2_kernel(const __gri
                 // chunk is staged, and the two boxes alternate so a store only waits for the one
                 // before last (out_pre_ln: both boxes per chunk)
                 tc::tmem_ld32(taddr + c_begin * 32, r);
-#pragma unroll
+#pragma unroll 1
                 for (int cc = 0; cc < CPT; ++cc) {
                     const int c = c_begin + cc;
                     const int col = n0 + c * 32;
