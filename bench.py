@@ -411,12 +411,17 @@ def run_band_sweep(args):
         rw = sf.build_rowwise(dm)
         t_bw = timed(lambda s_: sf.block_sparse_sdpa(q, k, v, bsr, out=o, stream=s_))
         t_rw = timed(lambda s_: sf.rowwise_sdpa(q, k, v, rw, out=o, stream=s_))
-        best = min(t_bw, t_rw)
-        chosen = lambda pl: t_bw if pl.kind == "block_wise" else t_rw
+        # the block executor also at the other tile height (block_m 64: head pairs), so the B200
+        # plan's tile choice is checked too
+        bsr64 = sf.build_bsr(dm, 64, 16)
+        t_bw64 = timed(lambda s_: sf.block_sparse_sdpa(q, k, v, bsr64, out=o, stream=s_))
+        best = min(t_bw, t_bw64, t_rw)
+        chosen = lambda pl: (t_bw64 if pl.block_m == 64 else t_bw) if pl.kind == "block_wise" else t_rw
         print(json.dumps({"band_sweep": pat, "seq_len": n, ("density" if pat == "random_cells" else "band"): w, "bs": bs, "heads": h, "nnz": dm.true_count(),
                           "eq1_threshold": ref_plan.threshold, "reference_plan": ref_plan.kind,
-                          "b200_plan": b200_plan.kind, "blockwise_us": t_bw, "rowwise_us": t_rw,
-                          "regret_reference_mode": chosen(ref_plan) / best,
+                          "b200_plan": [b200_plan.kind, b200_plan.block_m, b200_plan.block_n],
+                          "blockwise_us": t_bw, "blockwise_bm64_us": t_bw64, "rowwise_us": t_rw,
+                          "regret_reference_mode": (t_bw if ref_plan.kind == "block_wise" else t_rw) / best,
                           "regret_b200_mode": chosen(b200_plan) / best}), flush=True)
 
 
