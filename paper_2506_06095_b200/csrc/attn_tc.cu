@@ -46,6 +46,12 @@ constexpr int kSBuf = 2;
 constexpr uint32_t kPCol = 128, kOCol = 192;
 constexpr int kMaxRowBlocks = 128;           // n <= 8192 at block_m 64
 constexpr float kRescaleLog2 = 8.0f;         // lazy-rescale threshold (P <= 2^8)
+#ifndef SF_PAIR_VS
+#define SF_PAIR_VS 3
+#endif
+#ifndef SF_PAIR_QBUF
+#define SF_PAIR_QBUF 1
+#endif
 
 // Geometry per query-block height. BM = 128: one (b, h) slice per work item, M = 128 MMAs.
 // BM = 64 ("head pair"): a work item is one 64-row block of TWO heads that share the block's load
@@ -58,11 +64,15 @@ template <int BM>
 struct AttnGeo {
     static constexpr bool kPair = BM == 64;
     static constexpr int kHeads = kPair ? 2 : 1;
-    static constexpr int kStagesG = kPair ? 2 : kStages;
+    // ring depths: K (with the stage's mask bits), V, and Q buffers. Head pairs hold 32 KB per
+    // K + V stage; two CTAs per SM fit 2 K + SF_PAIR_VS V stages with Q single-buffered
+    static constexpr int kKS = kPair ? 2 : kStages;
+    static constexpr int kVS = kPair ? SF_PAIR_VS : kStages;
+    static constexpr int kQBuf = kPair ? SF_PAIR_QBUF : 2;
     static constexpr int kQB = BM * kD * 2 * kHeads;          // 16 KB either way
     static constexpr int kKVB = kHeads * kNS * kD * 2;         // one stage of K (or V), all heads
     static constexpr int kMaskB = BM * 8;                      // 64 bits per query row per stage
-    static constexpr int kSmemG = 1024 + 2 * kQB + 2 * kStagesG * kKVB + kStagesG * kMaskB + kStagesG * 16 +
+    static constexpr int kSmemG = 1024 + kQBuf * kQB + (kKS + kVS) * kKVB + kKS * kMaskB + (kKS + kVS) * 8 +
                                   kMaxRowBlocks * 4 + (kMaxRowBlocks + 4) * 4 + 512;
 };
 
@@ -104,7 +114,7 @@ template <typename T, int BN, int BM>
 __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_constant__ AttnParams p) {
     using Geo = AttnGeo<BM>;
     constexpr bool kPair = Geo::kPair;
-    constexpr int kStages = Geo::kStagesG;   // shadows the file-scope BM = 128 values
+    constexpr int kKS = Geo::kKS, kVS = Geo::kVS, kQBuf = Geo::kQBuf;
     constexpr int kQBytes = Geo::kQB;
     constexpr int kKVBytes = Geo::kKVB;
     constexpr int kMaskBytes = Geo::kMaskB;
@@ -113,10 +123,10 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     unsigned char* sQ = sm;                               // [2] Q tiles (double-buffered across items)
-    unsigned char* sK = sQ + 2 * kQBytes;
-    unsigned char* sV = sK + kStages * kKVBytes;
-    unsigned char* sMask = sV + kStages * kKVBytes;        // [kStages][BM * 8 B]: packed part-tile bits
-    int32_t* s_order = reinterpret_cast<int32_t*>(sMask + kStages * kMaskBytes) + 4 * kStages;  // [kMaxRowBlocks]
+    unsigned char* sK = sQ + kQBuf * kQBytes;
+    unsigned char* sV = sK + kKS * kKVBytes;
+    unsigned char* sMask = sV + kVS * kKVBytes;            // [kKS][BM * 8 B]: packed part-tile bits
+    int32_t* s_order = reinterpret_cast<int32_t*>(sMask + kKS * kMaskBytes) + 2 * (kKS + kVS);  // [kMaxRowBlocks]
     // load_row_ptr cached in smem: item decodes at item boundaries read no global memory
     int32_t* s_lrp = s_order + kMaxRowBlocks;  // [n_rows + 1]
     uint64_t* bars = reinterpret_cast<uint64_t*>(s_lrp + kMaxRowBlocks + 4);
@@ -125,11 +135,11 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
     // K (with the stage's bit rows) and V have separate barriers: a K slot is
     // released as soon as the softmax holds S of that step (and read its bits), a V slot when
     // P.V of that step is done, so K loads run about a step further ahead than V loads
-    uint64_t* k_full = q_empty + 2;           // [kStages]
-    uint64_t* k_empty = k_full + kStages;     // [kStages] (128 softmax arrivals)
-    uint64_t* v_full = k_empty + kStages;     // [kStages]
-    uint64_t* v_empty = v_full + kStages;     // [kStages]
-    uint64_t* s_full = v_empty + kStages;     // [kSBuf]
+    uint64_t* k_full = q_empty + 2;           // [kKS]
+    uint64_t* k_empty = k_full + kKS;         // [kKS] (128 softmax arrivals)
+    uint64_t* v_full = k_empty + kKS;         // [kVS]
+    uint64_t* v_empty = v_full + kVS;         // [kVS]
+    uint64_t* s_full = v_empty + kVS;         // [kSBuf]
     uint64_t* p_full = s_full + kSBuf;        // [kSBuf]
     uint64_t* o_full = p_full + kSBuf;        // [2]: P.V step g completes o_full[g&1] (parity waits are
                                               // unambiguous only within one phase of lag)
@@ -167,9 +177,11 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
             tc::mbar_init(&q_empty[i], 1);
             tc::mbar_init(&o_full[i], 1);
         }
-        for (int s = 0; s < kStages; ++s) {
+        for (int s = 0; s < kKS; ++s) {
             tc::mbar_init(&k_full[s], 1);
             tc::mbar_init(&k_empty[s], 128);
+        }
+        for (int s = 0; s < kVS; ++s) {
             tc::mbar_init(&v_full[s], 1);
             tc::mbar_init(&v_empty[s], 1);
         }
@@ -228,11 +240,11 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
                 hh2[t] = s_ % p.h;
             }
             if (lane == 0) {
-                tc::mbar_wait(&q_empty[qi & 1], ((qi >> 1) & 1) ^ 1);
-                tc::mbar_expect_tx(&q_full[qi & 1], kQBytes);
+                tc::mbar_wait(&q_empty[qi % kQBuf], ((qi / kQBuf) & 1) ^ 1);
+                tc::mbar_expect_tx(&q_full[qi % kQBuf], kQBytes);
 #pragma unroll
                 for (int t = 0; t < Geo::kHeads; ++t)
-                    tma_load_4d(sQ + (qi & 1) * kQBytes + t * (BM * kD * 2), &p.tq, &q_full[qi & 1], 0, rb * BM, hh2[t],
+                    tma_load_4d(sQ + (qi % kQBuf) * kQBytes + t * (BM * kD * 2), &p.tq, &q_full[qi % kQBuf], 0, rb * BM, hh2[t],
                                 hb[t]);
             }
             ++qi;
@@ -242,7 +254,7 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
                 const int my_tile = e < L ? p.load_tile[l0 + e] : -2;
                 const int j1 = min(nsteps, (c + 32) / G);
                 for (int j = c / G; j < j1; ++j, ++g) {
-                    const int st = g % kStages;
+                    const int st = g % kKS, sv = g % kVS;
                     // lane gg < G owns column block gg of the step: its K / V boxes and bit tile
                     // are issued from G lanes in parallel (one issuing thread sustains only one
                     // 16-row TMA box per ~160 cycles; tools/micro/tma_gather.cu)
@@ -250,7 +262,7 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
                     const int gcol = __shfl_sync(0xffffffffu, my_col, src);
                     const int gtile = __shfl_sync(0xffffffffu, my_tile, src);
                     const int parts = __popc(__ballot_sync(0xffffffffu, lane < G && gtile >= 0));
-                    const uint32_t ph = ((g / kStages) & 1) ^ 1;
+                    const uint32_t ph = ((g / kKS) & 1) ^ 1, phv = ((g / kVS) & 1) ^ 1;
                     if (lane == 0) {
                         SF_TRACE(g, 4);
                         tc::mbar_wait(&k_empty[st], ph);
@@ -292,20 +304,20 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
                     }
                     if (lane == 0) {
                         SF_TRACE(g, 7);
-                        tc::mbar_wait(&v_empty[st], ph);
+                        tc::mbar_wait(&v_empty[sv], phv);
                         SF_TRACE(g, 11);
-                        tc::mbar_expect_tx(&v_full[st], kKVBytes);
+                        tc::mbar_expect_tx(&v_full[sv], kKVBytes);
                     }
                     __syncwarp();
                     if (lane < G) {
                         const int gg = static_cast<int>(lane);
                         if (kPair && p.pair5) {
-                            tma_load_5d(sV + st * kKVBytes + gg * BN * kD * 2 * 2, &p.tv2, &v_full[st], 0, 0, hh2[0],
+                            tma_load_5d(sV + sv * kKVBytes + gg * BN * kD * 2 * 2, &p.tv2, &v_full[sv], 0, 0, hh2[0],
                                         gcol * (BN / 8), hb[0]);
                         } else {
 #pragma unroll
                             for (int t = 0; t < Geo::kHeads; ++t)
-                                tma_load_4d(sV + st * kKVBytes + t * (kNS * kD * 2) + gg * BN * kD * 2, &p.tv, &v_full[st],
+                                tma_load_4d(sV + sv * kKVBytes + t * (kNS * kD * 2) + gg * BN * kD * 2, &p.tv, &v_full[sv],
                                             0, gcol * BN, hh2[t], hb[t]);
                         }
                     }
@@ -324,17 +336,17 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
             uint32_t gS = 0;
             auto issue_s = [&]() {
                 if (cs.j == 0) {
-                    tc::mbar_wait(&q_full[cs.qi & 1], (cs.qi >> 1) & 1);
+                    tc::mbar_wait(&q_full[cs.qi % kQBuf], (cs.qi / kQBuf) & 1);
                     tc::fence_after_sync();
                 }
-                const int s = gS % kStages;
+                const int s = gS % kKS;
                 SF_TRACE(gS, 13);
-                tc::mbar_wait(&k_full[s], (gS / kStages) & 1);
+                tc::mbar_wait(&k_full[s], (gS / kKS) & 1);
                 SF_TRACE(gS, 14);
                 tc::fence_after_sync();
 #pragma unroll
                 for (int t = 0; t < Geo::kHeads; ++t) {  // head t: M = BM rows at TMEM lane offset 16t
-                    const uint32_t q0 = tc::smem_u32(sQ + (cs.qi & 1) * kQBytes + t * (BM * kD * 2));
+                    const uint32_t q0 = tc::smem_u32(sQ + (cs.qi % kQBuf) * kQBytes + t * (BM * kD * 2));
                     const bool p5 = kPair && p.pair5;
                     const uint32_t k0 = tc::smem_u32(sK + s * kKVBytes) + (p5 ? 1024u * t : static_cast<uint32_t>(t * (kNS * kD * 2)));
                     const uint32_t kv_sbo = p5 ? 2048u : 1024u;
@@ -344,17 +356,17 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
                                        sdesc_sw128_sbo(k0 + 32 * k, kv_sbo), idesc_s, k != 0);
                 }
                 tc::mma_commit(&s_full[gS % kSBuf]);
-                if (cs.j == cs.ns - 1) tc::mma_commit(&q_empty[cs.qi & 1]);  // last S of the item: Q free
+                if (cs.j == cs.ns - 1) tc::mma_commit(&q_empty[cs.qi % kQBuf]);  // last S of the item: Q free
                 ++gS;
                 cs.advance(items, feed);
             };
             for (int j = 0; j < kSBuf && cs.valid; ++j) issue_s();
             for (uint32_t g = 0; cp.valid; ++g) {
-                const int s = g % kStages;
+                const int s = g % kVS;
                 const int sb = g % kSBuf;
                 tc::mbar_wait(&p_full[sb], (g / kSBuf) & 1);  // P_g in TMEM (S_g consumed), O rescaled
                 SF_TRACE(g, 8);
-                tc::mbar_wait(&v_full[s], (g / kStages) & 1);
+                tc::mbar_wait(&v_full[s], (g / kVS) & 1);
                 tc::fence_after_sync();
 #pragma unroll
                 for (int t = 0; t < Geo::kHeads; ++t) {
@@ -442,13 +454,13 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
             items.decode(idx, rb, bh, l0, L, nsteps);
             float m = -INFINITY, l = 0.f;
             for (int j = 0; j < nsteps; ++j, ++g) {
-                const int st = g % kStages;
+                const int st = g % kKS;
                 const int sb = g % kSBuf;
                 const bool tr = warp == 2 && lane == 0 && k == 0;
                 const bool trw = lane == 0;  // per-warp events 16 + 4 (warp - 2) + {0..3}, by CTA step g
                 if (tr) SF_TRACE(j, 0);
                 if (trw) SF_TRACE(g, 16 + 4 * (warp - 2));
-                tc::mbar_wait(&k_full[st], (g / kStages) & 1);
+                tc::mbar_wait(&k_full[st], (g / kKS) & 1);
                 if (tr) SF_TRACE(j, 1);
                 // this row's 64 mask bits (the producer staged every tile's rows: full -> ones,
                 // part -> its pool rows, padding -> 0)
