@@ -52,6 +52,15 @@ constexpr float kRescaleLog2 = 8.0f;         // lazy-rescale threshold (P <= 2^8
 #ifndef SF_PAIR_QBUF
 #define SF_PAIR_QBUF 1
 #endif
+#ifndef SF_ONE_KS
+#define SF_ONE_KS 4
+#endif
+#ifndef SF_ONE_VS
+#define SF_ONE_VS 4
+#endif
+#ifndef SF_ONE_QBUF
+#define SF_ONE_QBUF 2
+#endif
 
 // Geometry per query-block height. BM = 128: one (b, h) slice per work item, M = 128 MMAs.
 // BM = 64 ("head pair"): a work item is one 64-row block of TWO heads that share the block's load
@@ -66,9 +75,9 @@ struct AttnGeo {
     static constexpr int kHeads = kPair ? 2 : 1;
     // ring depths: K (with the stage's mask bits), V, and Q buffers. Head pairs hold 32 KB per
     // K + V stage; two CTAs per SM fit 2 K + SF_PAIR_VS V stages with Q single-buffered
-    static constexpr int kKS = kPair ? 2 : kStages;
-    static constexpr int kVS = kPair ? SF_PAIR_VS : kStages;
-    static constexpr int kQBuf = kPair ? SF_PAIR_QBUF : 2;
+    static constexpr int kKS = kPair ? 2 : SF_ONE_KS;
+    static constexpr int kVS = kPair ? SF_PAIR_VS : SF_ONE_VS;
+    static constexpr int kQBuf = kPair ? SF_PAIR_QBUF : SF_ONE_QBUF;
     static constexpr int kQB = BM * kD * 2 * kHeads;          // 16 KB either way
     static constexpr int kKVB = kHeads * kNS * kD * 2;         // one stage of K (or V), all heads
     static constexpr int kMaskB = BM * 8;                      // 64 bits per query row per stage
