@@ -46,6 +46,9 @@ constexpr int kSBuf = 2;
 constexpr uint32_t kPCol = 128, kOCol = 192;
 constexpr int kMaxRowBlocks = 128;           // n <= 8192 at block_m 64
 constexpr float kRescaleLog2 = 8.0f;         // lazy-rescale threshold (P <= 2^8)
+#ifndef SF_PAIR_KS
+#define SF_PAIR_KS 2
+#endif
 #ifndef SF_PAIR_VS
 #define SF_PAIR_VS 3
 #endif
@@ -75,7 +78,7 @@ struct AttnGeo {
     static constexpr int kHeads = kPair ? 2 : 1;
     // ring depths: K (with the stage's mask bits), V, and Q buffers. Head pairs hold 32 KB per
     // K + V stage; two CTAs per SM fit 2 K + SF_PAIR_VS V stages with Q single-buffered
-    static constexpr int kKS = kPair ? 2 : SF_ONE_KS;
+    static constexpr int kKS = kPair ? SF_PAIR_KS : SF_ONE_KS;
     static constexpr int kVS = kPair ? SF_PAIR_VS : SF_ONE_VS;
     static constexpr int kQBuf = kPair ? SF_PAIR_QBUF : SF_ONE_QBUF;
     static constexpr int kQB = BM * kD * 2 * kHeads;          // 16 KB either way
