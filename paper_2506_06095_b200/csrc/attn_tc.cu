@@ -254,10 +254,14 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
             if (lane == 0) {
                 tc::mbar_wait(&q_empty[qi % kQBuf], ((qi / kQBuf) & 1) ^ 1);
                 tc::mbar_expect_tx(&q_full[qi % kQBuf], kQBytes);
+                if (kPair && p.pair5) {
+                    tma_load_4d(sQ + (qi % kQBuf) * kQBytes, &p.tq, &q_full[qi % kQBuf], 0, rb * BM, hh2[0], hb[0]);
+                } else {
 #pragma unroll
-                for (int t = 0; t < Geo::kHeads; ++t)
-                    tma_load_4d(sQ + (qi % kQBuf) * kQBytes + t * (BM * kD * 2), &p.tq, &q_full[qi % kQBuf], 0, rb * BM, hh2[t],
-                                hb[t]);
+                    for (int t = 0; t < Geo::kHeads; ++t)
+                        tma_load_4d(sQ + (qi % kQBuf) * kQBytes + t * (BM * kD * 2), &p.tq, &q_full[qi % kQBuf], 0, rb * BM,
+                                    hh2[t], hb[t]);
+                }
             }
             ++qi;
             for (int c = 0; c < L; c += 32) {
@@ -617,7 +621,7 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
 
 // 4-D map over (d, n, h, b) with element strides (1, sn, sh, sb); box {64, rows, 1, 1}, SW128.
 sf_status make_tmap_4d(CUtensorMap* map, const void* base, int n, int h, int bs, int64_t sn, int64_t sh, int64_t sb,
-                       uint32_t box_rows, bool bf16) {
+                       uint32_t box_rows, bool bf16, uint32_t box_heads = 1) {
     static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
     if (!encode) {
         cudaDriverEntryPointQueryResult q{};
@@ -630,7 +634,7 @@ sf_status make_tmap_4d(CUtensorMap* map, const void* base, int n, int h, int bs,
                                 static_cast<cuuint64_t>(bs)};
     const cuuint64_t strides[3] = {static_cast<cuuint64_t>(sn * 2), static_cast<cuuint64_t>(sh * 2),
                                    static_cast<cuuint64_t>(sb * 2)};
-    const cuuint32_t box[4] = {static_cast<cuuint32_t>(kD), box_rows, 1, 1};
+    const cuuint32_t box[4] = {static_cast<cuuint32_t>(kD), box_rows, box_heads, 1};
     const cuuint32_t estr[4] = {1, 1, 1, 1};
     CUresult r = encode(map, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4,
                         const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -764,6 +768,8 @@ sf_status attn_tc(const sf_attn_args& a, const sf_bsr_dev& b, cudaStream_t st, b
         if (!(e && *e == '0')) {
             SF_TRY(make_tmap_pair5(&p.tk2, a.k, a.seq_len, a.h, a.bs, a.q_sn, a.q_sh, a.q_sb, b.block_n, bf));
             SF_TRY(make_tmap_pair5(&p.tv2, a.v, a.seq_len, a.h, a.bs, a.q_sn, a.q_sh, a.q_sb, b.block_n, bf));
+            // Q of both heads in one box {64, 64, 2, 1}: [head][64 rows][128 B], head t at t * 8 KB
+            SF_TRY(make_tmap_4d(&p.tq, a.q, a.seq_len, a.h, a.bs, a.q_sn, a.q_sh, a.q_sb, b.block_m, bf, 2));
             p.pair5 = 1;
         }
     }
