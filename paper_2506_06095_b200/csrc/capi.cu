@@ -36,7 +36,7 @@ namespace {
 // per row when rows average <= 32 keys, 0.65 ns with a warp per row) and ~6e10 valid cells/s.
 constexpr double kBlockCellsPerUs = 1.8e6;
 constexpr double kBlockFloorUs = 12.0;
-constexpr double kPairCellRatio = 0.70;  // block_m 64 when its executed cells < 0.70x block_m 128's
+constexpr double kPairCellRatio = 0.80;  // block_m 64 when its executed cells < 0.80x block_m 128's
 constexpr double kRowNnzPerUs = 6.0e4;
 constexpr double kRowFloorUs = 10.0;
 

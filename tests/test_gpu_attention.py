@@ -182,8 +182,9 @@ def test_unified_mha_dispatch(sf, oracle):
     plan = sf.select_plan(wide, sf.hw_preset("b200"), 1024, 12, 16, 64, mode="b200")
     # BigBird's 16-row random blocks: 64-row blocks (head pairs) execute 0.67x the cells
     assert plan.kind == "block_wise" and (plan.block_m, plan.block_n) == (64, 16), plan
-    band = sf.select_plan(sf.gen_sliding_window(4096, 64), sf.hw_preset("b200"), 4096, 12, 16, 64, mode="b200")
-    assert band.kind == "block_wise" and band.block_m == 128, band  # wide band: 0.75x cells, slower as pairs
+    causal = sf.generate_mask([dict(pattern="causal", seq_len=1024)])
+    cp = sf.select_plan(causal, sf.hw_preset("b200"), 1024, 12, 16, 64, mode="b200")
+    assert cp.kind == "block_wise" and cp.block_m == 128, cp  # causal: 0.94x the cells, slower as pairs
 
 
 def test_b200_selector_calibration(sf):
