@@ -119,7 +119,7 @@ struct MhaContext {
         MhaContext ctx = make(mask, plan);
         MaskDescriptor d{"causal_local", mask.seq_len(), {}};
         d.params.band_width = band;
-        ctx.band_bsr = build_bsr(generate_mask(d), 128, 16);
+        ctx.band_bsr = build_bsr(generate_mask(d), 64, 16);  // the band part on head pairs
         ctx.strided_band = band;
         return ctx;
     }
