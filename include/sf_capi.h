@@ -286,7 +286,7 @@ sf_status sf_mha_strided(const sf_attn_args* args, int32_t band_width, const sf_
  * block executor on the tensors' rows p, p + s, ... with class_bsr = build_bsr(sliding(w) over
  * n / s rows, 128, bn); rest_bsr (NULL or empty: none) = build_bsr(mask AND NOT dilated(w, r), 128, bn)
  * runs over the full rows, and the two parts are merged per row by log-sum-exp. Needs n % s == 0,
- * head_size 64, block_m 128 BSRs. SF_PLAN_ERROR otherwise (no launch). */
+ * head_size 64, block_m 128 or 64 (head pairs) BSRs. SF_PLAN_ERROR otherwise (no launch). */
 sf_status sf_mha_dilated(const sf_attn_args* args, int32_t stride, const sf_bsr_dev* class_bsr,
                          const sf_bsr_dev* rest_bsr, void* stream);
 

@@ -78,8 +78,9 @@ extern "C" sf_status sf_mha_dilated(const sf_attn_args* args, int32_t stride, co
     if (a0.seq_len % stride != 0) return fail(SF_PLAN_ERROR, "dilated decomposition needs seq_len % stride == 0");
     if (class_bsr->seq_len != a0.seq_len / stride) return fail(SF_SHAPE_ERROR, "class BSR seq_len must be seq_len / stride");
     if (rest_bsr && rest_bsr->seq_len != a0.seq_len) return fail(SF_SHAPE_ERROR, "rest BSR seq_len differs from input");
-    if (a0.head_size != 64 || class_bsr->block_m != 128 || (rest_bsr && rest_bsr->block_m != 128))
-        return fail(SF_PLAN_ERROR, "dilated decomposition needs head_size 64 and block_m 128 BSRs");
+    auto tc_tile = [](const sf_bsr_dev* b) { return b->block_m == 128 || b->block_m == 64; };
+    if (a0.head_size != 64 || !tc_tile(class_bsr) || (rest_bsr && !tc_tile(rest_bsr)))
+        return fail(SF_PLAN_ERROR, "dilated decomposition needs head_size 64 and block_m 128 or 64 (head pairs) BSRs");
     cudaStream_t st = as_stream(stream);
     sf_attn_args a = a0;
     if (a.scale == 0.f) a.scale = 1.0f / std::sqrt(static_cast<float>(a.head_size));

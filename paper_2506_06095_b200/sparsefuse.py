@@ -562,6 +562,8 @@ class MhaContext:
             s, w = self.dilated
             n = mask.seq_len
             band = generate_mask([dict(pattern="sliding", seq_len=n // s, band_width=min(w, n // s))], stream)
+            # block_m 128: on head pairs the class bands measured 119.5 / 282.6 us at n 4096 / 8192
+            # vs 120 / 265 (tools/dilated_time.py)
             self.class_bsr = build_bsr(band, 128, 16, stream)
             dil = generate_mask([dict(pattern="dilated", seq_len=n, band_width=w, dilation_rate=s - 1)], stream)
             rest = build_bsr(mask_andnot(mask, dil, stream), 128, 16, stream)
