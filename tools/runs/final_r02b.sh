@@ -9,4 +9,5 @@ for c in cfg1 cfg3 cfg4; do timeout 900 python bench.py --config $c --no-cpu-bas
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv --log-file $O/launches_cfg2.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline > $O/launches.log 2>&1
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:"attn_tc|gemm2" -s 10 -c 5 -o $O/layer_cfg2 -f python tools/layer_once.py > $O/ncu_layer.log 2>&1
 tail -n 2 $O/gputest.log; cat $O/smoke.log
-timeout 900 python bench.py --sweep > $O/sweep_mha_v13.jsonl 2> $O/sweep.err
+timeout 900 python bench.py --sweep > $O/sweep_mha_v14.jsonl 2> $O/sweep.err
+timeout 900 python bench.py --band-sweep --steps 7 > $O/band_sweep_v5.jsonl 2>/dev/null
