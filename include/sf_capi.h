@@ -272,7 +272,8 @@ sf_status sf_mha_rowwise(const sf_attn_args* args, const sf_csr_dev* csr, void* 
 
 /* Masked MHA for the strided pattern (sf_pattern SF_PATTERN_STRIDED, band w) by mask decomposition:
  * strided(w) = causal-local(w) (disjoint-)union the diagonals i - j = k w, k >= 1. The band runs on
- * the tcgen05 block kernel over `band_bsr` (the block_m 128 BSR of the causal-local(w) mask, e.g.
+ * the tcgen05 block kernel over `band_bsr` (the block_m 128 or 64 — head pairs, the faster — BSR of
+ * the causal-local(w) mask, e.g.
  * sf_mask_generate of {SF_PATTERN_CAUSAL_LOCAL, w} then sf_bsr_build), emitting per-row
  * log-sum-exp; the diagonals are exact dense causal attention inside each residue class i % w
  * (warp-level tensor-core MMAs) merged into the band's output. Same result semantics as
