@@ -49,3 +49,25 @@ def test_host_only_entry_points_without_gpu():
     _lib.check(L.sf_select_plan_from_loads(64 * 64, C.byref(hw), 1024, 12, 8, 64, 0, C.byref(p)))
     assert p.kind == _lib.SF_BLOCK_WISE
     assert "sm_100a" in _lib.version()
+
+
+def test_decomposition_routing_host_logic():
+    """Which session masks the unified MHA decomposes (host logic, no device): one strided(w) term
+    at n >= 2048 with ceil(n / w) <= 128; one dilated(w, r >= 1) term with n % (r + 1) == 0 at
+    n >= DILATED_MIN_SEQ (others only as an explicit rest); everything else runs the plan's executor."""
+    import paper_2506_06095_b200.sparsefuse as sf
+    st = lambda n, w: [dict(pattern="strided", seq_len=n, band_width=w)]
+    assert sf.strided_band(st(2048, 45)) == 45
+    assert sf.strided_band(st(1024, 32)) is None          # below n = 2048
+    assert sf.strided_band(st(8192, 32)) is None          # 256 classes > 128 rows per class kernel
+    assert sf.strided_band(st(2048, 45) + [dict(pattern="global", seq_len=2048, global_width=8)]) is None
+    dil = lambda n, w, r: dict(pattern="dilated", seq_len=n, band_width=w, dilation_rate=r)
+    assert sf.dilated_split([dil(4096, 64, 1)]) == (2, 64)
+    assert sf.dilated_split([dil(4096, 64, 2)]) is None   # 4096 % 3 != 0
+    assert sf.dilated_split([dil(6144, 20, 2)]) == (3, 20)
+    assert sf.dilated_split([dil(2048, 45, 1)]) is None   # below DILATED_MIN_SEQ
+    assert sf.dilated_split([dil(2048, 45, 1)], min_seq_len=0) == (2, 45)
+    assert sf.dilated_split([dil(4096, 64, 0)]) is None   # rate 0 is a plain band
+    t5 = [dil(4096, 64, 1), dict(pattern="global", seq_len=4096, global_width=64)]
+    assert sf.dilated_split(t5) is None and sf.dilated_split(t5, allow_rest=True) == (2, 64)
+    assert sf.dilated_split([dict(pattern="sliding", seq_len=4096, band_width=64)]) is None
