@@ -241,7 +241,8 @@ extern "C" sf_status sf_select_plan(const uint32_t* d_bits, const sf_hw_spec* hw
         // longformer; never causal or wide bands (0.75-0.98x the cells, 1.04-1.08x the time)
         // (tools/bm_sweep.py, profiles/r02/bm_sweep.txt). SF_PLAN_PAIR=0 keeps block_m 128.
         const char* pe = std::getenv("SF_PLAN_PAIR");
-        if (out->kind == SF_BLOCK_WISE && out->block_m == 128 && !(pe && *pe == '0')) {
+        // (the tcgen05 kernel holds <= 128 row blocks: head pairs up to n = 8192)
+        if (out->kind == SF_BLOCK_WISE && out->block_m == 128 && seq_len <= 64 * 128 && !(pe && *pe == '0')) {
             sf_bsr_dev b64{};
             SF_TRY(sf_bsr_build(d_bits, static_cast<int32_t>(seq_len), 64, out->block_n, &b64, stream));
             const int64_t n_load64 = b64.n_load;
