@@ -119,7 +119,8 @@ struct MhaContext {
         MhaContext ctx = make(mask, plan);
         MaskDescriptor d{"causal_local", mask.seq_len(), {}};
         d.params.band_width = band;
-        ctx.band_bsr = build_bsr(generate_mask(d), 64, 16);  // the band part on head pairs
+        // the band part on head pairs where they hold the row blocks (n <= 8192)
+        ctx.band_bsr = build_bsr(generate_mask(d), mask.seq_len() <= 8192 ? 64 : 128, 16);
         ctx.strided_band = band;
         return ctx;
     }

@@ -557,7 +557,8 @@ class MhaContext:
             band = generate_mask([dict(pattern="causal_local", seq_len=mask.seq_len, band_width=strided_band)], stream)
             # the band part on head pairs (block_m 64): bs16 x 12 x n2048, w45: band part 47.0 vs
             # 51.7 us, decomposed 130.5 vs 135.8 us (tools/strided_time.py)
-            self.band_bsr = build_bsr(band, 64, 16, stream)
+            # (head pairs hold <= 128 row blocks of 64: n <= 8192; longer sequences keep block_m 128)
+            self.band_bsr = build_bsr(band, 64 if mask.seq_len <= 8192 else 128, 16, stream)
         elif self.dilated:  # (stride, w) from dilated_split(): class band + the rest of the mask
             s, w = self.dilated
             n = mask.seq_len
