@@ -321,3 +321,28 @@ def test_head_pair_boxes_ragged(sf, oracle, monkeypatch, n, bs, h, dtype):
         assert torch.equal(out, out1)
     finally:
         sf.set_attn_impl("auto")
+
+
+def test_long_sequences_keep_block_m_128(sf):
+    """Past n = 8192 the head-pair tile would exceed the tcgen05 kernel's 128 row blocks: the
+    selector keeps block_m 128 there and the strided context keeps a block_m 128 band; the
+    decomposed strided executor at n = 16384 agrees with the block executor over the whole mask."""
+    import torch
+    n, w = 16384, 128
+    bb = sf.gen_bigbird(n, 128, 128, 0.1, 0)
+    plan = sf.select_plan(bb, sf.hw_preset("b200"), n, 12, 1, 64, mode="b200")
+    assert plan.kind == "block_wise" and plan.block_m == 128, plan
+    terms = [dict(pattern="strided", seq_len=n, band_width=w)]
+    dm = sf.generate_mask(terms)
+    ctx = sf.context_for(terms, dm, sf.KernelPlan("block_wise", 128, 16))
+    assert ctx.strided_band == w and ctx.band_bsr.dev.block_m == 128
+    g = torch.Generator(device="cuda").manual_seed(3)
+    q, k, v = ((torch.rand(1, 2, n, 64, device="cuda", generator=g) * 2 - 1).half() for _ in range(3))
+    out = sf.mha(q, k, v, ctx)
+    sf.set_attn_impl("tcgen05")
+    try:
+        ref = sf.block_sparse_sdpa(q, k, v, sf.build_bsr(dm, 128, 16))
+    finally:
+        sf.set_attn_impl("auto")
+    d = (out.float() - ref.float()).abs()
+    assert d.max().item() <= 2e-2 and (d.sum() / ref.float().abs().sum()).item() <= 1e-3
