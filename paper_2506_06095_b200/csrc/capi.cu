@@ -36,6 +36,7 @@ namespace {
 // per row when rows average <= 32 keys, 0.65 ns with a warp per row) and ~6e10 valid cells/s.
 constexpr double kBlockCellsPerUs = 1.8e6;
 constexpr double kBlockFloorUs = 12.0;
+constexpr double kWideTileCellRatio = 1.05;  // block_n 64 / 32 when their cells are <= 1.05x block_n 16's
 constexpr double kPairCellRatio = 0.80;  // block_m 64 when its executed cells < 0.80x block_m 128's
 constexpr double kRowNnzPerUs = 6.0e4;
 constexpr double kRowFloorUs = 10.0;
@@ -250,6 +251,28 @@ extern "C" sf_status sf_select_plan(const uint32_t* d_bits, const sf_hw_spec* hw
             if (static_cast<double>(n_load64) * 64.0 < kPairCellRatio * static_cast<double>(n_load) * 128.0) {
                 out->block_m = 64;
                 out->score = plan_score(64, out->block_n, out->num_warps, *hw, seq_len, h, bs, head_size);
+            }
+        }
+        // block_n last: the widest of 64 / 32 whose tiles execute at most 5% more cells than the
+        // plan's. A step gathers 64 keys in 64 / block_n boxes per tensor, so wider tiles cut the
+        // TMA boxes and the bit-row fills per step (T5 cfg4 at (64, 64): 91.7 vs 100.7 us with the
+        // same cells; cfg2's BigBird keeps 16: 1.36x the cells at 32; tools/tile_test.py).
+        const char* be = std::getenv("SF_PLAN_BN");
+        if (out->kind == SF_BLOCK_WISE && out->block_n == 16 && !(be && *be == '0')) {
+            sf_bsr_dev b0{};
+            SF_TRY(sf_bsr_build(d_bits, static_cast<int32_t>(seq_len), out->block_m, 16, &b0, stream));
+            const double cells16 = static_cast<double>(b0.n_load) * 16.0;
+            SF_TRY(sf_bsr_free(&b0, stream));
+            for (int bn : {64, 32}) {
+                sf_bsr_dev bw{};
+                SF_TRY(sf_bsr_build(d_bits, static_cast<int32_t>(seq_len), out->block_m, bn, &bw, stream));
+                const double cells = static_cast<double>(bw.n_load) * bn;
+                SF_TRY(sf_bsr_free(&bw, stream));
+                if (cells <= kWideTileCellRatio * cells16) {
+                    out->block_n = bn;
+                    out->score = plan_score(out->block_m, bn, out->num_warps, *hw, seq_len, h, bs, head_size);
+                    break;
+                }
             }
         }
     }
