@@ -94,6 +94,7 @@ struct AttnParams {
     // ONE box per column block carries both heads' rows as [row / 8][head][8 rows][128 B], so head
     // t's swizzle atoms sit at t * 1 KB + a 2 KB stride (half the boxes of one box per head)
     CUtensorMap tk2, tv2;
+    CUtensorMap tk4, tv4;  // the same maps with a 64-row box: a step whose column blocks are consecutive
     int32_t pair5;
     int32_t n, h, bh, n_rows, n_items;  // bh: work units per row block (slices, or head pairs at BM 64)
     int32_t bh_total;                   // b * h slices
@@ -183,6 +184,10 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
         if (kPair && p.pair5) {
             tc::prefetch_tmap(&p.tk2);
             tc::prefetch_tmap(&p.tv2);
+        }
+        if (kPair && p.pair5 == 2) {
+            tc::prefetch_tmap(&p.tk4);
+            tc::prefetch_tmap(&p.tv4);
         }
         for (int i = 0; i < 2; ++i) {
             tc::mbar_init(&q_full[i], 1);
@@ -278,6 +283,11 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
                     const int gcol = __shfl_sync(0xffffffffu, my_col, src);
                     const int gtile = __shfl_sync(0xffffffffu, my_tile, src);
                     const int parts = __popc(__ballot_sync(0xffffffffu, lane < G && gtile >= 0));
+                    // a step over G consecutive column blocks (band interiors) loads each tensor with
+                    // ONE 64-row box instead of G: the same bytes land at the same stage addresses
+                    const int gcol0 = __shfl_sync(0xffffffffu, gcol, 0);
+                    const bool run = kPair && G > 1 && p.pair5 == 2 &&
+                                     __all_sync(0xffffffffu, lane >= G || gcol == gcol0 + static_cast<int>(lane));
                     const uint32_t ph = ((g / kKS) & 1) ^ 1, phv = ((g / kVS) & 1) ^ 1;
                     if (lane == 0) {
                         SF_TRACE(g, 4);
@@ -306,8 +316,11 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
                     if (lane < G) {
                         const int gg = static_cast<int>(lane);
                         if (kPair && p.pair5) {
-                            tma_load_5d(sK + st * kKVBytes + gg * BN * kD * 2 * 2, &p.tk2, &k_full[st], 0, 0, hh2[0],
-                                        gcol * (BN / 8), hb[0]);
+                            if (!run)
+                                tma_load_5d(sK + st * kKVBytes + gg * BN * kD * 2 * 2, &p.tk2, &k_full[st], 0, 0, hh2[0],
+                                            gcol * (BN / 8), hb[0]);
+                            else if (gg == 0)
+                                tma_load_5d(sK + st * kKVBytes, &p.tk4, &k_full[st], 0, 0, hh2[0], gcol0 * (BN / 8), hb[0]);
                         } else {
 #pragma unroll
                             for (int t = 0; t < Geo::kHeads; ++t)  // head t's 64 keys at t * 8 KB
@@ -328,8 +341,11 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
                     if (lane < G) {
                         const int gg = static_cast<int>(lane);
                         if (kPair && p.pair5) {
-                            tma_load_5d(sV + sv * kKVBytes + gg * BN * kD * 2 * 2, &p.tv2, &v_full[sv], 0, 0, hh2[0],
-                                        gcol * (BN / 8), hb[0]);
+                            if (!run)
+                                tma_load_5d(sV + sv * kKVBytes + gg * BN * kD * 2 * 2, &p.tv2, &v_full[sv], 0, 0, hh2[0],
+                                            gcol * (BN / 8), hb[0]);
+                            else if (gg == 0)
+                                tma_load_5d(sV + sv * kKVBytes, &p.tv4, &v_full[sv], 0, 0, hh2[0], gcol0 * (BN / 8), hb[0]);
                         } else {
 #pragma unroll
                             for (int t = 0; t < Geo::kHeads; ++t)
@@ -768,9 +784,14 @@ sf_status attn_tc(const sf_attn_args& a, const sf_bsr_dev& b, cudaStream_t st, b
         if (!(e && *e == '0')) {
             SF_TRY(make_tmap_pair5(&p.tk2, a.k, a.seq_len, a.h, a.bs, a.q_sn, a.q_sh, a.q_sb, b.block_n, bf));
             SF_TRY(make_tmap_pair5(&p.tv2, a.v, a.seq_len, a.h, a.bs, a.q_sn, a.q_sh, a.q_sb, b.block_n, bf));
+            const char* re = std::getenv("SF_ATTN_RUNBOX");
+            if (b.block_n < 64 && !(re && *re == '0')) {  // 64-row boxes for runs of consecutive blocks
+                SF_TRY(make_tmap_pair5(&p.tk4, a.k, a.seq_len, a.h, a.bs, a.q_sn, a.q_sh, a.q_sb, 64, bf));
+                SF_TRY(make_tmap_pair5(&p.tv4, a.v, a.seq_len, a.h, a.bs, a.q_sn, a.q_sh, a.q_sb, 64, bf));
+            }
             // Q of both heads in one box {64, 64, 2, 1}: [head][64 rows][128 B], head t at t * 8 KB
             SF_TRY(make_tmap_4d(&p.tq, a.q, a.seq_len, a.h, a.bs, a.q_sn, a.q_sh, a.q_sb, b.block_m, bf, 2));
-            p.pair5 = 1;
+            p.pair5 = (b.block_n < 64 && !(re && *re == '0')) ? 2 : 1;
         }
     }
     p.n = a.seq_len;
