@@ -96,6 +96,7 @@ struct AttnParams {
     CUtensorMap tk2, tv2;
     CUtensorMap tk4, tv4;  // the same maps with a 64-row box: a step whose column blocks are consecutive
     int32_t pair5;
+    int32_t run64;         // one head (BM 128): tk4 / tv4 are 4-D maps with a 64-row box
     int32_t n, h, bh, n_rows, n_items;  // bh: work units per row block (slices, or head pairs at BM 64)
     int32_t bh_total;                   // b * h slices
     const int32_t* load_row_ptr;
@@ -185,7 +186,7 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
             tc::prefetch_tmap(&p.tk2);
             tc::prefetch_tmap(&p.tv2);
         }
-        if (kPair && p.pair5 == 2) {
+        if ((kPair && p.pair5 == 2) || (!kPair && p.run64)) {
             tc::prefetch_tmap(&p.tk4);
             tc::prefetch_tmap(&p.tv4);
         }
@@ -286,7 +287,7 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
                     // a step over G consecutive column blocks (band interiors) loads each tensor with
                     // ONE 64-row box instead of G: the same bytes land at the same stage addresses
                     const int gcol0 = __shfl_sync(0xffffffffu, gcol, 0);
-                    const bool run = kPair && G > 1 && p.pair5 == 2 &&
+                    const bool run = G > 1 && (kPair ? p.pair5 == 2 : p.run64 != 0) &&
                                      __all_sync(0xffffffffu, lane >= G || gcol == gcol0 + static_cast<int>(lane));
                     const uint32_t ph = ((g / kKS) & 1) ^ 1, phv = ((g / kVS) & 1) ^ 1;
                     if (lane == 0) {
@@ -321,6 +322,8 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
                                             gcol * (BN / 8), hb[0]);
                             else if (gg == 0)
                                 tma_load_5d(sK + st * kKVBytes, &p.tk4, &k_full[st], 0, 0, hh2[0], gcol0 * (BN / 8), hb[0]);
+                        } else if (run) {
+                            if (gg == 0) tma_load_4d(sK + st * kKVBytes, &p.tk4, &k_full[st], 0, gcol0 * BN, hh2[0], hb[0]);
                         } else {
 #pragma unroll
                             for (int t = 0; t < Geo::kHeads; ++t)  // head t's 64 keys at t * 8 KB
@@ -346,6 +349,8 @@ __global__ void __launch_bounds__(kThreads, 2) attn_tc_kernel(const __grid_const
                                             gcol * (BN / 8), hb[0]);
                             else if (gg == 0)
                                 tma_load_5d(sV + sv * kKVBytes, &p.tv4, &v_full[sv], 0, 0, hh2[0], gcol0 * (BN / 8), hb[0]);
+                        } else if (run) {
+                            if (gg == 0) tma_load_4d(sV + sv * kKVBytes, &p.tv4, &v_full[sv], 0, gcol0 * BN, hh2[0], hb[0]);
                         } else {
 #pragma unroll
                             for (int t = 0; t < Geo::kHeads; ++t)
@@ -792,6 +797,14 @@ sf_status attn_tc(const sf_attn_args& a, const sf_bsr_dev& b, cudaStream_t st, b
             // Q of both heads in one box {64, 64, 2, 1}: [head][64 rows][128 B], head t at t * 8 KB
             SF_TRY(make_tmap_4d(&p.tq, a.q, a.seq_len, a.h, a.bs, a.q_sn, a.q_sh, a.q_sb, b.block_m, bf, 2));
             p.pair5 = (b.block_n < 64 && !(re && *re == '0')) ? 2 : 1;
+        }
+    }
+    if (b.block_m == 128 && b.block_n < 64) {  // 64-row boxes for runs of consecutive blocks
+        const char* re = std::getenv("SF_ATTN_RUNBOX");
+        if (!(re && *re == '0')) {
+            SF_TRY(make_tmap_4d(&p.tk4, a.k, a.seq_len, a.h, a.bs, a.q_sn, a.q_sh, a.q_sb, 64, bf));
+            SF_TRY(make_tmap_4d(&p.tv4, a.v, a.seq_len, a.h, a.bs, a.q_sn, a.q_sh, a.q_sb, 64, bf));
+            p.run64 = 1;
         }
     }
     p.n = a.seq_len;
