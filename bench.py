@@ -721,6 +721,32 @@ def main():
         windows.append(w_ms)
     e2e_ms = statistics.median(windows)
 
+    # the box's own PCIe ceiling for this e2e: the same per-step copies (H2D of the input, D2H of the
+    # output, both directions concurrently on the two copy streams) with no compute, same step count
+    cur = torch.cuda.current_stream()
+    torch.cuda.synchronize()
+    c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    c0.record(cur)
+    s_in.wait_stream(cur)
+    s_out.wait_stream(cur)
+    for i in range(e2e_steps):
+        b = i % NB
+        with torch.cuda.stream(s_in):
+            xs[b].copy_(hx, non_blocking=True)
+        if read_back:
+            with torch.cuda.stream(s_out):
+                hy[b].copy_(gath[b] if nccl_gather else Ls[b].out, non_blocking=True)
+    cur.wait_stream(s_in)
+    cur.wait_stream(s_out)
+    c1.record(cur)
+    torch.cuda.synchronize()
+    copy_ms = c0.elapsed_time(c1) / e2e_steps
+    pcie = {"copy_only_ms_per_step": copy_ms,
+            "h2d_gbs": hx.numel() * 2 / (copy_ms / 1e3) / 1e9,
+            "copy_only_tokens_per_s": tokens / (copy_ms / 1e3),
+            "e2e_frac_of_copy_only": copy_ms / e2e_ms,
+            "how": "the e2e's H2D and D2H copies alone, both directions concurrently, measured live on this box"}
+
     # ---- per-kernel breakdown (mean over the timed steps) and roofline of the dominant kernel ----
     parts = {k: v / args.steps for k, v in parts_sum.items()}
     wm, mha_flops = work_model(cfg, nnz)
@@ -761,7 +787,7 @@ def main():
                     "copies": "pinned host buffers, H2D/D2H on copy streams overlapping adjacent steps' compute"
                               + ("; each rank copies its shard in, an NCCL all-gather assembles the full output "
                                  "on every rank, rank 0 reads it back" if nccl_gather else ""),
-                    "pcie_bound": "25.2 MB each way per step at ~49 GB/s per direction concurrently (tools/pcie_bw.py)",
+                    "pcie_bound": pcie,
                     "windows_tokens_per_s": [tokens / (w / 1e3) for w in windows],
                     "window_steps": e2e_steps, "statistic": "median of the windows"},
             "gpu_launches": int(launches), "roofline": roof, "kernels_ms": parts, "mha": mha,

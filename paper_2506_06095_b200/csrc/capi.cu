@@ -325,9 +325,16 @@ extern "C" sf_status sf_time_best(sf_launch_fn fn, void* user, int32_t warmup, i
     if (!fn || !best_ms || reps < 1) return fail(SF_INVALID_PARAMETER, "bad timing arguments");
     cudaStream_t st = as_stream(stream);
     for (int i = 0; i < warmup; ++i) SF_TRY(fn(user, stream));
-    cudaEvent_t e0, e1;
-    SF_CUDA_TRY(cudaEventCreate(&e0));
-    SF_CUDA_TRY(cudaEventCreate(&e1));
+    struct Events {  // destroyed on every return path, error returns included
+        cudaEvent_t e[2] = {nullptr, nullptr};
+        ~Events() {
+            for (cudaEvent_t x : e)
+                if (x) cudaEventDestroy(x);
+        }
+    } ev;
+    SF_CUDA_TRY(cudaEventCreate(&ev.e[0]));
+    SF_CUDA_TRY(cudaEventCreate(&ev.e[1]));
+    cudaEvent_t e0 = ev.e[0], e1 = ev.e[1];
     float best = INFINITY;
     for (int i = 0; i < reps; ++i) {
         SF_CUDA_TRY(cudaEventRecord(e0, st));
@@ -338,8 +345,6 @@ extern "C" sf_status sf_time_best(sf_launch_fn fn, void* user, int32_t warmup, i
         SF_CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
         best = std::min(best, ms);
     }
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
     *best_ms = best;
     return SF_OK;
 }
